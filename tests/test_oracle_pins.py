@@ -1,0 +1,595 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names the passage / closed form it checks.  A plausible mistake in
+the oracle (dropped term, wrong sign or index, transposed operand) must fail one
+of these.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+f32 = np.float32
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- O1 level table
+def test_level_table_cfg0_hand_listed():
+    # BASELINE cfg0: L=8, base 16, growth 2, finest 2048 capped at 128, T=2^12
+    lt = O.level_table(O.ModelConfig())
+    assert [l.res for l in lt] == [16, 32, 64, 128, 128, 128, 128, 128]
+    assert not any(l.dense for l in lt)           # 17^3 = 4913 > 4096
+    assert O.table_entries(O.ModelConfig()) == 32768
+
+
+def test_level_table_cfg1_hand_listed():
+    # BASELINE cfg1: L=16, resolutions 16 -> 512, T=2^16
+    cfg = O.ModelConfig(levels=16, log2_T=16, finest_res=512.0, res_cap=0)
+    lt = O.level_table(cfg)
+    assert [l.res for l in lt] == [16, 20, 25, 32, 40, 50, 64, 80, 101, 128, 161, 203, 256, 322, 406, 512]
+    assert [l.dense for l in lt] == [True] * 4 + [False] * 12      # 33^3 <= 65536 < 41^3
+    assert O.table_entries(cfg) == 17 ** 3 + 21 ** 3 + 26 ** 3 + 33 ** 3 + 12 * 65536 == 854119
+
+
+# ---------------------------------------------------------------- O2 RNG
+def test_splitmix64_published_vectors():
+    vals = [int(l, 16) for l in open(os.path.join(GOLD, "splitmix64_seed0.txt")) if l.strip() and not l.startswith("#")]
+    state = 0
+    for v in vals:
+        state = (state + O.GOLDEN) & ((1 << 64) - 1)
+        assert int(O.mix64(state)) == v
+
+
+def test_rng_unit_range_and_uniformity():
+    u = O.u32_to_unit(O.rng_u32(5, 3, 7, np.arange(200000), 16))
+    assert u.dtype == np.float32 and u.min() >= 0 and u.max() < 1
+    h, _ = np.histogram(u, bins=20, range=(0, 1))
+    chi2 = ((h - 10000.0) ** 2 / 10000.0).sum()
+    assert chi2 < 45          # 19 dof, p ~ 1e-3
+    # streams / rays / steps / objects are decorrelated
+    a = O.rng_u32(5, 3, 7, np.arange(1000), 1)
+    b = O.rng_u32(5, 3, 7, np.arange(1000), 2)
+    c = O.rng_u32(5, 4, 7, np.arange(1000), 1)
+    assert (a != b).mean() > 0.99 and (a != c).mean() > 0.99
+
+
+# ---------------------------------------------------------------- a0 / O3 pixels
+def _kf(x0, y0, w, h, cls_val=1):
+    return O.Keyframe(np.eye(3, 4, dtype=f32), np.array([10, 10, 5, 5], f32), x0, y0, w, h,
+                      np.zeros((h, w, 3), np.uint8), np.full((h, w), cls_val, np.uint8), None)
+
+
+def test_ingest_aabb_and_classes():
+    mask = np.zeros((6, 8), np.uint16)
+    mask[2:5, 3:6] = 7
+    mask[2, 3] = 9      # occluder inside the box
+    mask[4, 5] = 0
+    rgb = np.arange(6 * 8 * 3, dtype=np.uint8).reshape(6, 8, 3)
+    kf = O.ingest_observation(rgb, mask, np.eye(3, 4), [1, 1, 0, 0], 7)
+    assert (kf.x0, kf.y0, kf.w, kf.h) == (3, 2, 3, 3)
+    assert kf.cls[0, 0] == O.CLS_OCCLUDER and kf.cls[2, 2] == O.CLS_BACKGROUND and kf.cls[1, 1] == O.CLS_OBJECT
+    assert np.array_equal(kf.rgb, rgb[2:5, 3:6])
+    with pytest.raises(ValueError):
+        O.ingest_observation(rgb, mask, np.eye(3, 4), [1, 1, 0, 0], 3)
+
+
+def test_pixel_index_bijection_brute_force():
+    kfs = [_kf(0, 0, 3, 2), _kf(5, 1, 2, 4), _kf(2, 2, 1, 1)]
+    total = 6 + 8 + 1
+    k, lx, ly = O.pixel_of_index(kfs, np.arange(total))
+    seen = {(int(a), int(b), int(c)) for a, b, c in zip(k, lx, ly)}
+    every = {(i, x, y) for i, kf in enumerate(kfs) for y in range(kf.h) for x in range(kf.w)}
+    assert seen == every and len(seen) == total
+
+
+def test_pixel_draw_uniform_chi2():
+    kfs = [_kf(0, 0, 3, 2), _kf(5, 1, 2, 4), _kf(2, 2, 1, 1)]
+    R = 150000
+    k, lx, ly = O.draw_pixels(kfs, 1, 2, 3, R)
+    key = k * 100 + ly * 10 + lx
+    _, cnt = np.unique(key, return_counts=True)
+    assert cnt.size == 15
+    e = R / 15
+    assert ((cnt - e) ** 2 / e).sum() < 36     # 14 dof, p ~ 1e-3
+
+
+# ---------------------------------------------------------------- O4 rays
+def test_principal_point_ray():
+    # pixel (cx, cy), identity poses -> direction (0,0,1)
+    K = np.array([100.0, 100.0, 10.5, 20.5], f32)
+    o, d, n = O.make_rays([10], [20], K, np.eye(3, 4, dtype=f32), [0, 0, 0], 0.0)
+    assert np.array_equal(d[0], np.array([0, 0, 1], f32)) and np.array_equal(o[0], np.zeros(3, f32))
+
+
+def test_ray_projection_round_trip():
+    # project o + s d back through the camera -> pixel centre within 1e-4 px
+    g = np.random.default_rng(0)
+    for _ in range(200):
+        ang = g.uniform(-np.pi, np.pi, 3)
+        Rx = np.array([[1, 0, 0], [0, math.cos(ang[0]), -math.sin(ang[0])], [0, math.sin(ang[0]), math.cos(ang[0])]])
+        Rz = np.array([[math.cos(ang[1]), -math.sin(ang[1]), 0], [math.sin(ang[1]), math.cos(ang[1]), 0], [0, 0, 1]])
+        Rwc = Rz @ Rx
+        T = np.concatenate([Rwc, g.uniform(-2, 2, (3, 1))], 1).astype(f32)
+        K = np.array([g.uniform(300, 600), g.uniform(300, 600), 320, 240], f32)
+        bt = g.uniform(-1, 1, 3).astype(f32)
+        yaw = float(g.uniform(-1, 1))
+        px, py = int(g.integers(0, 640)), int(g.integers(0, 480))
+        o, d, _ = O.make_rays([px], [py], K, T, bt, yaw)
+        s = g.uniform(0.5, 5.0)
+        xo = o[0].astype(np.float64) + s * d[0].astype(np.float64)
+        c, sn = math.cos(yaw), math.sin(yaw)
+        xw = np.array([c * xo[0] - sn * xo[1], sn * xo[0] + c * xo[1], xo[2]]) + bt
+        T64 = T.astype(np.float64)
+        xc = T64[:, :3].T @ (xw - T64[:, 3])
+        u = K[0] * xc[0] / xc[2] + K[2]
+        v = K[1] * xc[1] / xc[2] + K[3]
+        assert abs(u - (px + 0.5)) < 1e-3 and abs(v - (py + 0.5)) < 1e-3
+        assert abs(np.linalg.norm(d[0].astype(np.float64)) - 1) < 1e-6
+
+
+# ---------------------------------------------------------------- O5 ray / box
+def test_ray_box_example():
+    tn, tf, hit = O.ray_box([[-5, 0, 0]], [[1, 0, 0]], [1, 1, 1])
+    assert hit[0] and tn[0] == 4 and tf[0] == 6
+
+
+def test_ray_box_parallel_miss_and_inside_origin():
+    tn, tf, hit = O.ray_box([[0, 2, 0], [0, 0.5, 0]], [[1, 0, 0], [1, 0, 0]], [1, 1, 1])
+    assert not hit[0]
+    assert hit[1] and tn[1] == 0 and tf[1] == 1            # origin inside: t_near clamped to 0
+
+
+def test_ray_box_dense_stepping():
+    # interval endpoints agree with a dense ray-marching membership oracle
+    g = np.random.default_rng(1)
+    o = g.uniform(-3, 3, (2000, 3)).astype(f32)
+    d = g.normal(size=(2000, 3))
+    d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(f32)
+    a = np.array([0.7, 0.4, 1.1], f32)
+    tn, tf, hit = O.ray_box(o, d, a)
+    ts = np.linspace(0, 10, 4001)
+    step = ts[1] - ts[0]
+    for i in range(o.shape[0]):
+        p = o[i][None].astype(np.float64) + ts[:, None] * d[i][None].astype(np.float64)
+        inside = np.all(np.abs(p) <= a, axis=1)
+        if not inside.any():
+            assert not hit[i] or tf[i] - tn[i] < 2 * step
+            continue
+        assert hit[i]
+        assert abs(ts[inside][0] - tn[i]) <= step + 1e-5 and abs(ts[inside][-1] - tf[i]) <= step + 1e-5
+
+
+# ---------------------------------------------------------------- O6 samples
+def test_stratified_one_per_stratum_and_mean():
+    N = 32
+    R = 4000
+    tn = np.full(R, 1.0, f32)
+    tf = np.full(R, 3.0, f32)
+    xi = O.u32_to_unit(O.rng_u32(0, 0, 1, np.arange(R)[:, None], 16 + np.arange(N)[None, :]))
+    dist, delta = O.stratified(tn, tf, N, xi)
+    Dl = 2.0 / N
+    k = np.floor((dist - 1.0) / Dl)
+    assert np.array_equal(k, np.broadcast_to(np.arange(N), k.shape))
+    assert np.all(np.diff(dist, axis=1) > 0) and np.all(delta > 0)
+    assert abs(dist.mean() - 2.0) < 0.01 * 2.0
+    d1, _ = O.stratified(tn[:5], tf[:5], 1, xi[:5, :1])
+    assert np.all((d1 >= 1) & (d1 <= 3))
+
+
+# ---------------------------------------------------------------- O7 hash encoding
+def _one_level_cfg(res, log2_T=16):
+    return O.ModelConfig(levels=1, base_res=res, finest_res=float(res), res_cap=0, log2_T=log2_T)
+
+
+def test_encode_reproduces_linear_field_on_dense_level():
+    # trilinear interpolation of a linear vertex field is exact: a wrong axis order,
+    # dense index formula or weight bit fails this.
+    cfg = _one_level_cfg(12)
+    lev = O.level_table(cfg)[0]
+    assert lev.dense
+    n1 = lev.res + 1
+    table = np.zeros((lev.size, 2))
+    for z in range(n1):
+        for y in range(n1):
+            for x in range(n1):
+                table[x + n1 * (y + n1 * z)] = [x + 2.0 * y + 3.0 * z, 5.0 * x - y + 0.5 * z]
+    g = np.random.default_rng(0)
+    u = g.uniform(0, 1, (500, 3)).astype(f32)
+    feat, idx, w = O.hash_encode(u, table, cfg)
+    pos = u.astype(np.float64) * lev.res
+    exp = np.stack([pos[:, 0] + 2 * pos[:, 1] + 3 * pos[:, 2], 5 * pos[:, 0] - pos[:, 1] + 0.5 * pos[:, 2]], 1)
+    assert np.allclose(feat, exp, rtol=0, atol=1e-5)
+
+
+def test_encode_vertex_centre_weights_sum():
+    cfg = O.ModelConfig(levels=4, log2_T=10, base_res=4, finest_res=32.0, res_cap=0)
+    g = np.random.default_rng(2)
+    table = g.normal(size=(O.table_entries(cfg), 2))
+    lt = O.level_table(cfg)
+    u = g.uniform(0, 1, (300, 3)).astype(f32)
+    feat, idx, w = O.hash_encode(u, table, cfg)
+    assert np.allclose(w.sum(axis=2), 1.0, atol=1e-12)                       # north_star
+    for l, lev in enumerate(lt):
+        one = O.ModelConfig(levels=1, log2_T=10, base_res=lev.res, finest_res=float(lev.res), res_cap=0)
+        sub = table[lev.offset:lev.offset + lev.size]
+        v = np.array([[3, 1, 2]]) / lev.res                                   # exact vertex (3,1,2)
+        fv, iv, _ = O.hash_encode(v.astype(f32), sub, one)
+        e = O.corner_index(lev, 3, 1, 2, 1 << 10)
+        assert np.allclose(fv[0], sub[e])
+        ctr = (np.array([[3, 1, 2]]) + 0.5) / lev.res
+        fc, ic, _ = O.hash_encode(ctr.astype(f32), sub, one)
+        assert np.allclose(fc[0], sub[ic[0, 0]].mean(axis=0))
+
+
+def test_dense_level_index_bijection():
+    for res in (3, 7, 12):
+        lev = O.Level(res, True, (res + 1) ** 3, 0)
+        r = np.arange(res + 1)
+        z, y, x = np.meshgrid(r, r, r, indexing="ij")
+        idx = O.corner_index(lev, x.ravel(), y.ravel(), z.ravel(), 1 << 20)
+        assert np.array_equal(np.sort(idx), np.arange((res + 1) ** 3))
+
+
+def test_hash_primes_brute_force():
+    # the 3-prime XOR hash of instant-NGP [21] on python ints
+    lev = O.Level(100, False, 1 << 12, 0)
+    g = np.random.default_rng(3)
+    for _ in range(200):
+        x, y, z = (int(v) for v in g.integers(0, 101, 3))
+        h = ((x * 1) ^ (y * 2654435761) ^ (z * 805459861)) % (1 << 32) % (1 << 12)
+        assert int(O.corner_index(lev, x, y, z, 1 << 12)) == h
+    assert int(O.corner_index(lev, 0, 1, 0, 1 << 12)) == 2654435761 % 4096
+
+
+def test_encode_continuity_across_cells():
+    # SPEC.md:278
+    cfg = O.ModelConfig(levels=3, log2_T=8, base_res=5, finest_res=20.0, res_cap=0)
+    g = np.random.default_rng(4)
+    table = g.normal(size=(O.table_entries(cfg), 2))
+    for lev_res in (5, 10):
+        b = np.float32(3.0 / lev_res)
+        lo = np.nextafter(b, f32(0))
+        hi = np.nextafter(b, f32(1))
+        ua = np.array([[lo, 0.31, 0.77]], f32)
+        ub = np.array([[hi, 0.31, 0.77]], f32)
+        fa, _, _ = O.hash_encode(ua, table, cfg)
+        fb, _, _ = O.hash_encode(ub, table, cfg)
+        assert np.allclose(fa, fb, atol=1e-5)
+
+
+def test_hash_encode_backward_is_adjoint():
+    # <encode(u; table), g> is linear in table: its gradient is encode's adjoint
+    cfg = O.ModelConfig(levels=3, log2_T=6, base_res=2, finest_res=8.0, res_cap=0)
+    g = np.random.default_rng(5)
+    E = O.table_entries(cfg)
+    u = g.uniform(0, 1, (40, 3)).astype(f32)
+    gf = g.normal(size=(40, 6))
+    t1 = g.normal(size=(E, 2))
+    f1, idx, w = O.hash_encode(u, t1, cfg)
+    G = O.hash_encode_backward(gf, idx, w, E, 2)
+    assert abs((f1 * gf).sum() - (G * t1).sum()) < 1e-9
+
+
+# ---------------------------------------------------------------- O8 SH
+def test_sh_orthonormal_quadrature():
+    xg, wg = np.polynomial.legendre.leggauss(24)
+    nphi = 48
+    phi = (np.arange(nphi) + 0.5) * 2 * np.pi / nphi
+    ct, ph = np.meshgrid(xg, phi, indexing="ij")
+    st = np.sqrt(1 - ct ** 2)
+    d = np.stack([st * np.cos(ph), st * np.sin(ph), ct], -1).reshape(-1, 3)
+    wt = (wg[:, None] * np.full(nphi, 2 * np.pi / nphi)[None, :]).reshape(-1)
+    Y = O.sh4(d)
+    G = (Y * wt[:, None]).T @ Y
+    assert np.allclose(G, np.eye(16), atol=1e-10)
+
+
+def test_sh_addition_theorem():
+    g = np.random.default_rng(6)
+    d = g.normal(size=(100, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    Y = O.sh4(d)
+    band = [0, 1, 1, 1, 2, 2, 2, 2, 2, 3, 3, 3, 3, 3, 3, 3]
+    for l in range(4):
+        s = (Y[:, [i for i in range(16) if band[i] == l]] ** 2).sum(axis=1)
+        assert np.allclose(s, (2 * l + 1) / (4 * np.pi))
+
+
+# ---------------------------------------------------------------- O9 MLP
+def test_mlp_zero_model_constant():
+    # SPEC.md:253 with bias-free layers (R4): raw=0 -> sigma=exp(0)=1, c=0.5
+    cfg = O.ModelConfig()
+    W = [np.zeros(s) for s in O.mlp_shapes(cfg)]
+    g = np.random.default_rng(0)
+    fw = O.mlp_forward(g.normal(size=(10, 16)), O.sh4(g.normal(size=(10, 3))), W, cfg)
+    assert np.allclose(fw["sigma"], 1.0) and np.allclose(fw["rgb"], 0.5)
+    cfg2 = O.ModelConfig(density_act=1)
+    fw2 = O.mlp_forward(g.normal(size=(10, 16)), O.sh4(g.normal(size=(10, 3))), W, cfg2)
+    assert np.allclose(fw2["sigma"], math.log(2.0))
+
+
+def test_mlp_selection_weights():
+    # W1 picks feature 0, W2 passes hidden unit 0 to raw0: sigma = exp(relu(f0));
+    # colour net: only raw0 -> hidden0 -> hidden0 -> red: c_r = sigmoid(relu(relu(relu(f0))))
+    cfg = O.ModelConfig()
+    W = [np.zeros(s) for s in O.mlp_shapes(cfg)]
+    W[0][0, 0] = 1
+    W[1][0, 0] = 1
+    W[2][0, 0] = 1
+    W[3][0, 0] = 1
+    W[4][0, 0] = 1
+    f = np.zeros((3, 16))
+    f[:, 0] = [-0.5, 0.3, 1.2]
+    fw = O.mlp_forward(f, np.zeros((3, 16)), W, cfg)
+    r = np.maximum(f[:, 0], 0)
+    assert np.allclose(fw["sigma"], np.exp(r))
+    assert np.allclose(fw["rgb"][:, 0], 1 / (1 + np.exp(-r))) and np.allclose(fw["rgb"][:, 1:], 0.5)
+
+
+# ---------------------------------------------------------------- O10 render
+def test_render_special_cases():
+    d = np.array([[1.0, 2.0]])
+    z = np.zeros((1, 3))
+    vr = O.volume_render(np.zeros((1, 2)), np.ones((1, 2, 3)), d, np.ones((1, 2)), z)
+    assert np.all(vr["w"] == 0) and np.all(vr["C"] == 0) and vr["D"][0] == 0
+    c = np.array([[[0.2, 0.4, 0.6], [0.9, 0.9, 0.9]]])
+    vr = O.volume_render(np.array([[50.0, 1.0]]), c, d, np.ones((1, 2)), z)
+    assert abs(vr["w"][0, 0] - 1) < 1e-9 and np.allclose(vr["C"][0], c[0, 0], atol=1e-9)
+    assert abs(vr["D"][0] - 1.0) < 1e-9
+    vr = O.volume_render(np.array([[math.log(2), math.log(2)]]), c, d, np.ones((1, 2)), z)
+    assert np.allclose(1 - vr["alpha"][0], [0.5, 0.5]) and np.allclose(vr["w"][0], [0.5, 0.25])
+
+
+def test_render_constant_density_closed_form():
+    # north_star: constant sigma with midpoint samples -> A = 1 - exp(-sigma L)
+    for sig, L, N in [(0.7, 1.3, 32), (5.0, 0.4, 64), (0.01, 2.0, 7)]:
+        dist, delta = O.midpoints(np.array([0.5], f32), np.array([0.5 + L], f32), N)
+        vr = O.volume_render(np.full((1, N), sig), np.zeros((1, N, 3)), dist, delta, np.zeros((1, 3)))
+        Lf = float(delta[0, 0]) * N
+        assert abs(vr["A"][0] - (1 - math.exp(-sig * Lf))) < 1e-12
+        assert abs(Lf - L) < 1e-5
+
+
+def test_render_weight_identity_and_monotonicity():
+    g = np.random.default_rng(7)
+    s = g.uniform(0, 3, (50, 16))
+    dl = g.uniform(0.01, 0.2, (50, 16))
+    dist = np.cumsum(dl, axis=1)
+    c = g.uniform(0, 1, (50, 16, 3))
+    vr = O.volume_render(s, c, dist, dl, np.zeros((50, 3)))
+    assert np.allclose(vr["A"], 1 - np.prod(np.exp(-s * dl), axis=1))
+    assert np.all(vr["C"] <= 1 + 1e-12) and np.all(vr["C"] >= 0)
+    s2 = s.copy()
+    s2[:, 0] += 1.0
+    vr2 = O.volume_render(s2, c, dist, dl, np.zeros((50, 3)))
+    assert np.all(vr2["w"][:, 1:] <= vr["w"][:, 1:] + 1e-15)
+
+
+def test_render_backward_finite_differences():
+    g = np.random.default_rng(8)
+    R, N = 5, 9
+    s = g.uniform(0.1, 3, (R, N))
+    dl = g.uniform(0.05, 0.3, (R, N))
+    dist = np.cumsum(dl, axis=1)
+    c = g.uniform(0, 1, (R, N, 3))
+    bg = g.uniform(0, 1, (R, 3))
+    gC = g.normal(size=(R, 3))
+    gD = g.normal(size=R)
+
+    def f(s_, c_):
+        vr = O.volume_render(s_, c_, dist, dl, bg)
+        return (vr["C"] * gC).sum() + (vr["D"] * gD).sum()
+    vr = O.volume_render(s, c, dist, dl, bg)
+    ds, dc = O.volume_render_backward(vr, gC, gD, c, dist, dl, bg)
+    h = 1e-6
+    for r in range(R):
+        for i in range(N):
+            sp, sm = s.copy(), s.copy()
+            sp[r, i] += h
+            sm[r, i] -= h
+            assert abs((f(sp, c) - f(sm, c)) / (2 * h) - ds[r, i]) < 1e-7
+            cp, cm = c.copy(), c.copy()
+            cp[r, i, 1] += h
+            cm[r, i, 1] -= h
+            assert abs((f(s, cp) - f(s, cm)) / (2 * h) - dc[r, i, 1]) < 1e-7
+
+
+# ---------------------------------------------------------------- O11 losses
+def test_loss_examples():
+    cfg = O.ModelConfig()
+    cls = np.array([1])
+    C = np.array([[0.8, 0.5, 0.9]])
+    tgt = C - np.array([[0.3, 0.0, 0.4]])
+    Ls, gC, gD = O.losses_and_render_grads(cls, np.array([True]), np.array([False]), C, np.zeros(1), tgt,
+                                           np.zeros((1, 3)), np.zeros(1), np.zeros(1), 1.0, cfg)
+    assert abs(Ls["l_rgb"] - 0.5) < 1e-12 and abs(Ls["l_total"] - 0.5) < 1e-12
+    assert np.allclose(gC[0], [0.6, 0.0, 0.8])
+    Ls, gC, gD = O.losses_and_render_grads(cls, np.array([True]), np.array([False]), C, np.zeros(1), C,
+                                           np.zeros((1, 3)), np.zeros(1), np.zeros(1), 1.0, cfg)
+    assert Ls["l_total"] == 0 and np.all(gC == 0)
+    # composed example with both lambdas: 1 object ray with depth, 1 bg ray
+    cls = np.array([1, 0])
+    C = np.array([[0.5, 0.5, 0.5], [0.2, 0.2, 0.2]])
+    tgt = np.array([[0.5, 0.5, 0.8], [0.0, 0.0, 0.0]])
+    bg = np.array([[0, 0, 0], [0.2, 0.6, 0.2]])
+    Ls, _, gD = O.losses_and_render_grads(cls, np.array([True, True]), np.array([True, False]), C,
+                                          np.array([2.0, 0.0]), tgt, bg, np.array([1.5, 0.0]),
+                                          np.array([0.0, 30.0]), 4.0, cfg)
+    assert abs(Ls["l_rgb"] - 0.3 / 4) < 1e-12 and abs(Ls["l_rr"] - 0.4 / 4) < 1e-12
+    assert abs(Ls["l_depth"] - 0.5 / 4) < 1e-12 and abs(Ls["l_density"] - 30 / 4) < 1e-12
+    assert abs(Ls["l_total"] - (0.3 / 4 + 0.4 / 4 + 0.5 * 0.5 / 4 + 0.01 * 30 / 4)) < 1e-12
+    assert abs(gD[0] - 0.5 / 4) < 1e-12 and gD[1] == 0
+
+
+# ---------------------------------------------------------------- whole-step pins
+def _small_state(cfg, seed=0, n_kf=3, occluders=False, depth=False):
+    import scenes
+    sc = scenes.sphere_scene(seed, n_views=n_kf, size=32, f=32.0, depth_per_view=6 if depth else 0)
+    P = O.init_params(cfg, seed)
+    P["table"] = np.random.default_rng(seed + 11).uniform(-0.5, 0.5, P["table"].shape)
+    st = O.ObjectState(cfg, sc.objects[0].t, 0.0, sc.objects[0].a, 3, P)
+    for fr in sc.frames:
+        m = fr.mask.copy()
+        if occluders:
+            m[: m.shape[0] // 2, : m.shape[1] // 2][m[: m.shape[0] // 2, : m.shape[1] // 2] == 1] = 5
+        st.kfs.append(O.ingest_observation(fr.rgb, m, fr.T_wc, fr.K, 1, fr.depth.get(1)))
+    return st
+
+
+def test_occluder_exclusion_bitwise():
+    # perturbing occluder-ray target colours changes no loss and no gradient
+    cfg = O.ModelConfig(rays_per_iter=128, samples_per_ray=8)
+    st = _small_state(cfg, occluders=True)
+    assert any((k.cls == O.CLS_OCCLUDER).any() for k in st.kfs)
+    L1, g1, _ = O.loss_and_grads(st, 1)
+    for k in st.kfs:
+        k.rgb[k.cls == O.CLS_OCCLUDER] = 255 - k.rgb[k.cls == O.CLS_OCCLUDER]
+    L2, g2, _ = O.loss_and_grads(st, 1)
+    assert L1 == L2 and np.array_equal(g1["table"], g2["table"])
+    assert all(np.array_equal(a, b) for a, b in zip(g1["W"], g2["W"]))
+
+
+def test_background_only_batch():
+    # SPEC.md:427
+    cfg = O.ModelConfig(rays_per_iter=64, samples_per_ray=8)
+    st = _small_state(cfg)
+    for k in st.kfs:
+        k.cls[:] = O.CLS_BACKGROUND
+    L, _, _ = O.loss_and_grads(st, 1)
+    assert L["l_rgb"] == 0 and L["l_depth"] == 0 and L["l_density"] > 0 and L["l_rr"] > 0
+
+
+def test_decomposition_identity():
+    # SPEC.md:449
+    cfg = O.ModelConfig(rays_per_iter=64, samples_per_ray=8)
+    st = _small_state(cfg, depth=True)
+    L, _, _ = O.loss_and_grads(st, 2)
+    assert abs(L["l_total"] - (L["l_rgb"] + L["l_rr"] + 0.5 * L["l_depth"] + 0.01 * L["l_density"])) <= 1e-12 * abs(L["l_total"])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_full_step_gradient_central_differences(seed):
+    # O12: analytic gradients of the whole step vs central differences in fp64,
+    # tiny grid (L=2, T=2^6, N_min=2) and tiny nets
+    cfg = O.ModelConfig(levels=2, log2_T=6, base_res=2, finest_res=4.0, res_cap=0, width=4, density_out=3,
+                        rays_per_iter=24, samples_per_ray=6, seed=seed)
+    st = _small_state(cfg, seed=seed, occluders=(seed % 2 == 1), depth=True)
+    g = np.random.default_rng(100 + seed)
+    st.params["W"] = [g.normal(0, 0.8, w.shape) for w in st.params["W"]]
+    rays = O.forward_rays(st, 1)
+    L0, grads, _ = O.loss_and_grads(st, 1, rays=rays)
+
+    def loss_at(P):
+        return O.loss_and_grads(st, 1, params=P, rays=rays)[0]["l_total"]
+    h = 1e-6
+    checked = 0
+    cand = [("table", i, j) for i in np.nonzero(np.abs(grads["table"]).sum(1) > 0)[0] for j in range(2)]
+    cand = [cand[i] for i in g.permutation(len(cand))[:12]]
+    for li, w in enumerate(st.params["W"]):
+        for _ in range(3):
+            cand.append(("W", li, tuple(int(g.integers(0, s)) for s in w.shape)))
+    for kind, a, b in cand:
+        Pp = {"table": st.params["table"].copy(), "W": [w.copy() for w in st.params["W"]]}
+        Pm = {"table": st.params["table"].copy(), "W": [w.copy() for w in st.params["W"]]}
+        if kind == "table":
+            Pp["table"][a, b] += h
+            Pm["table"][a, b] -= h
+            an = grads["table"][a, b]
+        else:
+            Pp["W"][a][b] += h
+            Pm["W"][a][b] -= h
+            an = grads["W"][a][b]
+        fd = (loss_at(Pp) - loss_at(Pm)) / (2 * h)
+        assert abs(fd - an) <= 1e-5 * max(1.0, abs(an)) + 1e-7, (kind, a, b, fd, an)
+        checked += 1
+    assert checked >= 20
+
+
+# ---------------------------------------------------------------- O14 Adam
+def test_adam_closed_form_constant_gradient():
+    # constant g from zero moments: m_hat = g, v_hat = g^2 exactly -> each step moves lr*g/(|g|+eps)
+    cfg = O.ModelConfig()
+    p = np.array([1.0, -2.0, 0.5])
+    g = np.array([1.0, -0.25, 3.0])
+    m = np.zeros(3)
+    v = np.zeros(3)
+    for t in range(1, 6):
+        O.adam_update(p, g, m, v, t, cfg, sparse=False)
+        assert np.allclose(p, np.array([1.0, -2.0, 0.5]) - t * cfg.lr * g / (np.abs(g) + cfg.eps), rtol=0, atol=1e-12)
+    p1 = np.array([0.0])
+    O.adam_update(p1, np.array([1.0]), np.zeros(1), np.zeros(1), 1, cfg, sparse=False)
+    assert abs(p1[0] + cfg.lr / (1 + cfg.eps)) < 1e-15
+
+
+def test_adam_zero_gradient_and_sparse_locality():
+    cfg = O.ModelConfig()
+    p = np.array([1.0, 2.0, 3.0])
+    m = np.array([0.1, 0.0, 0.2])
+    v = np.array([0.01, 0.0, 0.04])
+    p0, m0, v0 = p.copy(), m.copy(), v.copy()
+    O.adam_update(p, np.array([0.0, 0.5, 0.0]), m, v, 3, cfg, sparse=True)
+    assert p[0] == p0[0] and p[2] == p0[2] and m[0] == m0[0] and v[2] == v0[2]
+    assert p[1] != p0[1]
+    q = np.array([1.0, 2.0])
+    O.adam_update(q, np.zeros(2), np.zeros(2), np.zeros(2), 1, cfg, sparse=False)
+    assert np.array_equal(q, [1.0, 2.0])
+
+
+def test_train_iteration_untouched_entries_bit_identical():
+    cfg = O.ModelConfig(rays_per_iter=64, samples_per_ray=8)
+    st = _small_state(cfg)
+    p0 = st.params["table"].copy()
+    L, g, _ = O.train_iteration(st)
+    untouched = g["table"] == 0
+    assert untouched.any() and np.array_equal(st.params["table"][untouched], p0[untouched])
+    assert np.all(st.m["table"][untouched] == 0)
+
+
+# ---------------------------------------------------------------- O15 inference
+def _constant_density_params(cfg, raw0):
+    # table of ones -> feat = ones (sum of weights = 1); W1 row 0 = raw0/LF; W2[0,0]=1
+    P = {"table": np.ones((O.table_entries(cfg), cfg.feats)), "W": [np.zeros(s) for s in O.mlp_shapes(cfg)]}
+    lf = cfg.levels * cfg.feats
+    P["W"][0][0, :] = raw0 / lf
+    P["W"][1][0, 0] = 1.0
+    return P
+
+
+def test_render_and_query_constant_density():
+    cfg = O.ModelConfig(levels=2, log2_T=8, base_res=4, finest_res=8.0, res_cap=0)
+    P = _constant_density_params(cfg, 0.9)
+    sig = math.exp(0.9)
+    a = np.array([0.4, 0.3, 0.2], f32)
+    T = np.concatenate([np.eye(3), [[0.05], [0.02], [-2.0]]], 1).astype(f32)
+    K = np.array([40, 40, 8, 8], f32)
+    rgb, dep, opa = O.render(cfg, np.zeros(3, f32), 0.0, a, P, T, K, 16, 16, 16)
+    o, d, _ = O.make_rays(np.tile(np.arange(16), 16), np.repeat(np.arange(16), 16), K, T, np.zeros(3), 0.0)
+    tn, tf, hit = O.ray_box(o, d, a)
+    L = np.where(hit, (tf - tn).astype(np.float64), 0.0)
+    assert hit.any() and (~hit).any()
+    assert np.allclose(opa.reshape(-1), np.where(hit, 1 - np.exp(-sig * L), 0.0), atol=1e-6)
+    assert np.allclose(rgb.reshape(-1, 3), 0.5 * opa.reshape(-1, 1), atol=1e-12)
+    q = np.array([[0.0, 0.0, 0.0], [0.39, -0.29, 0.19], [0.41, 0.0, 0.0], [0, 0, -0.21]], f32)
+    s = O.query_density(cfg, a, P, q)
+    assert np.allclose(s, [sig, sig, 0.0, 0.0])
+
+
+def test_render_scene_two_boxes_closed_form():
+    cfg = O.ModelConfig(levels=2, log2_T=8, base_res=4, finest_res=8.0, res_cap=0)
+    P1 = _constant_density_params(cfg, 0.5)
+    P2 = _constant_density_params(cfg, 0.2)
+    a = np.array([0.3, 0.3, 0.3], f32)
+    objs = [(cfg, np.array([0.0, 0.0, 0.0], f32), 0.0, a, P1, 0), (cfg, np.array([0.0, 0.0, 1.0], f32), 0.4, a, P2, 1)]
+    T = np.concatenate([np.eye(3), [[0.0], [0.0], [-2.0]]], 1).astype(f32)
+    K = np.array([60, 60, 6, 6], f32)
+    rgb, dep, opa = O.render_scene(objs, T, K, 12, 12, 32)
+    Ltot = np.zeros(144)
+    for (c, bt, yaw, ba, P, oid) in objs:
+        o, d, _ = O.make_rays(np.tile(np.arange(12), 12), np.repeat(np.arange(12), 12), K, T, bt, yaw)
+        tn, tf, hit = O.ray_box(o, d, ba)
+        sg = math.exp(0.5 if oid == 0 else 0.2)
+        Ltot += np.where(hit, sg * (tf - tn).astype(np.float64), 0.0)
+    assert np.allclose(opa.reshape(-1), 1 - np.exp(-Ltot), atol=1e-6)
