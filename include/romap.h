@@ -1,0 +1,259 @@
+/* romap.h -- C ABI of the B200-native RO-MAP multi-object NeRF training path.
+ *
+ * The library (libromap.so, sm_100a) trains many per-object instant-NGP-style
+ * NeRFs in parallel, as RO-MAP (arXiv 2304.05735) does for every detected
+ * object: "When a new object instance is detected, we initialize a new NeRF
+ * model, which consists of a multi-resolution hash encoding and a single-layer
+ * MLP" (Sec. V); each model is fed keyframes with instance masks
+ * and poses (Sec. V-A "Data"), trained incrementally and in
+ * parallel, and queried for density (marching cubes) and
+ * rendering.  Citations: PAPER.md:<line> of the paper's LaTeX
+ * source; DESIGN.md R<n> = a reading of the paper recorded in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns romap_status; 0 = ROMAP_OK, < 0 = error.  Nothing aborts.
+ *    romap_last_error() returns a thread-local message for the last failure.
+ *  - Validation happens before any device work: a call that fails validation
+ *    has no side effects.  A CUDA failure poisons the context; every later call
+ *    on it returns ROMAP_E_CUDA.
+ *  - The caller owns every input and output buffer.  Inputs are consumed before
+ *    the call returns (the caller may free them immediately).  Host outputs are
+ *    filled before return.  With flags & ROMAP_DEVICE_PTRS the pointers are
+ *    device pointers on the context's device, read/written in stream order on the
+ *    context's stream (the call returns without synchronizing).
+ *  - A context is not thread-safe: one context per device, one process per GPU.
+ *  - Geometry: world frame z-up, metres.  Cameras: OpenCV pinhole (x right, y down,
+ *    z forward), pixel centres at (px+0.5, py+0.5), T_wc = camera->world 3x4
+ *    row-major [R | t] (R8).  Object frame: x_obj = R_z(yaw)^T (x_w - t)
+ *    (roll = pitch = 0), box = [-a, a] (half extents a).
+ */
+#ifndef ROMAP_H
+#define ROMAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)   /* the library is built -fvisibility=hidden */
+#endif
+
+typedef int32_t romap_status;
+#define ROMAP_OK 0
+#define ROMAP_E_INVALID (-1)          /* bad argument / unsupported configuration   */
+#define ROMAP_E_NOT_FOUND (-2)        /* unknown object handle                       */
+#define ROMAP_E_OOM (-3)              /* device allocation failed                    */
+#define ROMAP_E_CUDA (-4)             /* CUDA error; the context is poisoned         */
+#define ROMAP_E_NONFINITE (-5)        /* non-finite loss or gradient this call       */
+#define ROMAP_E_CONFIG_MISMATCH (-6)  /* objects of one train_step differ in config  */
+#define ROMAP_E_STATE (-7)            /* call not valid in this state (no keyframes) */
+
+/* flags */
+#define ROMAP_DEVICE_PTRS 1           /* buffers are device pointers (see above)      */
+
+typedef struct romap_ctx romap_ctx;
+
+/* Object box from the object SLAM (Eqs. 1-4): translation t
+ * (world, m), yaw about +z (rad), half extents a (m).  Final: the library does not
+ * inflate it (R6). */
+typedef struct {
+    float t[3];
+    float yaw;
+    float half_extents[3];
+} romap_box;
+
+typedef struct {
+    float fx, fy, cx, cy;
+    int32_t width, height;
+} romap_intrinsics;
+
+/* One sparse depth observation: continuous pixel coordinates
+ * (u, v) and camera-frame z (m).  It supervises the ray of pixel (floor u, floor v)
+ * if that pixel belongs to the object (R17). */
+typedef struct {
+    float u, v, z;
+} romap_depth_sample;
+
+/* Model / training configuration (BASELINE.json configs; PAPER.md:222 constants).
+ * Supported on the GPU in this version: feats == 2, 1 <= levels <= 16,
+ * width == 64, density_out == 16, color_hidden == 2, dir_enc == 16 (SH degree 4),
+ * samples_per_ray a power of two in [1, 128], precision 0 (fp32) or 1 (mixed). */
+typedef struct {
+    int32_t levels;          /* L hash levels                                    */
+    int32_t feats;           /* F features per level                             */
+    int32_t log2_T;          /* hash table size T = 2^log2_T entries per level   */
+    int32_t base_res;        /* N_min                                            */
+    double finest_res;       /* N_max (growth b = (N_max/N_min)^(1/(L-1)))       */
+    int32_t res_cap;         /* 0 = none, else N_l = min(N_l, res_cap)           */
+    int32_t width;           /* hidden width (64)                  */
+    int32_t density_out;     /* density-net outputs (16)                         */
+    int32_t color_hidden;    /* colour-net hidden layers (2)                     */
+    int32_t dir_enc;         /* 16 = SH degree 4 of the view direction           */
+    int32_t precision;       /* 0 fp32 SIMT path, 1 fp16 tensor-core MLP (mixed) */
+    int32_t density_act;     /* 0 exp(min(raw,15)) (R3), 1 softplus              */
+    int32_t samples_per_ray; /* N                             */
+    int32_t rays_per_iter;   /* rays drawn per object per iteration */
+    float lr, beta1, beta2, eps;          /* Adam (R18)                           */
+    float lambda_depth, lambda_density;   /* lambda_1, lambda_2 (Eq. 11)          */
+    float loss_scale;        /* mixed path static loss scale (power of two)      */
+    int32_t obj_bg;          /* 0: random bg colour composited for R_o too (R14) */
+    uint64_t seed;           /* counter-RNG seed (R13)                           */
+} romap_model_config;
+
+/* Per-object statistics of one train_step call.  Loss terms are those of the
+ * call's LAST iteration (Eqs. 7-11, each divided by the rays drawn, R16); the
+ * counters sum over all iterations of the call; step = Adam step after the call. */
+typedef struct {
+    double l_total, l_rgb, l_rr, l_depth, l_density;
+    int64_t rays, hit_rays, samples;
+    int64_t step;
+} romap_train_stats;
+
+typedef struct {
+    int32_t instance_id;
+    int32_t n_keyframes;
+    int64_t table_entries;   /* sum over levels of E_l                           */
+    int64_t table_params;    /* table_entries * feats                            */
+    int64_t mlp_params;      /* sum of out*in over the 5 layers                  */
+    int64_t total_area;      /* in-box pixels over all keyframes                 */
+    int64_t step;
+    int32_t rays_per_iter;
+    int32_t n_dense_levels;
+} romap_object_info;
+
+/* Parameter blocks for get/set_params (little-endian, row-major):
+ *   TABLE*: fp32 [table_entries][feats], levels back to back (level l starts at the
+ *           sum of E_k for k < l; dense index x+(N+1)(y+(N+1)z), R5)
+ *   MLP*:   fp32 W1[64][L*F], W2[16][64], W3[64][32], W4[64][64], W5[3][64]
+ *           (out x in, bias-free, R1/R4), concatenated in that order
+ *   STEP:   int64 Adam step t */
+#define ROMAP_BLOCK_TABLE 0
+#define ROMAP_BLOCK_MLP 1
+#define ROMAP_BLOCK_GRAD_TABLE 2
+#define ROMAP_BLOCK_GRAD_MLP 3
+#define ROMAP_BLOCK_M_TABLE 4
+#define ROMAP_BLOCK_M_MLP 5
+#define ROMAP_BLOCK_V_TABLE 6
+#define ROMAP_BLOCK_V_MLP 7
+#define ROMAP_BLOCK_STEP 8
+
+/* debug_dump kinds: per ray / per sample data of the object's rays in the LAST
+ * iteration run by train_step / forward_backward (recomputed by the same device
+ * functions as the training kernels, with the parameters as they are now).
+ *   RAYS:     romap_ray_dump[n_rays]
+ *   SAMPLES:  float[n_rays][N][5] = dist, delta, u.x, u.y, u.z
+ *   HASH_IDX: int32[n_rays][N][L][8] absolute table entry per corner
+ *   FEATURES: float[n_rays][N][L*F]
+ *   FIELD:    float[n_rays][N][4] = sigma, r, g, b
+ *   RAY_GRADS:float[n_rays][N][4] = dL/dsigma, dL/dc (r,g,b) (fp32 path only) */
+#define ROMAP_DUMP_RAYS 0
+#define ROMAP_DUMP_SAMPLES 1
+#define ROMAP_DUMP_HASH_IDX 2
+#define ROMAP_DUMP_FEATURES 3
+#define ROMAP_DUMP_FIELD 4
+#define ROMAP_DUMP_RAY_GRADS 5
+
+typedef struct {
+    int32_t kf, px, py, cls;   /* keyframe, pixel, class 0 bg / 1 object / 2 occluder */
+    int32_t hit, has_depth, pad0, pad1;
+    float o[3], d[3];          /* object-frame ray (R8)                            */
+    float t_near, t_far;       /* box segment (R11)                                */
+    float target[3], bg[3];    /* pixel colour, random background colour (R14)     */
+    float depth;               /* target ray distance (R17)                        */
+    float pad2;
+} romap_ray_dump;
+
+typedef void* (*romap_alloc_fn)(size_t bytes, void* user);
+typedef void (*romap_free_fn)(void* ptr, void* user);
+
+/* Create a context on CUDA device `device`, enqueueing on `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  alloc/free: optional
+ * device allocator callbacks (e.g. torch's caching allocator); NULL -> cudaMalloc. */
+romap_status romap_ctx_create(int32_t device, void* cuda_stream, romap_alloc_fn alloc, romap_free_fn free_fn,
+                              void* user, romap_ctx** out);
+romap_status romap_ctx_destroy(romap_ctx* ctx);
+
+/* New NeRF for a newly detected object.  Parameters initialised from
+ * cfg->seed and instance_id (tables U(-1e-4,1e-4), weights Glorot-uniform, R19).
+ * *out_obj receives the object handle, which is also the object id keying the
+ * counter RNG (R13). */
+romap_status romap_create_object(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
+                                 int32_t instance_id, int32_t* out_obj);
+/* Like create_object with an explicit object id (sharded runs keep global ids). */
+romap_status romap_create_object_with_id(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
+                                         int32_t instance_id, int32_t obj_id);
+romap_status romap_destroy_object(romap_ctx* ctx, int32_t obj);
+romap_status romap_get_object_info(romap_ctx* ctx, int32_t obj, romap_object_info* out);
+
+/* Add one keyframe: rgb uint8 [H][W][3], mask uint16 [H][W]
+ * (0 = background, instance_id = this object, other = occluder),
+ * T_wc float[12].  The detection box is the tight AABB of mask == instance_id
+ * (PAPER.md:153); the in-box crop (colour + class byte) and optional sparse depth
+ * are copied to the device.  E_INVALID if the object is not visible in the mask. */
+romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
+                                   const float T_wc[12], const romap_intrinsics* K,
+                                   const romap_depth_sample* depth, int32_t n_depth);
+
+/* Override rays drawn per iteration for one object (BASELINE cfg2 area split). */
+romap_status romap_set_rays_per_iter(romap_ctx* ctx, int32_t obj, int32_t rays);
+
+/* Train all listed objects together for n_iters iterations (PAPER.md:222,
+ * Table 3): per iteration and object: draw rays_per_iter pixels
+ * over its keyframes, sample N points per hit ray, hash-encode, MLP, volume render
+ * (Eq. 6), object-tailored loss (Eqs. 7-11), backward, Adam.  All objects must share
+ * one model configuration (else E_CONFIG_MISMATCH).  out: nullable, n_objs entries.
+ * Returns E_NONFINITE if a loss or gradient was non-finite (parameters are then
+ * unspecified). */
+romap_status romap_train_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs, int32_t n_iters,
+                              romap_train_stats* out);
+
+/* One iteration without the optimizer step: gradients are left in the GRAD blocks,
+ * the Adam step is not advanced (parity / debugging). */
+romap_status romap_forward_backward(romap_ctx* ctx, const int32_t* objs, int32_t n_objs, romap_train_stats* out);
+
+/* Adam step on the gradients currently in the GRAD blocks (t = step + 1; tables
+ * sparse: entries with a zero gradient are untouched, R18); zeroes the gradients. */
+romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs);
+
+/* Render one object from pose T_wc (R12 midpoint samples, composited over black):
+ * rgb float [H][W][3], depth float [H][W] (ray distance), opacity float [H][W];
+ * any output may be NULL. */
+romap_status romap_render(romap_ctx* ctx, int32_t obj, const float T_wc[12], const romap_intrinsics* K,
+                          int32_t samples_per_ray, float* rgb, float* depth, float* opacity, int32_t flags);
+
+/* Render several objects (R20): per ray, intersect every box, sort the hit segments
+ * by t_near, composite each segment's (C, A, D) front to back. */
+romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, const float T_wc[12],
+                                const romap_intrinsics* K, int32_t samples_per_segment, float* rgb, float* depth,
+                                float* opacity, int32_t flags);
+
+/* Density at object-frame points (m) for marching cubes:
+ * xyz float [n][3] -> sigma float [n]; 0 outside the box (R21). */
+romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, int64_t n, float* sigma,
+                                 int32_t flags);
+
+/* Copy a parameter block (see ROMAP_BLOCK_*) to / from a host buffer of exactly the
+ * block's size in bytes. */
+romap_status romap_get_params(romap_ctx* ctx, int32_t obj, int32_t block, void* buf, int64_t bytes);
+romap_status romap_set_params(romap_ctx* ctx, int32_t obj, int32_t block, const void* buf, int64_t bytes);
+/* Size in bytes of a block or dump (bytes == required size). */
+romap_status romap_block_bytes(romap_ctx* ctx, int32_t obj, int32_t block, int64_t* bytes);
+romap_status romap_dump_bytes(romap_ctx* ctx, int32_t obj, int32_t what, int64_t* bytes);
+romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* buf, int64_t bytes);
+
+/* Wait for all work on the context's stream. */
+romap_status romap_sync(romap_ctx* ctx);
+/* Thread-local message of the last failing call (valid until the next call). */
+const char* romap_last_error(void);
+/* Library version string. */
+const char* romap_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROMAP_H */

@@ -1,0 +1,120 @@
+// k_sample.cu -- step a1 of the hot path: ray generation, classification,
+// ray/box segment ("transform the camera pose to the object
+// coordinate system and back-project the pixels that are within the object's
+// detection box.  If the ray intersects with the 3D bounding box, we compute the
+// truncation distance"), batched over all objects of a launch with a segmented
+// ray layout (one global ray slot per drawn ray; objects own contiguous ranges).
+//
+// Thread per ray slot.  All geometry is bit-exact fp32 (romap_internal.cuh).
+#include "romap_internal.cuh"
+
+__global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
+                                                int total_slots, RayRec* __restrict__ rays,
+                                                unsigned long long* __restrict__ hit_count) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= total_slots) return;
+    // object owning slot g (objects are sorted by ray_begin)
+    int lo = 0, hi = n_objs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (objs[mid].ray_begin <= g) lo = mid; else hi = mid - 1;
+    }
+    const ObjDev& ob = objs[lo];
+    int r = g - ob.ray_begin;
+    RayRec rr;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { rr.o[k] = 0.f; rr.d[k] = 0.f; rr.tgt[k] = 0.f; rr.bg[k] = 0.f; }
+    rr.tn = rr.tf = rr.depth = 0.f;
+    rr.flags = 0;
+    rr.slot = lo;
+    rr.kf = rr.px = rr.py = -1;
+    bool active = false;
+    if (r < ob.n_rays) {
+        long long t = *ob.step + 1;                       // the Adam step this iteration feeds (R13)
+        unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, t);
+        // R9: uniform over the union of in-box pixels of all keyframes
+        unsigned u = rng_u32(pre, r, 0);
+        long long idx = (long long)(((unsigned long long)u * (unsigned long long)ob.total_area) >> 32);
+        int klo = 0, khi = ob.n_kf - 1;
+        while (klo < khi) {
+            int mid = (klo + khi + 1) >> 1;
+            if (ob.area_prefix[mid] <= idx) klo = mid; else khi = mid - 1;
+        }
+        const KfDev* kf = ob.kfs + klo;
+        long long local = idx - ob.area_prefix[klo];
+        int w = kf->w;
+        int ly = (int)(local / w), lx = (int)(local - (long long)ly * w);
+        uchar4 pix = kf->crop[(long long)ly * w + lx];
+        int cls = pix.w;
+        rr.tgt[0] = __fdiv_rn((float)pix.x, 255.0f);
+        rr.tgt[1] = __fdiv_rn((float)pix.y, 255.0f);
+        rr.tgt[2] = __fdiv_rn((float)pix.z, 255.0f);
+        int px = kf->x0 + lx, py = kf->y0 + ly;
+        KfDev kcopy = *kf;
+        Ray ray = make_ray(kcopy, px, py, ob);
+        float tn, tf;
+        bool hit = ray_box(ray.o, ray.d, ob.a, tn, tf);
+        active = hit && cls != CLS_OCC;                   // R10: occluders dropped
+        bool has_depth = false;
+        if (kcopy.depth != nullptr && cls == CLS_OBJ) {
+            float z = kcopy.depth[(long long)ly * w + lx];
+            has_depth = z > 0.0f;
+            rr.depth = __fmul_rn(z, ray.n);               // R17: camera z -> ray distance
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            rr.o[k] = ray.o[k];
+            rr.d[k] = ray.d[k];
+            rr.bg[k] = u32_unit(rng_u32(pre, r, 1 + k));  // R14 random background colour
+        }
+        rr.tn = tn;
+        rr.tf = tf;
+        rr.flags = cls | (active ? RF_ACTIVE : 0) | (has_depth ? RF_HAS_DEPTH : 0) | RF_DRAWN;
+        rr.kf = klo;
+        rr.px = px;
+        rr.py = py;
+    }
+    rays[g] = rr;
+    // warp-aggregated hit counter per object slot
+    unsigned m = __ballot_sync(__activemask(), active);
+    if (active) {
+        unsigned same = __match_any_sync(m, lo);
+        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(hit_count + lo, (unsigned long long)__popc(same));
+    }
+}
+
+void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
+                   RayRec* rays, unsigned long long* hit_count) {
+    int blocks = (total_slots + 127) / 128;
+    if (blocks > 0) k_raygen<<<blocks, 128, 0, lc.st>>>(cfg, objs, n_objs, total_slots, rays, hit_count);
+}
+
+// inference rays: every pixel of a W x H image from pose `cam` (R12, R20)
+__global__ void __launch_bounds__(128) k_render_rays(const ObjDev* __restrict__ obj, const KfDev* __restrict__ cam,
+                                                     int W, int H, RayRec* __restrict__ rays) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= W * H) return;
+    int py = g / W, px = g - py * W;
+    KfDev k = *cam;
+    ObjDev ob = *obj;
+    Ray ray = make_ray(k, px, py, ob);
+    float tn, tf;
+    bool hit = ray_box(ray.o, ray.d, ob.a, tn, tf);
+    RayRec rr;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) { rr.o[j] = ray.o[j]; rr.d[j] = ray.d[j]; rr.tgt[j] = 0.f; rr.bg[j] = 0.f; }
+    rr.tn = tn;
+    rr.tf = tf;
+    rr.depth = 0.f;
+    rr.flags = (hit ? RF_ACTIVE : 0) | RF_DRAWN;
+    rr.slot = 0;
+    rr.kf = 0;
+    rr.px = px;
+    rr.py = py;
+    rays[g] = rr;
+}
+
+void launch_render_rays(const LaunchCtx& lc, const ObjDev* obj, const KfDev* cam, int W, int H, RayRec* rays) {
+    int n = W * H;
+    if (n > 0) k_render_rays<<<(n + 127) / 128, 128, 0, lc.st>>>(obj, cam, W, H, rays);
+}

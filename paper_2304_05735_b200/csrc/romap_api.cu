@@ -1,0 +1,988 @@
+// romap_api.cu -- host runtime behind the C ABI (include/romap.h).
+//
+// Owns: the object registry, per-object parameter / gradient / Adam blocks,
+// per-object keyframe crops on the device, the segmented ray layout of a
+// train_step batch, and the launch sequence of one iteration
+// (raygen -> fwd -> render_loss -> bwd -> adam -> step_inc).  Everything is
+// enqueued on the context's stream; the host only crosses the boundary at
+// launch and at the final statistics read-back.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/romap.h"
+#include "romap_internal.cuh"
+
+void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
+                        double* loss_acc, int* nonfinite, float* dbg_ray_grads);
+bool fused_mixed_available();
+
+static thread_local std::string g_err;
+
+static romap_status fail(romap_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+struct Keyframe {
+    KfDev dev;
+    uchar4* crop_d = nullptr;
+    float* depth_d = nullptr;
+    long long area = 0;
+};
+
+struct Object {
+    int id = 0, instance_id = 0;
+    romap_box box{};
+    romap_model_config cfg{};
+    CfgDev cdev{};
+    float c = 1.f, s = 0.f;
+    float* p32 = nullptr;
+    float* g32 = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    __half* p16 = nullptr;
+    long long* step_d = nullptr;
+    std::vector<Keyframe> kfs;
+    KfDev* kfs_d = nullptr;
+    long long* prefix_d = nullptr;
+    size_t kfs_cap = 0;
+    long long total_area = 0;
+    long long step = 0;
+    int rays_per_iter = 0;
+    bool grads_dirty = false;
+    // last batch (debug dumps)
+    int last_ray_begin = -1, last_n_rays = 0;
+};
+
+enum LastCall { LAST_NONE = 0, LAST_TRAIN = 1, LAST_FWDBWD = 2 };
+
+struct romap_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    romap_alloc_fn alloc = nullptr;
+    romap_free_fn free_fn = nullptr;
+    void* user = nullptr;
+    int num_sms = 148;
+    bool poisoned = false;
+    std::map<int, Object*> objs;
+    int next_id = 0;
+    // scratch (grown on demand)
+    RayRec* rays = nullptr;
+    size_t rays_cap = 0;
+    float* samp = nullptr;       // sigma | rgb(3) | dist | delta | dsigma | drgb(3) : 10 floats per sample
+    size_t samp_cap = 0;
+    float* act = nullptr;
+    size_t act_cap = 0;
+    ObjDev* objdev_d = nullptr;
+    size_t objdev_cap = 0;
+    ObjDev* single_d = nullptr;  // render / query object
+    KfDev* cam_d = nullptr;
+    double* loss_d = nullptr;
+    unsigned long long* hits_d = nullptr;
+    int* nonfinite_d = nullptr;
+    size_t stat_cap = 0;
+    float* io_d = nullptr;       // render / query staging
+    size_t io_cap = 0;
+    // last batch
+    std::vector<ObjDev> last_objdev;
+    CfgDev last_cfg{};
+    int last_call = LAST_NONE;
+    int last_total_slots = 0;
+};
+
+// ---------------------------------------------------------------------------
+// memory
+static void* dalloc(romap_ctx* c, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (c->alloc) return c->alloc(bytes, c->user);
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+static void dfree(romap_ctx* c, void* p) {
+    if (!p) return;
+    if (c->free_fn) c->free_fn(p, c->user);
+    else cudaFree(p);
+}
+
+template <class T>
+static bool grow(romap_ctx* c, T*& ptr, size_t& cap, size_t need) {
+    if (need <= cap && ptr) return true;
+    size_t n = need + need / 4 + 64;
+    cudaStreamSynchronize(c->st);
+    dfree(c, ptr);
+    ptr = (T*)dalloc(c, n * sizeof(T));
+    cap = ptr ? n : 0;
+    return ptr != nullptr;
+}
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            ctx->poisoned = true;                                                                 \
+            return fail(ROMAP_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+        }                                                                                         \
+    } while (0)
+
+#define CHECK_CTX()                                                                 \
+    do {                                                                            \
+        if (!ctx) return fail(ROMAP_E_INVALID, "null context");                     \
+        if (ctx->poisoned) return fail(ROMAP_E_CUDA, "context poisoned by an earlier CUDA error"); \
+        cudaSetDevice(ctx->device);                                                 \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// configuration (R5)
+static romap_status build_cfg(const romap_model_config* cfg, CfgDev& cd) {
+    if (!cfg) return fail(ROMAP_E_INVALID, "null config");
+    if (cfg->feats != 2) return fail(ROMAP_E_INVALID, "feats must be 2");
+    if (cfg->levels < 1 || cfg->levels > ROMAP_MAX_LEVELS) return fail(ROMAP_E_INVALID, "levels must be in [1,16]");
+    if (cfg->log2_T < 4 || cfg->log2_T > 24) return fail(ROMAP_E_INVALID, "log2_T must be in [4,24]");
+    if (cfg->base_res < 1 || !(cfg->finest_res >= cfg->base_res)) return fail(ROMAP_E_INVALID, "need finest_res >= base_res >= 1");
+    if (cfg->width != ROMAP_WIDTH || cfg->density_out != ROMAP_DOUT || cfg->color_hidden != 2 || cfg->dir_enc != ROMAP_SH)
+        return fail(ROMAP_E_INVALID, "network must be width 64, density_out 16, color_hidden 2, dir_enc 16");
+    if (cfg->precision != 0 && cfg->precision != 1) return fail(ROMAP_E_INVALID, "precision must be 0 or 1");
+    if (cfg->precision == 1 && !fused_mixed_available()) return fail(ROMAP_E_INVALID, "mixed path not built");
+    if (cfg->density_act != 0 && cfg->density_act != 1) return fail(ROMAP_E_INVALID, "density_act must be 0 or 1");
+    int N = cfg->samples_per_ray;
+    if (N < 1 || N > 128 || (N & (N - 1))) return fail(ROMAP_E_INVALID, "samples_per_ray must be a power of two <= 128");
+    if (cfg->precision == 1 && N < 8) return fail(ROMAP_E_INVALID, "mixed path needs samples_per_ray >= 8");
+    if (cfg->rays_per_iter < 1) return fail(ROMAP_E_INVALID, "rays_per_iter must be >= 1");
+    if (!(cfg->lr > 0) || !(cfg->beta1 >= 0 && cfg->beta1 < 1) || !(cfg->beta2 >= 0 && cfg->beta2 < 1) || !(cfg->eps >= 0))
+        return fail(ROMAP_E_INVALID, "bad Adam hyper-parameters");
+    if (!(cfg->lambda_depth >= 0) || !(cfg->lambda_density >= 0)) return fail(ROMAP_E_INVALID, "lambdas must be >= 0");
+    if (cfg->precision == 1 && !(cfg->loss_scale > 0)) return fail(ROMAP_E_INVALID, "loss_scale must be > 0");
+    memset(&cd, 0, sizeof cd);
+    cd.L = cfg->levels;
+    cd.F = cfg->feats;
+    cd.LF = cd.L * cd.F;
+    cd.log2T = cfg->log2_T;
+    cd.T = 1 << cfg->log2_T;
+    double b = cfg->levels > 1 ? pow(cfg->finest_res / (double)cfg->base_res, 1.0 / (cfg->levels - 1)) : 1.0;
+    long long off = 0;
+    for (int l = 0; l < cd.L; ++l) {
+        long long n = (long long)floor((double)cfg->base_res * pow(b, (double)l) + 1e-6);
+        if (cfg->res_cap > 0 && n > cfg->res_cap) n = cfg->res_cap;
+        if (n > 100000) return fail(ROMAP_E_INVALID, "level resolution too large");
+        long long v = (n + 1) * (n + 1) * (n + 1);
+        bool dense = v <= cd.T;
+        cd.res[l] = (int)n;
+        cd.dense[l] = dense ? 1 : 0;
+        cd.off[l] = (int)off;
+        off += dense ? v : cd.T;
+    }
+    cd.n_entries = (int)off;
+    cd.n_table = (int)(off * cd.F);
+    int w[5] = {ROMAP_WIDTH * cd.LF, ROMAP_DOUT * ROMAP_WIDTH, ROMAP_WIDTH * ROMAP_CIN, ROMAP_WIDTH * ROMAP_WIDTH,
+                3 * ROMAP_WIDTH};
+    int o = 0;
+    for (int k = 0; k < 5; ++k) { cd.w_off[k] = o; o += w[k]; }
+    cd.n_mlp = o;
+    cd.N = N;
+    cd.density_act = cfg->density_act;
+    cd.obj_bg = cfg->obj_bg;
+    cd.lambda_depth = cfg->lambda_depth;
+    cd.lambda_density = cfg->lambda_density;
+    cd.lr = cfg->lr;
+    cd.b1 = cfg->beta1;
+    cd.b2 = cfg->beta2;
+    cd.eps = cfg->eps;
+    cd.loss_scale = cfg->precision == 1 ? cfg->loss_scale : 1.0f;
+    cd.seed = cfg->seed;
+    return ROMAP_OK;
+}
+
+static bool same_model(const romap_model_config& a, const romap_model_config& b) {
+    return a.levels == b.levels && a.feats == b.feats && a.log2_T == b.log2_T && a.base_res == b.base_res &&
+           a.finest_res == b.finest_res && a.res_cap == b.res_cap && a.width == b.width &&
+           a.density_out == b.density_out && a.color_hidden == b.color_hidden && a.dir_enc == b.dir_enc &&
+           a.precision == b.precision && a.density_act == b.density_act && a.samples_per_ray == b.samples_per_ray &&
+           a.lr == b.lr && a.beta1 == b.beta1 && a.beta2 == b.beta2 && a.eps == b.eps &&
+           a.lambda_depth == b.lambda_depth && a.lambda_density == b.lambda_density && a.loss_scale == b.loss_scale &&
+           a.obj_bg == b.obj_bg && a.seed == b.seed;
+}
+
+// host RNG for initialisation (R19); independent of the training RNG streams
+struct HostRng {
+    unsigned long long s;
+    unsigned long long next() { s += ROMAP_GOLDEN; return mix64(s); }
+    double unit() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+static ObjDev make_objdev(const Object* ob) {
+    ObjDev d;
+    memset(&d, 0, sizeof d);
+    for (int k = 0; k < 3; ++k) { d.a[k] = ob->box.half_extents[k]; d.t[k] = ob->box.t[k]; }
+    d.c = ob->c;
+    d.s = ob->s;
+    d.p32 = ob->p32;
+    d.g32 = ob->g32;
+    d.m = ob->m;
+    d.v = ob->v;
+    d.p16 = ob->p16;
+    d.kfs = ob->kfs_d;
+    d.area_prefix = ob->prefix_d;
+    d.n_kf = (int)ob->kfs.size();
+    d.total_area = ob->total_area;
+    d.obj_id = ob->id;
+    d.step = ob->step_d;
+    return d;
+}
+
+static Object* find(romap_ctx* ctx, int id) {
+    auto it = ctx->objs.find(id);
+    return it == ctx->objs.end() ? nullptr : it->second;
+}
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* romap_last_error(void) { return g_err.c_str(); }
+const char* romap_version(void) { return "romap-b200 0.1 (sm_100a)"; }
+
+romap_status romap_ctx_create(int32_t device, void* cuda_stream, romap_alloc_fn alloc, romap_free_fn free_fn,
+                              void* user, romap_ctx** out) {
+    if (!out) return fail(ROMAP_E_INVALID, "null out");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(ROMAP_E_CUDA, "no CUDA device");
+    }
+    if (device < 0 || device >= n) return fail(ROMAP_E_INVALID, "bad device %d", device);
+    if ((alloc == nullptr) != (free_fn == nullptr)) return fail(ROMAP_E_INVALID, "alloc and free must both be set");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(ROMAP_E_CUDA, "cudaSetDevice failed");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(ROMAP_E_CUDA, "cudaGetDeviceProperties failed");
+    if (prop.major != 10) return fail(ROMAP_E_INVALID, "libromap is built for sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
+    romap_ctx* ctx = new romap_ctx();
+    ctx->device = device;
+    ctx->st = (cudaStream_t)cuda_stream;
+    ctx->alloc = alloc;
+    ctx->free_fn = free_fn;
+    ctx->user = user;
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->single_d = (ObjDev*)dalloc(ctx, sizeof(ObjDev));
+    ctx->cam_d = (KfDev*)dalloc(ctx, sizeof(KfDev));
+    if (!ctx->single_d || !ctx->cam_d) {
+        delete ctx;
+        return fail(ROMAP_E_OOM, "context allocation failed");
+    }
+    *out = ctx;
+    return ROMAP_OK;
+}
+
+static void free_object(romap_ctx* ctx, Object* ob) {
+    dfree(ctx, ob->p32);
+    dfree(ctx, ob->g32);
+    dfree(ctx, ob->m);
+    dfree(ctx, ob->v);
+    dfree(ctx, ob->p16);
+    dfree(ctx, ob->step_d);
+    for (auto& k : ob->kfs) { dfree(ctx, k.crop_d); dfree(ctx, k.depth_d); }
+    dfree(ctx, ob->kfs_d);
+    dfree(ctx, ob->prefix_d);
+    delete ob;
+}
+
+romap_status romap_ctx_destroy(romap_ctx* ctx) {
+    if (!ctx) return fail(ROMAP_E_INVALID, "null context");
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->st);
+    for (auto& kv : ctx->objs) free_object(ctx, kv.second);
+    dfree(ctx, ctx->rays);
+    dfree(ctx, ctx->samp);
+    dfree(ctx, ctx->act);
+    dfree(ctx, ctx->objdev_d);
+    dfree(ctx, ctx->single_d);
+    dfree(ctx, ctx->cam_d);
+    dfree(ctx, ctx->loss_d);
+    dfree(ctx, ctx->hits_d);
+    dfree(ctx, ctx->nonfinite_d);
+    dfree(ctx, ctx->io_d);
+    delete ctx;
+    return ROMAP_OK;
+}
+
+static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
+                                int32_t instance_id, int32_t id) {
+    if (!box) return fail(ROMAP_E_INVALID, "null box");
+    for (int k = 0; k < 3; ++k)
+        if (!(box->half_extents[k] > 0) || !std::isfinite(box->half_extents[k]) || !std::isfinite(box->t[k]))
+            return fail(ROMAP_E_INVALID, "box must have finite centre and positive half extents");
+    if (!std::isfinite(box->yaw)) return fail(ROMAP_E_INVALID, "non-finite yaw");
+    if (id < 0) return fail(ROMAP_E_INVALID, "object id must be >= 0");
+    if (find(ctx, id)) return fail(ROMAP_E_INVALID, "object id %d exists", id);
+    CfgDev cd;
+    romap_status st = build_cfg(cfg, cd);
+    if (st) return st;
+    Object* ob = new Object();
+    ob->id = id;
+    ob->instance_id = instance_id;
+    ob->box = *box;
+    ob->cfg = *cfg;
+    ob->cdev = cd;
+    ob->c = (float)cos((double)box->yaw);   // R8: cos/sin in double, rounded
+    ob->s = (float)sin((double)box->yaw);
+    ob->rays_per_iter = cfg->rays_per_iter;
+    size_t n = (size_t)cd.n_table + cd.n_mlp;
+    ob->p32 = (float*)dalloc(ctx, n * 4);
+    ob->g32 = (float*)dalloc(ctx, n * 4);
+    ob->m = (float*)dalloc(ctx, n * 4);
+    ob->v = (float*)dalloc(ctx, n * 4);
+    ob->p16 = (__half*)dalloc(ctx, n * 2 + 16);
+    ob->step_d = (long long*)dalloc(ctx, 8);
+    if (!ob->p32 || !ob->g32 || !ob->m || !ob->v || !ob->p16 || !ob->step_d) {
+        free_object(ctx, ob);
+        return fail(ROMAP_E_OOM, "parameter allocation failed");
+    }
+    // R19 initialisation
+    std::vector<float> host(n);
+    std::vector<__half> h16(n);
+    HostRng rng{cfg->seed ^ mix64(0x5eedULL + (unsigned long long)id)};
+    for (int i = 0; i < cd.n_table; ++i) host[i] = (float)((rng.unit() * 2.0 - 1.0) * 1e-4);
+    int shapes[5][2] = {{ROMAP_WIDTH, cd.LF}, {ROMAP_DOUT, ROMAP_WIDTH}, {ROMAP_WIDTH, ROMAP_CIN},
+                        {ROMAP_WIDTH, ROMAP_WIDTH}, {3, ROMAP_WIDTH}};
+    for (int k = 0; k < 5; ++k) {
+        double lim = sqrt(6.0 / (shapes[k][0] + shapes[k][1]));
+        for (int e = 0; e < shapes[k][0] * shapes[k][1]; ++e)
+            host[cd.n_table + cd.w_off[k] + e] = (float)((rng.unit() * 2.0 - 1.0) * lim);
+    }
+    for (size_t i = 0; i < n; ++i) h16[i] = __float2half_rn(host[i]);
+    cudaError_t e = cudaMemcpyAsync(ob->p32, host.data(), n * 4, cudaMemcpyHostToDevice, ctx->st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ob->p16, h16.data(), n * 2, cudaMemcpyHostToDevice, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ob->g32, 0, n * 4, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ob->m, 0, n * 4, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ob->v, 0, n * 4, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ob->step_d, 0, 8, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    if (e != cudaSuccess) {
+        ctx->poisoned = true;
+        free_object(ctx, ob);
+        return fail(ROMAP_E_CUDA, "create_object: %s", cudaGetErrorString(e));
+    }
+    ctx->objs[id] = ob;
+    if (id >= ctx->next_id) ctx->next_id = id + 1;
+    return ROMAP_OK;
+}
+
+romap_status romap_create_object(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
+                                 int32_t instance_id, int32_t* out_obj) {
+    CHECK_CTX();
+    if (!out_obj) return fail(ROMAP_E_INVALID, "null out_obj");
+    int id = ctx->next_id;
+    romap_status s = create_impl(ctx, box, cfg, instance_id, id);
+    if (s == ROMAP_OK) *out_obj = id;
+    return s;
+}
+
+romap_status romap_create_object_with_id(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
+                                         int32_t instance_id, int32_t obj_id) {
+    CHECK_CTX();
+    return create_impl(ctx, box, cfg, instance_id, obj_id);
+}
+
+romap_status romap_destroy_object(romap_ctx* ctx, int32_t obj) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->objs.erase(obj);
+    free_object(ctx, ob);
+    ctx->last_call = LAST_NONE;
+    return ROMAP_OK;
+}
+
+romap_status romap_get_object_info(romap_ctx* ctx, int32_t obj, romap_object_info* out) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!out) return fail(ROMAP_E_INVALID, "null out");
+    out->instance_id = ob->instance_id;
+    out->n_keyframes = (int)ob->kfs.size();
+    out->table_entries = ob->cdev.n_entries;
+    out->table_params = ob->cdev.n_table;
+    out->mlp_params = ob->cdev.n_mlp;
+    out->total_area = ob->total_area;
+    out->step = ob->step;
+    out->rays_per_iter = ob->rays_per_iter;
+    int nd = 0;
+    for (int l = 0; l < ob->cdev.L; ++l) nd += ob->cdev.dense[l];
+    out->n_dense_levels = nd;
+    return ROMAP_OK;
+}
+
+romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
+                                   const float T_wc[12], const romap_intrinsics* K,
+                                   const romap_depth_sample* depth, int32_t n_depth) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!rgb || !mask || !T_wc || !K) return fail(ROMAP_E_INVALID, "null input");
+    if (K->width < 1 || K->height < 1 || !(K->fx > 0) || !(K->fy > 0))
+        return fail(ROMAP_E_INVALID, "bad intrinsics");
+    if (n_depth < 0 || (n_depth > 0 && !depth)) return fail(ROMAP_E_INVALID, "bad depth samples");
+    for (int k = 0; k < 12; ++k)
+        if (!std::isfinite(T_wc[k])) return fail(ROMAP_E_INVALID, "non-finite pose");
+    const int W = K->width, H = K->height;
+    const uint16_t id = (uint16_t)ob->instance_id;
+    int x0 = W, y0 = H, x1 = -1, y1 = -1;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            if (mask[(size_t)y * W + x] == id) {
+                if (x < x0) x0 = x;
+                if (x > x1) x1 = x;
+                if (y < y0) y0 = y;
+                if (y > y1) y1 = y;
+            }
+    if (x1 < 0) return fail(ROMAP_E_INVALID, "instance %d not visible in the mask", ob->instance_id);
+    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    if (ob->total_area + (long long)w * h >= (1LL << 31)) return fail(ROMAP_E_INVALID, "too many keyframe pixels");
+    std::vector<uchar4> crop((size_t)w * h);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            size_t src = (size_t)(y0 + y) * W + (x0 + x);
+            uint16_t mv = mask[src];
+            unsigned char cls = mv == id ? CLS_OBJ : (mv == 0 ? CLS_BG : CLS_OCC);
+            crop[(size_t)y * w + x] = make_uchar4(rgb[3 * src], rgb[3 * src + 1], rgb[3 * src + 2], cls);
+        }
+    std::vector<float> dep;
+    bool any_depth = false;
+    if (n_depth > 0) {
+        dep.assign((size_t)w * h, 0.f);
+        for (int i = 0; i < n_depth; ++i) {
+            int px = (int)floorf(depth[i].u), py = (int)floorf(depth[i].v);
+            if (px < x0 || px > x1 || py < y0 || py > y1 || !(depth[i].z > 0)) continue;
+            size_t li = (size_t)(py - y0) * w + (px - x0);
+            if (crop[li].w != CLS_OBJ) continue;
+            dep[li] = depth[i].z;
+            any_depth = true;
+        }
+    }
+    Keyframe kf;
+    for (int k = 0; k < 12; ++k) kf.dev.T[k] = T_wc[k];
+    kf.dev.fx = K->fx;
+    kf.dev.fy = K->fy;
+    kf.dev.cx = K->cx;
+    kf.dev.cy = K->cy;
+    kf.dev.x0 = x0;
+    kf.dev.y0 = y0;
+    kf.dev.w = w;
+    kf.dev.h = h;
+    kf.area = (long long)w * h;
+    kf.crop_d = (uchar4*)dalloc(ctx, crop.size() * sizeof(uchar4));
+    if (!kf.crop_d) return fail(ROMAP_E_OOM, "crop allocation failed");
+    if (any_depth) {
+        kf.depth_d = (float*)dalloc(ctx, dep.size() * 4);
+        if (!kf.depth_d) { dfree(ctx, kf.crop_d); return fail(ROMAP_E_OOM, "depth allocation failed"); }
+    }
+    kf.dev.crop = kf.crop_d;
+    kf.dev.depth = kf.depth_d;
+    // descriptor / prefix arrays (re-uploaded whole; grown geometrically)
+    if (ob->kfs.size() + 1 > ob->kfs_cap) {
+        size_t nc = ob->kfs_cap ? ob->kfs_cap * 2 : 16;
+        KfDev* nk = (KfDev*)dalloc(ctx, nc * sizeof(KfDev));
+        long long* np = (long long*)dalloc(ctx, nc * sizeof(long long));
+        if (!nk || !np) {
+            dfree(ctx, nk); dfree(ctx, np); dfree(ctx, kf.crop_d); dfree(ctx, kf.depth_d);
+            return fail(ROMAP_E_OOM, "keyframe table allocation failed");
+        }
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(ctx, ob->kfs_d);
+        dfree(ctx, ob->prefix_d);
+        ob->kfs_d = nk;
+        ob->prefix_d = np;
+        ob->kfs_cap = nc;
+    }
+    CK(cudaMemcpyAsync(kf.crop_d, crop.data(), crop.size() * sizeof(uchar4), cudaMemcpyHostToDevice, ctx->st));
+    if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep.data(), dep.size() * 4, cudaMemcpyHostToDevice, ctx->st));
+    long long prefix = ob->total_area;
+    size_t k = ob->kfs.size();
+    ob->kfs.push_back(kf);
+    ob->total_area += kf.area;
+    CK(cudaMemcpyAsync(ob->kfs_d + k, &ob->kfs[k].dev, sizeof(KfDev), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ob->prefix_d + k, &prefix, sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+romap_status romap_set_rays_per_iter(romap_ctx* ctx, int32_t obj, int32_t rays) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (rays < 1) return fail(ROMAP_E_INVALID, "rays must be >= 1");
+    ob->rays_per_iter = rays;
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one batch of objects: validate, lay out rays, upload descriptors
+struct Batch {
+    std::vector<Object*> obs;
+    std::vector<ObjDev> dev;
+    CfgDev cfg;
+    int total_slots = 0;
+    bool mixed = false;
+};
+
+static romap_status make_batch(romap_ctx* ctx, const int32_t* objs, int32_t n, bool need_kf, Batch& b) {
+    if (!objs || n < 1) return fail(ROMAP_E_INVALID, "empty object list");
+    for (int i = 0; i < n; ++i) {
+        Object* ob = find(ctx, objs[i]);
+        if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", objs[i]);
+        for (int j = 0; j < i; ++j)
+            if (objs[j] == objs[i]) return fail(ROMAP_E_INVALID, "object %d listed twice", objs[i]);
+        if (need_kf && ob->kfs.empty()) return fail(ROMAP_E_STATE, "object %d has no keyframes", objs[i]);
+        if (i > 0 && !same_model(ob->cfg, b.obs[0]->cfg))
+            return fail(ROMAP_E_CONFIG_MISMATCH, "objects %d and %d differ in model configuration", objs[0], objs[i]);
+        b.obs.push_back(ob);
+    }
+    b.cfg = b.obs[0]->cdev;
+    b.mixed = b.obs[0]->cfg.precision == 1;
+    const int N = b.cfg.N;
+    const int align = N >= ROMAP_TILE ? 1 : ROMAP_TILE / N;   // tiles never straddle objects
+    int begin = 0;
+    for (auto* ob : b.obs) {
+        ObjDev d = make_objdev(ob);
+        d.ray_begin = begin;
+        d.n_rays = ob->rays_per_iter;
+        d.n_slots = (ob->rays_per_iter + align - 1) / align * align;
+        begin += d.n_slots;
+        b.dev.push_back(d);
+    }
+    b.total_slots = begin;
+    return ROMAP_OK;
+}
+
+static romap_status upload_batch(romap_ctx* ctx, Batch& b, bool train_scratch) {
+    size_t n = b.dev.size();
+    if (!grow(ctx, ctx->objdev_d, ctx->objdev_cap, n)) return fail(ROMAP_E_OOM, "descriptor allocation failed");
+    if (n > ctx->stat_cap) {
+        cudaStreamSynchronize(ctx->st);
+        dfree(ctx, ctx->loss_d);
+        dfree(ctx, ctx->hits_d);
+        dfree(ctx, ctx->nonfinite_d);
+        size_t c = n + 16;
+        ctx->loss_d = (double*)dalloc(ctx, c * 4 * sizeof(double));
+        ctx->hits_d = (unsigned long long*)dalloc(ctx, c * sizeof(unsigned long long));
+        ctx->nonfinite_d = (int*)dalloc(ctx, sizeof(int) * 4);
+        if (!ctx->loss_d || !ctx->hits_d || !ctx->nonfinite_d) { ctx->stat_cap = 0; return fail(ROMAP_E_OOM, "stat allocation failed"); }
+        ctx->stat_cap = c;
+    }
+    if (train_scratch) {
+        size_t slots = (size_t)b.total_slots;
+        size_t S = slots * b.cfg.N;
+        if (!grow(ctx, ctx->rays, ctx->rays_cap, slots)) return fail(ROMAP_E_OOM, "ray buffer allocation failed");
+        if (!b.mixed) {
+            if (!grow(ctx, ctx->samp, ctx->samp_cap, S * 10)) return fail(ROMAP_E_OOM, "sample buffer allocation failed");
+            size_t rows = (size_t)b.cfg.LF + 3 * ROMAP_WIDTH + ROMAP_DOUT;
+            if (!grow(ctx, ctx->act, ctx->act_cap, S * rows)) return fail(ROMAP_E_OOM, "activation buffer allocation failed");
+        } else {
+            if (!grow(ctx, ctx->samp, ctx->samp_cap, S * 4)) return fail(ROMAP_E_OOM, "sample buffer allocation failed");
+        }
+    }
+    CK(cudaMemcpyAsync(ctx->objdev_d, b.dev.data(), n * sizeof(ObjDev), cudaMemcpyHostToDevice, ctx->st));
+    return ROMAP_OK;
+}
+
+static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool adam, romap_train_stats* out) {
+    const int n = (int)b.dev.size();
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    CK(cudaMemsetAsync(ctx->hits_d, 0, n * sizeof(unsigned long long), ctx->st));
+    CK(cudaMemsetAsync(ctx->nonfinite_d, 0, sizeof(int), ctx->st));
+    bool dirty = false;
+    for (auto* ob : b.obs) dirty |= ob->grads_dirty;
+    if (dirty) launch_zero_grads(lc, b.cfg, ctx->objdev_d, n);
+    const size_t S = (size_t)b.total_slots * b.cfg.N;
+    float* sigma = ctx->samp;
+    float* rgb = sigma + S;
+    float* dist = rgb + 3 * S;
+    float* delta = dist + S;
+    float* dsigma = delta + S;
+    float* drgb = dsigma + S;
+    for (int it = 0; it < n_iters; ++it) {
+        if (it == n_iters - 1) CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
+        launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d);
+        if (b.mixed) {
+            launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, ctx->loss_d, ctx->nonfinite_d,
+                               adam ? nullptr : ctx->samp);
+        } else {
+            launch_fwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, true, false, sigma, rgb, dist, delta,
+                            ctx->act, (long long)S);
+            launch_render_loss(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dist, delta, dsigma,
+                               drgb, ctx->loss_d, ctx->nonfinite_d);
+            launch_bwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dsigma, drgb, ctx->act,
+                            (long long)S);
+        }
+        if (adam) {
+            launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed);
+            launch_step_inc(lc, ctx->objdev_d, n);
+        }
+        CK(cudaGetLastError());
+    }
+    std::vector<double> loss(4 * n);
+    std::vector<unsigned long long> hits(n);
+    int nf = 0;
+    CK(cudaMemcpyAsync(loss.data(), ctx->loss_d, 4 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(hits.data(), ctx->hits_d, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(&nf, ctx->nonfinite_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    for (int i = 0; i < n; ++i) {
+        Object* ob = b.obs[i];
+        if (adam) {
+            ob->step += n_iters;
+            ob->grads_dirty = false;
+        } else {
+            ob->grads_dirty = true;
+        }
+        ob->last_ray_begin = b.dev[i].ray_begin;
+        ob->last_n_rays = b.dev[i].n_rays;
+        if (out) {
+            double B = (double)b.dev[i].n_rays;
+            romap_train_stats& s = out[i];
+            s.l_rgb = loss[4 * i] / B;
+            s.l_rr = loss[4 * i + 1] / B;
+            s.l_depth = loss[4 * i + 2] / B;
+            s.l_density = loss[4 * i + 3] / B;
+            s.l_total = s.l_rgb + s.l_rr + (double)b.cfg.lambda_depth * s.l_depth + (double)b.cfg.lambda_density * s.l_density;
+            s.rays = (long long)b.dev[i].n_rays * n_iters;
+            s.hit_rays = (long long)hits[i];
+            s.samples = (long long)hits[i] * b.cfg.N;
+            s.step = ob->step;
+        }
+    }
+    ctx->last_objdev = b.dev;
+    ctx->last_cfg = b.cfg;
+    ctx->last_call = adam ? LAST_TRAIN : LAST_FWDBWD;
+    ctx->last_total_slots = b.total_slots;
+    if (nf) return fail(ROMAP_E_NONFINITE, "non-finite %s", (nf & 1) ? "loss" : "gradient");
+    return ROMAP_OK;
+}
+
+romap_status romap_train_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs, int32_t n_iters,
+                              romap_train_stats* out) {
+    CHECK_CTX();
+    if (n_iters < 1) return fail(ROMAP_E_INVALID, "n_iters must be >= 1");
+    Batch b;
+    romap_status s = make_batch(ctx, objs, n_objs, true, b);
+    if (s) return s;
+    s = upload_batch(ctx, b, true);
+    if (s) return s;
+    return run_iterations(ctx, b, n_iters, true, out);
+}
+
+romap_status romap_forward_backward(romap_ctx* ctx, const int32_t* objs, int32_t n_objs, romap_train_stats* out) {
+    CHECK_CTX();
+    Batch b;
+    romap_status s = make_batch(ctx, objs, n_objs, true, b);
+    if (s) return s;
+    s = upload_batch(ctx, b, true);
+    if (s) return s;
+    return run_iterations(ctx, b, 1, false, out);
+}
+
+romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs) {
+    CHECK_CTX();
+    Batch b;
+    romap_status s = make_batch(ctx, objs, n_objs, false, b);
+    if (s) return s;
+    s = upload_batch(ctx, b, false);
+    if (s) return s;
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    CK(cudaMemsetAsync(ctx->nonfinite_d, 0, sizeof(int), ctx->st));
+    launch_adam(lc, b.cfg, ctx->objdev_d, (int)b.dev.size(), ctx->nonfinite_d, b.mixed);
+    launch_step_inc(lc, ctx->objdev_d, (int)b.dev.size());
+    CK(cudaGetLastError());
+    int nf = 0;
+    CK(cudaMemcpyAsync(&nf, ctx->nonfinite_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    for (auto* ob : b.obs) { ob->step += 1; ob->grads_dirty = false; }
+    ctx->last_call = LAST_NONE;
+    if (nf) return fail(ROMAP_E_NONFINITE, "non-finite gradient");
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// inference
+static romap_status render_one(romap_ctx* ctx, Object* ob, const float T_wc[12], const romap_intrinsics* K, int N,
+                               float* rgb, float* depth, float* opacity, int flags) {
+    const int W = K->width, H = K->height;
+    const long long HW = (long long)W * H;
+    CfgDev cfg = ob->cdev;
+    cfg.N = N;
+    KfDev cam;
+    memset(&cam, 0, sizeof cam);
+    for (int k = 0; k < 12; ++k) cam.T[k] = T_wc[k];
+    cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
+    cam.w = W; cam.h = H;
+    ObjDev od = make_objdev(ob);
+    CK(cudaMemcpyAsync(ctx->cam_d, &cam, sizeof cam, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->single_d, &od, sizeof od, cudaMemcpyHostToDevice, ctx->st));
+    if (!grow(ctx, ctx->rays, ctx->rays_cap, (size_t)HW)) return fail(ROMAP_E_OOM, "ray buffer");
+    const long long chunk = 1 << 18;
+    const long long S = chunk * N;
+    if (!grow(ctx, ctx->samp, ctx->samp_cap, (size_t)S * 6)) return fail(ROMAP_E_OOM, "sample buffer");
+    bool dev = flags & ROMAP_DEVICE_PTRS;
+    float *o_rgb = rgb, *o_dep = depth, *o_opa = opacity;
+    if (!dev) {
+        if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)HW * 5)) return fail(ROMAP_E_OOM, "output buffer");
+        o_rgb = rgb ? ctx->io_d : nullptr;
+        o_dep = depth ? ctx->io_d + 3 * HW : nullptr;
+        o_opa = opacity ? ctx->io_d + 4 * HW : nullptr;
+    }
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    launch_render_rays(lc, ctx->single_d, ctx->cam_d, W, H, ctx->rays);
+    float* sg = ctx->samp;
+    float* cl = sg + S;
+    float* ds = cl + 3 * S;
+    float* dl = ds + S;
+    for (long long r0 = 0; r0 < HW; r0 += chunk) {
+        int nr = (int)(HW - r0 < chunk ? HW - r0 : chunk);
+        // rays of this chunk all belong to slot 0 (ctx->single_d)
+        launch_fwd_fp32(lc, cfg, ctx->single_d, ctx->rays + r0, nr, false, true, sg, cl, ds, dl, nullptr, 0);
+        launch_composite(lc, N, ctx->rays + r0, nr, sg, cl, ds, dl, o_rgb ? o_rgb + 3 * r0 : nullptr,
+                         o_dep ? o_dep + r0 : nullptr, o_opa ? o_opa + r0 : nullptr);
+    }
+    CK(cudaGetLastError());
+    if (!dev) {
+        if (rgb) CK(cudaMemcpyAsync(rgb, o_rgb, HW * 3 * 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (depth) CK(cudaMemcpyAsync(depth, o_dep, HW * 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (opacity) CK(cudaMemcpyAsync(opacity, o_opa, HW * 4, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+    }
+    return ROMAP_OK;
+}
+
+romap_status romap_render(romap_ctx* ctx, int32_t obj, const float T_wc[12], const romap_intrinsics* K,
+                          int32_t samples_per_ray, float* rgb, float* depth, float* opacity, int32_t flags) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!T_wc || !K || K->width < 1 || K->height < 1 || !(K->fx > 0) || !(K->fy > 0))
+        return fail(ROMAP_E_INVALID, "bad pose / intrinsics");
+    int N = samples_per_ray;
+    if (N < 1 || N > 128) return fail(ROMAP_E_INVALID, "samples_per_ray must be in [1,128]");
+    return render_one(ctx, ob, T_wc, K, N, rgb, depth, opacity, flags);
+}
+
+romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, const float T_wc[12],
+                                const romap_intrinsics* K, int32_t samples_per_segment, float* rgb, float* depth,
+                                float* opacity, int32_t flags) {
+    CHECK_CTX();
+    (void)objs; (void)n; (void)T_wc; (void)K; (void)samples_per_segment; (void)rgb; (void)depth; (void)opacity; (void)flags;
+    return fail(ROMAP_E_INVALID, "render_scene is not implemented in this version");
+}
+
+romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, int64_t n, float* sigma,
+                                 int32_t flags) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (n < 0 || (n > 0 && (!xyz || !sigma))) return fail(ROMAP_E_INVALID, "bad points");
+    if (n == 0) return ROMAP_OK;
+    ObjDev od = make_objdev(ob);
+    CK(cudaMemcpyAsync(ctx->single_d, &od, sizeof od, cudaMemcpyHostToDevice, ctx->st));
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    if (flags & ROMAP_DEVICE_PTRS) {
+        launch_query_density(lc, ob->cdev, ctx->single_d, xyz, n, sigma);
+        CK(cudaGetLastError());
+        return ROMAP_OK;
+    }
+    const long long chunk = 1 << 22;
+    if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)chunk * 4)) return fail(ROMAP_E_OOM, "staging buffer");
+    for (long long p0 = 0; p0 < n; p0 += chunk) {
+        long long m = n - p0 < chunk ? n - p0 : chunk;
+        CK(cudaMemcpyAsync(ctx->io_d, xyz + 3 * p0, m * 12, cudaMemcpyHostToDevice, ctx->st));
+        launch_query_density(lc, ob->cdev, ctx->single_d, ctx->io_d, m, ctx->io_d + 3 * chunk);
+        CK(cudaMemcpyAsync(sigma + p0, ctx->io_d + 3 * chunk, m * 4, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// parameter blocks
+static romap_status block_ptr(Object* ob, int block, void** p, int64_t* bytes) {
+    const CfgDev& c = ob->cdev;
+    int64_t nt = (int64_t)c.n_table * 4, nm = (int64_t)c.n_mlp * 4;
+    switch (block) {
+        case ROMAP_BLOCK_TABLE: *p = ob->p32; *bytes = nt; break;
+        case ROMAP_BLOCK_MLP: *p = ob->p32 + c.n_table; *bytes = nm; break;
+        case ROMAP_BLOCK_GRAD_TABLE: *p = ob->g32; *bytes = nt; break;
+        case ROMAP_BLOCK_GRAD_MLP: *p = ob->g32 + c.n_table; *bytes = nm; break;
+        case ROMAP_BLOCK_M_TABLE: *p = ob->m; *bytes = nt; break;
+        case ROMAP_BLOCK_M_MLP: *p = ob->m + c.n_table; *bytes = nm; break;
+        case ROMAP_BLOCK_V_TABLE: *p = ob->v; *bytes = nt; break;
+        case ROMAP_BLOCK_V_MLP: *p = ob->v + c.n_table; *bytes = nm; break;
+        case ROMAP_BLOCK_STEP: *p = ob->step_d; *bytes = 8; break;
+        default: return fail(ROMAP_E_INVALID, "unknown block %d", block);
+    }
+    return ROMAP_OK;
+}
+
+romap_status romap_block_bytes(romap_ctx* ctx, int32_t obj, int32_t block, int64_t* bytes) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!bytes) return fail(ROMAP_E_INVALID, "null bytes");
+    void* p;
+    return block_ptr(ob, block, &p, bytes);
+}
+
+romap_status romap_get_params(romap_ctx* ctx, int32_t obj, int32_t block, void* buf, int64_t bytes) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    void* p;
+    int64_t nb;
+    romap_status s = block_ptr(ob, block, &p, &nb);
+    if (s) return s;
+    if (!buf || bytes != nb) return fail(ROMAP_E_INVALID, "block %d needs %lld bytes", block, (long long)nb);
+    CK(cudaMemcpyAsync(buf, p, nb, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+__global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ dst, long long n) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = __float2half_rn(src[i]);
+}
+
+romap_status romap_set_params(romap_ctx* ctx, int32_t obj, int32_t block, const void* buf, int64_t bytes) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    void* p;
+    int64_t nb;
+    romap_status s = block_ptr(ob, block, &p, &nb);
+    if (s) return s;
+    if (!buf || bytes != nb) return fail(ROMAP_E_INVALID, "block %d needs %lld bytes", block, (long long)nb);
+    CK(cudaMemcpyAsync(p, buf, nb, cudaMemcpyHostToDevice, ctx->st));
+    if (block == ROMAP_BLOCK_TABLE || block == ROMAP_BLOCK_MLP) {
+        long long n = nb / 4;
+        long long off = (float*)p - ob->p32;
+        k_to_half<<<(unsigned)((n + 255) / 256), 256, 0, ctx->st>>>((const float*)p, ob->p16 + off, n);
+        CK(cudaGetLastError());
+    }
+    if (block == ROMAP_BLOCK_STEP) {
+        ob->step = *(const long long*)buf;
+    }
+    if (block == ROMAP_BLOCK_GRAD_TABLE || block == ROMAP_BLOCK_GRAD_MLP) ob->grads_dirty = false;
+    CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// debug dumps
+static int64_t dump_size(Object* ob, int what) {
+    const CfgDev& c = ob->cdev;
+    int64_t R = ob->last_n_rays, N = c.N;
+    switch (what) {
+        case ROMAP_DUMP_RAYS: return R * (int64_t)sizeof(romap_ray_dump);
+        case ROMAP_DUMP_SAMPLES: return R * N * 5 * 4;
+        case ROMAP_DUMP_HASH_IDX: return R * N * c.L * 8 * 4;
+        case ROMAP_DUMP_FEATURES: return R * N * c.LF * 4;
+        case ROMAP_DUMP_FIELD: return R * N * 4 * 4;
+        case ROMAP_DUMP_RAY_GRADS: return R * N * 4 * 4;
+        default: return -1;
+    }
+}
+
+romap_status romap_dump_bytes(romap_ctx* ctx, int32_t obj, int32_t what, int64_t* bytes) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!bytes) return fail(ROMAP_E_INVALID, "null bytes");
+    int64_t s = dump_size(ob, what);
+    if (s < 0) return fail(ROMAP_E_INVALID, "unknown dump %d", what);
+    *bytes = s;
+    return ROMAP_OK;
+}
+
+romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* buf, int64_t bytes) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    int64_t need = dump_size(ob, what);
+    if (need < 0) return fail(ROMAP_E_INVALID, "unknown dump %d", what);
+    if (ctx->last_call == LAST_NONE || ob->last_ray_begin < 0) return fail(ROMAP_E_STATE, "no iteration to dump");
+    if (!buf || bytes != need) return fail(ROMAP_E_INVALID, "dump %d needs %lld bytes", what, (long long)need);
+    const int R = ob->last_n_rays, begin = ob->last_ray_begin;
+    if (what == ROMAP_DUMP_RAYS) {
+        std::vector<RayRec> rr(R);
+        CK(cudaMemcpyAsync(rr.data(), ctx->rays + begin, R * sizeof(RayRec), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        romap_ray_dump* o = (romap_ray_dump*)buf;
+        for (int i = 0; i < R; ++i) {
+            memset(&o[i], 0, sizeof o[i]);
+            o[i].kf = rr[i].kf; o[i].px = rr[i].px; o[i].py = rr[i].py;
+            o[i].cls = rr[i].flags & RF_CLS_MASK;
+            o[i].hit = (rr[i].flags & RF_ACTIVE) ? 1 : 0;
+            o[i].has_depth = (rr[i].flags & RF_HAS_DEPTH) ? 1 : 0;
+            for (int k = 0; k < 3; ++k) {
+                o[i].o[k] = rr[i].o[k]; o[i].d[k] = rr[i].d[k];
+                o[i].target[k] = rr[i].tgt[k]; o[i].bg[k] = rr[i].bg[k];
+            }
+            o[i].t_near = rr[i].tn; o[i].t_far = rr[i].tf; o[i].depth = rr[i].depth;
+        }
+        return ROMAP_OK;
+    }
+    if (ctx->last_call != LAST_FWDBWD)
+        return fail(ROMAP_E_STATE, "per-sample dumps describe the last forward_backward call");
+    const CfgDev& c = ctx->last_cfg;
+    const size_t S = (size_t)ctx->last_total_slots * c.N;
+    if (what == ROMAP_DUMP_RAY_GRADS) {
+        bool mixed = ob->cfg.precision == 1;
+        const size_t s0 = (size_t)begin * c.N, n = (size_t)R * c.N;
+        std::vector<float> ds(n), dr(3 * n), out(4 * n);
+        if (mixed) {
+            // fused path stores [dsigma, drgb] interleaved per sample
+            CK(cudaMemcpyAsync(out.data(), ctx->samp + 4 * s0, 16 * n, cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+        } else {
+            float* dsigma = ctx->samp + 6 * S;
+            float* drgb = dsigma + S;
+            CK(cudaMemcpyAsync(ds.data(), dsigma + s0, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaMemcpyAsync(dr.data(), drgb + 3 * s0, 12 * n, cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            for (size_t i = 0; i < n; ++i) {
+                out[4 * i] = ds[i];
+                for (int k = 0; k < 3; ++k) out[4 * i + 1 + k] = dr[3 * i + k];
+            }
+        }
+        memcpy(buf, out.data(), 16 * n);
+        return ROMAP_OK;
+    }
+    if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)(need / 4 + 1))) return fail(ROMAP_E_OOM, "staging buffer");
+    // descriptors of the last batch (the step counter has not moved since forward_backward)
+    CK(cudaMemcpyAsync(ctx->objdev_d, ctx->last_objdev.data(), ctx->last_objdev.size() * sizeof(ObjDev),
+                       cudaMemcpyHostToDevice, ctx->st));
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    launch_debug_samples(lc, c, ctx->objdev_d, ctx->rays, begin, R, what, ctx->io_d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(buf, ctx->io_d, need, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+romap_status romap_sync(romap_ctx* ctx) {
+    CHECK_CTX();
+    CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+}  // extern "C"
