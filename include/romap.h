@@ -243,6 +243,24 @@ romap_status romap_block_bytes(romap_ctx* ctx, int32_t obj, int32_t block, int64
 romap_status romap_dump_bytes(romap_ctx* ctx, int32_t obj, int32_t what, int64_t* bytes);
 romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* buf, int64_t bytes);
 
+/* Per-stage device timing of train_step / forward_backward / optimizer_step:
+ * when enabled, the library brackets every kernel it launches with CUDA events
+ * on the context's stream and accumulates the elapsed time per stage.  Launch
+ * counters are always kept.  enable(ctx, 1) also resets the counters. */
+typedef struct {
+    char name[24];
+    int64_t launches;
+    double ms;
+} romap_stage_time;
+romap_status romap_profile_enable(romap_ctx* ctx, int32_t on);
+romap_status romap_profile_read(romap_ctx* ctx, romap_stage_time* out, int32_t max_stages, int32_t* n_stages);
+
+/* Measurement hook (bench.py timing rules): when bytes > 0, train_step writes a
+ * scratch buffer of that size before every iteration so that no iteration starts
+ * with the previous one's working set in L2; the writes are timed as stage
+ * "l2_flush" and are not part of any other stage. 0 disables (default). */
+romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes);
+
 /* Wait for all work on the context's stream. */
 romap_status romap_sync(romap_ctx* ctx);
 /* Thread-local message of the last failing call (valid until the next call). */

@@ -66,6 +66,26 @@ struct Object {
 
 enum LastCall { LAST_NONE = 0, LAST_TRAIN = 1, LAST_FWDBWD = 2 };
 
+enum Stage { ST_RAYGEN = 0, ST_FWD, ST_RENDER_LOSS, ST_BWD, ST_FUSED, ST_ADAM, ST_STEP_INC, ST_ZERO_GRADS, ST_FLUSH,
+             ST_COUNT };
+static const char* kStageNames[ST_COUNT] = {"raygen", "fwd_fp32", "render_loss", "bwd_fp32", "fused_mixed",
+                                             "adam", "step_inc", "zero_grads", "l2_flush"};
+
+// per-stage launch counters and (optional) CUDA-event timing on the ctx stream
+struct Profiler {
+    bool on = false;
+    long long launches[ST_COUNT] = {};
+    double ms[ST_COUNT] = {};
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    cudaEvent_t get() {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+
 struct romap_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -98,7 +118,41 @@ struct romap_ctx {
     CfgDev last_cfg{};
     int last_call = LAST_NONE;
     int last_total_slots = 0;
+    Profiler prof;
+    void* flush_buf = nullptr;
+    size_t flush_bytes = 0;
 };
+
+// bracket one launch: stage_begin returns the start event (or null)
+static cudaEvent_t stage_begin(romap_ctx* ctx, int stage) {
+    ctx->prof.launches[stage]++;
+    if (!ctx->prof.on) return nullptr;
+    cudaEvent_t e = ctx->prof.get();
+    cudaEventRecord(e, ctx->st);
+    return e;
+}
+static void stage_end(romap_ctx* ctx, int stage, cudaEvent_t e0) {
+    if (!e0) return;
+    cudaEvent_t e1 = ctx->prof.get();
+    cudaEventRecord(e1, ctx->st);
+    ctx->prof.pending.push_back({stage, {e0, e1}});
+}
+// after a stream sync: fold pending intervals into the totals
+static void prof_collect(romap_ctx* ctx) {
+    for (auto& p : ctx->prof.pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) ctx->prof.ms[p.first] += ms;
+        ctx->prof.pool.push_back(p.second.first);
+        ctx->prof.pool.push_back(p.second.second);
+    }
+    ctx->prof.pending.clear();
+}
+#define STAGE(stage, launch)                      \
+    do {                                          \
+        cudaEvent_t e0_ = stage_begin(ctx, stage); \
+        launch;                                   \
+        stage_end(ctx, stage, e0_);               \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 // memory
@@ -313,6 +367,9 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->hits_d);
     dfree(ctx, ctx->nonfinite_d);
     dfree(ctx, ctx->io_d);
+    dfree(ctx, ctx->flush_buf);
+    prof_collect(ctx);
+    for (auto e : ctx->prof.pool) cudaEventDestroy(e);
     delete ctx;
     return ROMAP_OK;
 }
@@ -605,7 +662,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     CK(cudaMemsetAsync(ctx->nonfinite_d, 0, sizeof(int), ctx->st));
     bool dirty = false;
     for (auto* ob : b.obs) dirty |= ob->grads_dirty;
-    if (dirty) launch_zero_grads(lc, b.cfg, ctx->objdev_d, n);
+    if (dirty) STAGE(ST_ZERO_GRADS, launch_zero_grads(lc, b.cfg, ctx->objdev_d, n));
     const size_t S = (size_t)b.total_slots * b.cfg.N;
     float* sigma = ctx->samp;
     float* rgb = sigma + S;
@@ -615,21 +672,27 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     float* drgb = dsigma + S;
     for (int it = 0; it < n_iters; ++it) {
         if (it == n_iters - 1) CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
-        launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d);
+        if (ctx->flush_bytes) {
+            cudaEvent_t e0 = ctx->prof.on ? ctx->prof.get() : nullptr;
+            if (e0) cudaEventRecord(e0, ctx->st);
+            CK(cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st));
+            stage_end(ctx, ST_FLUSH, e0);
+        }
+        STAGE(ST_RAYGEN, launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d));
         if (b.mixed) {
-            launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, ctx->loss_d, ctx->nonfinite_d,
-                               adam ? nullptr : ctx->samp);
+            STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, ctx->loss_d,
+                                               ctx->nonfinite_d, adam ? nullptr : ctx->samp));
         } else {
-            launch_fwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, true, false, sigma, rgb, dist, delta,
-                            ctx->act, (long long)S);
-            launch_render_loss(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dist, delta, dsigma,
-                               drgb, ctx->loss_d, ctx->nonfinite_d);
-            launch_bwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dsigma, drgb, ctx->act,
-                            (long long)S);
+            STAGE(ST_FWD, launch_fwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, true, false, sigma, rgb,
+                                          dist, delta, ctx->act, (long long)S));
+            STAGE(ST_RENDER_LOSS, launch_render_loss(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb,
+                                                     dist, delta, dsigma, drgb, ctx->loss_d, ctx->nonfinite_d));
+            STAGE(ST_BWD, launch_bwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dsigma, drgb,
+                                          ctx->act, (long long)S));
         }
         if (adam) {
-            launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed);
-            launch_step_inc(lc, ctx->objdev_d, n);
+            STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed));
+            STAGE(ST_STEP_INC, launch_step_inc(lc, ctx->objdev_d, n));
         }
         CK(cudaGetLastError());
     }
@@ -640,6 +703,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     CK(cudaMemcpyAsync(hits.data(), ctx->hits_d, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaMemcpyAsync(&nf, ctx->nonfinite_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    prof_collect(ctx);
     for (int i = 0; i < n; ++i) {
         Object* ob = b.obs[i];
         if (adam) {
@@ -703,12 +767,13 @@ romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n
     if (s) return s;
     LaunchCtx lc{ctx->st, ctx->num_sms};
     CK(cudaMemsetAsync(ctx->nonfinite_d, 0, sizeof(int), ctx->st));
-    launch_adam(lc, b.cfg, ctx->objdev_d, (int)b.dev.size(), ctx->nonfinite_d, b.mixed);
-    launch_step_inc(lc, ctx->objdev_d, (int)b.dev.size());
+    STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, (int)b.dev.size(), ctx->nonfinite_d, b.mixed));
+    STAGE(ST_STEP_INC, launch_step_inc(lc, ctx->objdev_d, (int)b.dev.size()));
     CK(cudaGetLastError());
     int nf = 0;
     CK(cudaMemcpyAsync(&nf, ctx->nonfinite_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    prof_collect(ctx);
     for (auto* ob : b.obs) { ob->step += 1; ob->grads_dirty = false; }
     ctx->last_call = LAST_NONE;
     if (nf) return fail(ROMAP_E_NONFINITE, "non-finite gradient");
@@ -976,6 +1041,45 @@ romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* b
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(buf, ctx->io_d, need, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    return ROMAP_OK;
+}
+
+romap_status romap_profile_enable(romap_ctx* ctx, int32_t on) {
+    CHECK_CTX();
+    CK(cudaStreamSynchronize(ctx->st));
+    prof_collect(ctx);
+    ctx->prof.on = on != 0;
+    for (int i = 0; i < ST_COUNT; ++i) { ctx->prof.launches[i] = 0; ctx->prof.ms[i] = 0.0; }
+    return ROMAP_OK;
+}
+
+romap_status romap_profile_read(romap_ctx* ctx, romap_stage_time* out, int32_t max_stages, int32_t* n_stages) {
+    CHECK_CTX();
+    if (!n_stages || (max_stages > 0 && !out)) return fail(ROMAP_E_INVALID, "null output");
+    CK(cudaStreamSynchronize(ctx->st));
+    prof_collect(ctx);
+    *n_stages = ST_COUNT;
+    for (int i = 0; i < ST_COUNT && i < max_stages; ++i) {
+        memset(out[i].name, 0, sizeof out[i].name);
+        strncpy(out[i].name, kStageNames[i], sizeof out[i].name - 1);
+        out[i].launches = ctx->prof.launches[i];
+        out[i].ms = ctx->prof.ms[i];
+    }
+    return ROMAP_OK;
+}
+
+romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes) {
+    CHECK_CTX();
+    if (bytes < 0) return fail(ROMAP_E_INVALID, "bytes must be >= 0");
+    CK(cudaStreamSynchronize(ctx->st));
+    dfree(ctx, ctx->flush_buf);
+    ctx->flush_buf = nullptr;
+    ctx->flush_bytes = 0;
+    if (bytes > 0) {
+        ctx->flush_buf = dalloc(ctx, (size_t)bytes);
+        if (!ctx->flush_buf) return fail(ROMAP_E_OOM, "flush buffer");
+        ctx->flush_bytes = (size_t)bytes;
+    }
     return ROMAP_OK;
 }
 

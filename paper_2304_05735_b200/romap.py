@@ -67,6 +67,10 @@ class ObjectInfo(C.Structure):
                 ("step", C.c_int64), ("rays_per_iter", C.c_int32), ("n_dense_levels", C.c_int32)]
 
 
+class StageTime(C.Structure):
+    _fields_ = [("name", C.c_char * 24), ("launches", C.c_int64), ("ms", C.c_double)]
+
+
 RAY_DUMP_DTYPE = np.dtype([("kf", "<i4"), ("px", "<i4"), ("py", "<i4"), ("cls", "<i4"), ("hit", "<i4"),
                            ("has_depth", "<i4"), ("pad0", "<i4"), ("pad1", "<i4"), ("o", "<f4", 3), ("d", "<f4", 3),
                            ("t_near", "<f4"), ("t_far", "<f4"), ("target", "<f4", 3), ("bg", "<f4", 3),
@@ -95,6 +99,9 @@ _SIGS = {
     "romap_dump_bytes": [_P, _I, _I, C.POINTER(C.c_int64)],
     "romap_debug_dump": [_P, _I, _I, _P, C.c_int64],
     "romap_sync": [_P],
+    "romap_profile_enable": [_P, _I],
+    "romap_profile_read": [_P, _P, _I, C.POINTER(_I)],
+    "romap_set_l2_flush": [_P, C.c_int64],
 }
 
 
@@ -293,3 +300,15 @@ class Context:
 
     def sync(self):
         _check(_lib.romap_sync(self._h))
+
+    def set_l2_flush(self, nbytes: int):
+        _check(_lib.romap_set_l2_flush(self._h, int(nbytes)))
+
+    def profile_enable(self, on: bool = True):
+        _check(_lib.romap_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        arr = (StageTime * 16)()
+        n = C.c_int32()
+        _check(_lib.romap_profile_read(self._h, C.cast(arr, C.c_void_p), 16, C.byref(n)))
+        return {arr[i].name.decode(): {"launches": arr[i].launches, "ms": arr[i].ms} for i in range(n.value)}

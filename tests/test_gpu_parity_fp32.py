@@ -146,13 +146,14 @@ def test_adam_on_identical_gradients(ctx, scene0):
     p = ctx.get_params(h, R.BLOCK_TABLE).reshape(-1, 2)
     m = ctx.get_params(h, R.BLOCK_M_TABLE).reshape(-1, 2)
     v = ctx.get_params(h, R.BLOCK_V_TABLE).reshape(-1, 2)
-    assert np.allclose(p, st.params["table"], rtol=1e-6, atol=1e-9)
+    # fp32 Adam: each of the t updates rounds at |p| ~ 0.1 -> absolute error ~ t * ulp(0.1)
+    assert np.allclose(p, st.params["table"], rtol=1e-6, atol=3e-8)
     assert np.allclose(m, st.m["table"], rtol=1e-5, atol=1e-12)
     assert np.allclose(v, st.v["table"], rtol=1e-5, atol=1e-15)
     untouched = (st.m["table"] == 0)
     assert np.all(m[untouched] == 0) and np.all(v[untouched] == 0)
     pm = ctx.get_params(h, R.BLOCK_MLP)
-    assert np.allclose(pm, flat_W(st.params["W"]), rtol=1e-6, atol=1e-9)
+    assert np.allclose(pm, flat_W(st.params["W"]), rtol=1e-6, atol=3e-8)
     assert ctx.get_params(h, R.BLOCK_STEP)[0] == 3
     assert np.all(ctx.get_params(h, R.BLOCK_GRAD_TABLE) == 0)
     ctx.destroy_object(h)
