@@ -566,12 +566,19 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     }
     CK(cudaMemcpyAsync(kf.crop_d, crop.data(), crop.size() * sizeof(uchar4), cudaMemcpyHostToDevice, ctx->st));
     if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep.data(), dep.size() * 4, cudaMemcpyHostToDevice, ctx->st));
-    long long prefix = ob->total_area;
-    size_t k = ob->kfs.size();
     ob->kfs.push_back(kf);
     ob->total_area += kf.area;
-    CK(cudaMemcpyAsync(ob->kfs_d + k, &ob->kfs[k].dev, sizeof(KfDev), cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ob->prefix_d + k, &prefix, sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
+    // descriptor table and exclusive area prefix, uploaded whole (the arrays may have been reallocated)
+    std::vector<KfDev> descs(ob->kfs.size());
+    std::vector<long long> prefix(ob->kfs.size());
+    long long acc = 0;
+    for (size_t i = 0; i < ob->kfs.size(); ++i) {
+        descs[i] = ob->kfs[i].dev;
+        prefix[i] = acc;
+        acc += ob->kfs[i].area;
+    }
+    CK(cudaMemcpyAsync(ob->kfs_d, descs.data(), descs.size() * sizeof(KfDev), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ob->prefix_d, prefix.data(), prefix.size() * sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return ROMAP_OK;
 }

@@ -148,8 +148,10 @@ def test_adam_on_identical_gradients(ctx, scene0):
     v = ctx.get_params(h, R.BLOCK_V_TABLE).reshape(-1, 2)
     # fp32 Adam: each of the t updates rounds at |p| ~ 0.1 -> absolute error ~ t * ulp(0.1)
     assert np.allclose(p, st.params["table"], rtol=1e-6, atol=3e-8)
-    assert np.allclose(m, st.m["table"], rtol=1e-5, atol=1e-12)
-    assert np.allclose(v, st.v["table"], rtol=1e-5, atol=1e-15)
+    for name, a, b in (("m", m, st.m["table"]), ("v", v, st.v["table"])):
+        err = np.abs(a - b) / (np.abs(b) + 1e-30)
+        i = np.unravel_index(err.argmax(), err.shape)
+        assert err.max() < 1e-5, (name, i, a[i], b[i], gt[i])
     untouched = (st.m["table"] == 0)
     assert np.all(m[untouched] == 0) and np.all(v[untouched] == 0)
     pm = ctx.get_params(h, R.BLOCK_MLP)
@@ -185,7 +187,7 @@ def test_cfg0d_dense_levels_and_ragged(ctx, scene0):
 def test_cfg1_shape_fp32_several_tiles(ctx):
     # BASELINE cfg1 grid (L=16, T=2^16, 16->512, N=64) on a small object scene,
     # 301 rays = 151 tiles of 2 rays incl. a ragged tail, with occluders absent
-    sc = scenes.object_scene(1, n_views=4, W=160, H=120, f=131.25, depth_per_view=8)
+    sc = scenes.object_scene(1, n_views=20, W=160, H=120, f=131.25, depth_per_view=8)   # >16 keyframes: table growth
     kw = dict(levels=16, log2_T=16, base_res=16, finest_res=512.0, res_cap=0, samples_per_ray=64,
               rays_per_iter=301, precision=0, seed=1)
     h, st, stats, L, g, dbg = _fwdbwd(ctx, sc, kw)
