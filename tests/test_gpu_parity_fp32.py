@@ -148,8 +148,10 @@ def test_adam_on_identical_gradients(ctx, scene0):
     v = ctx.get_params(h, R.BLOCK_V_TABLE).reshape(-1, 2)
     # fp32 Adam: each of the t updates rounds at |p| ~ 0.1 -> absolute error ~ t * ulp(0.1)
     assert np.allclose(p, st.params["table"], rtol=1e-6, atol=3e-8)
-    for name, a, b in (("m", m, st.m["table"]), ("v", v, st.v["table"])):
-        err = np.abs(a - b) / (np.abs(b) + 1e-30)
+    # fp32 moments: relative 1e-5, with an absolute floor of ~1e-6 of the size of the
+    # terms being summed (m ~ (1-b1)|g| ~ 1e-4, v ~ (1-b2) g^2 ~ 1e-8) for cancellations
+    for name, a, b, floor in (("m", m, st.m["table"], 1e-10), ("v", v, st.v["table"], 1e-14)):
+        err = np.abs(a - b) / (np.abs(b) + floor / 1e-5)
         i = np.unravel_index(err.argmax(), err.shape)
         assert err.max() < 1e-5, (name, i, a[i], b[i], gt[i])
     untouched = (st.m["table"] == 0)

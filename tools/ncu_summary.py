@@ -1,0 +1,86 @@
+"""Summarise an ncu launch list (csv) and an ncu --set full report into
+profiles/<tag>_*.md / .json, and update profiles/ncu_traffic.json (dram bytes
+per launch per stage) that bench.py reads for roofline.traffic."""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+STAGE = {"k_raygen": "raygen", "k_fwd_fp32": "fwd_fp32", "k_render_loss": "render_loss", "k_bwd_fp32": "bwd_fp32",
+         "k_fused_mixed": "fused_mixed", "k_adam": "adam", "k_step_inc": "step_inc", "k_zero_grads": "zero_grads"}
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+           "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+           "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+           "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr = rows[hi]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(list)
+    unit = None
+    for r in rows[hi + 1:]:
+        agg[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
+        unit = r[ui]
+    scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}.get(unit, 1e-3)
+    tot = sum(sum(v) for v in agg.values())
+    return {k: {"n": len(v), "mean_us": sum(v) / len(v) * scale, "share": sum(v) / tot} for k, v in agg.items()}
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")].split("(")[0]}
+        for m in METRICS:
+            if m in hdr:
+                d[m] = r[hdr.index(m)] + " " + units[hdr.index(m)]
+        res.append(d)
+    return res
+
+
+def to_bytes(s):
+    v, u = s.split()
+    v = float(v.replace(",", ""))
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+
+
+def main(tag, launch_csv, rep):
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    L = launches(launch_csv) if launch_csv and os.path.exists(launch_csv) else {}
+    F = full(rep) if rep and os.path.exists(rep) else []
+    md = [f"# ncu summary {tag}", "", "## launch list (ncu --metrics gpu__time_duration.sum, cold-cache, serialised)", "",
+          "| kernel | launches | mean us | share |", "|---|---|---|---|"]
+    for k, v in sorted(L.items(), key=lambda x: -x[1]["share"]):
+        md.append(f"| {k} | {v['n']} | {v['mean_us']:.1f} | {v['share']:.3f} |")
+    md += ["", "## ncu --set full (per captured launch)", ""]
+    traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    for d in F:
+        md.append(f"### {d['kernel']}")
+        for m in METRICS:
+            if m in d:
+                md.append(f"- {m}: {d[m]}")
+        md.append("")
+        if "dram__bytes_read.sum" in d and d["kernel"] in STAGE:
+            traffic[STAGE[d["kernel"]]] = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
+    open(os.path.join(ROOT, "profiles", f"{tag}_ncu.md"), "w").write("\n".join(md) + "\n")
+    json.dump({"launches": L, "full": F}, open(os.path.join(ROOT, "profiles", f"{tag}_ncu.json"), "w"), indent=1)
+    json.dump(traffic, open(traffic_path, "w"), indent=1)
+    print("\n".join(md))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, sys.argv[3] if len(sys.argv) > 3 else None)
