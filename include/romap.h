@@ -261,6 +261,13 @@ romap_status romap_profile_read(romap_ctx* ctx, romap_stage_time* out, int32_t m
  * "l2_flush" and are not part of any other stage. 0 disables (default). */
 romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes);
 
+/* Tensor-core self test (GPU tests only): with the operand layouts of the mixed
+ * path, computes on device 0 out1[128x64] = X[128x32] W[64x32]^T,
+ * out2[128x32] = Dl[128x64] W, out3[64x32] = Dl^T X from fp16 copies of the
+ * inputs (host pointers, row-major fp32). */
+romap_status romap_selftest_mma(const float* X, const float* W, const float* Dl, float* out1, float* out2,
+                                float* out3);
+
 /* Wait for all work on the context's stream. */
 romap_status romap_sync(romap_ctx* ctx);
 /* Thread-local message of the last failing call (valid until the next call). */

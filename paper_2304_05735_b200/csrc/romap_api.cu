@@ -215,6 +215,8 @@ static romap_status build_cfg(const romap_model_config* cfg, CfgDev& cd) {
     int N = cfg->samples_per_ray;
     if (N < 1 || N > 128 || (N & (N - 1))) return fail(ROMAP_E_INVALID, "samples_per_ray must be a power of two <= 128");
     if (cfg->precision == 1 && N < 8) return fail(ROMAP_E_INVALID, "mixed path needs samples_per_ray >= 8");
+    if (cfg->precision == 1 && cfg->levels != 8 && cfg->levels != 16)
+        return fail(ROMAP_E_INVALID, "mixed path needs levels 8 or 16 (L*F = 16 or 32 tensor-core columns)");
     if (cfg->rays_per_iter < 1) return fail(ROMAP_E_INVALID, "rays_per_iter must be >= 1");
     if (!(cfg->lr > 0) || !(cfg->beta1 >= 0 && cfg->beta1 < 1) || !(cfg->beta2 >= 0 && cfg->beta2 < 1) || !(cfg->eps >= 0))
         return fail(ROMAP_E_INVALID, "bad Adam hyper-parameters");

@@ -1,0 +1,129 @@
+// tc_sm100.cuh -- minimal tcgen05 / TMEM / mbarrier helpers (inline PTX, sm_100a).
+//
+// Operand layout used everywhere ("interleaved core-matrix" layout, SWIZZLE_NONE):
+// a fp16 matrix with R rows and C columns (both multiples of 8) is stored as
+// (R/8) x (C/8) blocks of 8x8 elements; block (rb, cb) starts at byte
+// (rb * (C/8) + cb) * 128 and holds its 8 rows of 8 contiguous fp16 (16 B each).
+// The same bytes are a valid UMMA operand in both majors:
+//   K-major  (rows = M|N, cols = K):  LBO = 128 B,            SBO = (C/8)*128 B
+//   MN-major (rows = K,   cols = M|N): LBO = (C/8)*128 B,     SBO = 128 B
+// (canonical forms: K-major ((8,m),(T,2)):((1T,SBO),(1,LBO)); MN-major
+// ((T,1,m),(8,k)):((1,T,SBO),(1T,LBO)), T = 8 fp16 per 16 B).
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// byte offset of element (r, c) in an interleaved R x C fp16 matrix
+__device__ __forceinline__ uint32_t il_offset(int r, int c, int C) {
+    return (uint32_t)((((r >> 3) * (C >> 3) + (c >> 3)) << 7) + ((r & 7) << 4) + ((c & 7) << 1));
+}
+
+// shared-memory matrix descriptor (SWIZZLE_NONE, version 1 for sm_100)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;   // version = 1 (Blackwell)
+    return d;                 // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+}
+
+// descriptor of the K-step `ks` (16 elements of K) of an interleaved matrix
+// used K-major (cols = K): start advances by 2 column blocks
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int C, int ks) {
+    return make_desc(base + (uint32_t)(ks * 2 * 128), 128u, (uint32_t)((C >> 3) * 128));
+}
+// ... used MN-major (rows = K): start advances by 2 row blocks
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int C, int ks) {
+    return make_desc(base + (uint32_t)(ks * 2 * (C >> 3) * 128), (uint32_t)((C >> 3) * 128), 128u);
+}
+
+// instruction descriptor: kind::f16, A/B fp16, D fp32
+__device__ __forceinline__ uint32_t idesc_f16(int M, int N, bool a_mn, bool b_mn) {
+    uint32_t d = 0;
+    d |= 1u << 4;                          // D format F32
+    // A, B format F16 = 0
+    d |= (a_mn ? 1u : 0u) << 15;
+    d |= (b_mn ? 1u : 0u) << 16;
+    d |= (uint32_t)(N >> 3) << 17;
+    d |= (uint32_t)(M >> 4) << 24;
+    return d;
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+        :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// arrive on an mbarrier once all prior tcgen05.mma of this thread completed
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                 :: "r"(smem_u32(mbar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n"
+        :: "r"(smem_u32(mbar)), "r"(phase) : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+// generic-proxy smem writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// TMEM allocation (whole warp)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 :: "r"(smem_u32(dst_smem)), "r"(ncols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(taddr), "r"(ncols) : "memory");
+}
+
+// 32 lanes x 16 columns of 32-bit: thread t of warp w gets lane 32*(w%4)+t
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// TMEM address of (lane_base, col)
+__device__ __forceinline__ uint32_t taddr(uint32_t base, int lane_base, int col) {
+    return base + ((uint32_t)lane_base << 16) + (uint32_t)col;
+}
+
+// store 8 fp16 (16 B) at an interleaved position (row r, column block starting at c)
+__device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, int C, const float* v8) {
+    __half2 h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v8[2 * i], v8[2 * i + 1]);
+    *reinterpret_cast<uint4*>(buf + il_offset(r, c, C)) = *reinterpret_cast<uint4*>(h);
+}
+
+}  // namespace tc

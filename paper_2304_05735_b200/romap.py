@@ -128,6 +128,20 @@ def _check(status):
         raise RomapError(status, _lib.romap_last_error().decode())
 
 
+def selftest_mma(X, W, Dl):
+    """tcgen05 layout self test (see romap.h): returns X W^T, Dl W, Dl^T X."""
+    X = np.ascontiguousarray(X, np.float32)
+    W = np.ascontiguousarray(W, np.float32)
+    Dl = np.ascontiguousarray(Dl, np.float32)
+    o1 = np.zeros((128, 64), np.float32)
+    o2 = np.zeros((128, 32), np.float32)
+    o3 = np.zeros((64, 32), np.float32)
+    _lib.romap_selftest_mma.argtypes = [_P] * 6
+    _lib.romap_selftest_mma.restype = C.c_int32
+    _check(_lib.romap_selftest_mma(_ptr(X), _ptr(W), _ptr(Dl), _ptr(o1), _ptr(o2), _ptr(o3)))
+    return o1, o2, o3
+
+
 def version() -> str:
     return _lib.romap_version().decode()
 
