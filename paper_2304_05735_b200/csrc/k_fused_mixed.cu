@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
                                                          int* __restrict__ nonfinite, float* __restrict__ dbg) {
     extern __shared__ __align__(1024) uint8_t smem[];
     Misc* misc = reinterpret_cast<Misc*>(smem + OFF_MISC);
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int t = threadIdx.x, warp = t >> 5;
     const int N = cfg.N, LF = cfg.LF;
     const float scale = cfg.loss_scale, inv_scale = 1.0f / cfg.loss_scale;
 

@@ -1,0 +1,106 @@
+"""GPU mixed path (fp16 tensor-core MLP, fp16 tables, fp32 master / atomics) vs
+the CPU oracle.  BASELINE north_star: parameter gradients within 2e-2 relative
+(norm-relative per block); geometry stays bit-exact (same raygen / sampling).
+Losses: 1e-2 relative (fp16 operands)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import scenes
+from gpu_common import flat_W, make_pair, norm_rel
+
+pytestmark = pytest.mark.gpu
+
+from paper_2304_05735_b200 import romap as R  # noqa: E402
+
+GRAD_TOL = 2e-2
+CFG0M = dict(levels=8, log2_T=12, base_res=16, finest_res=2048.0, res_cap=128, samples_per_ray=32, rays_per_iter=256,
+             precision=1, seed=0)
+CFG1M = dict(levels=16, log2_T=16, base_res=16, finest_res=512.0, res_cap=0, samples_per_ray=64, rays_per_iter=4096,
+             precision=1, seed=1)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = R.Context(0)
+    yield c
+    c.close()
+
+
+def _check_grads(ctx, h, L, g, dbg, stats, N, loss_tol=1e-2):
+    for k in ("l_total", "l_rgb", "l_rr", "l_density"):
+        assert abs(stats[k] - L[k]) <= loss_tol * max(abs(L[k]), 1e-4), (k, stats[k], L[k])
+    hit = dbg["rays"]["hit"]
+    rg = ctx.debug_dump(h, R.DUMP_RAY_GRADS).reshape(dbg["rays"]["R"], N, 4)[hit]
+    assert norm_rel(rg[..., 0], dbg["dsigma"]) < GRAD_TOL
+    assert norm_rel(rg[..., 1:], dbg["drgb"]) < GRAD_TOL
+    gt = ctx.get_params(h, R.BLOCK_GRAD_TABLE).reshape(-1, 2)
+    e_tab = norm_rel(gt, g["table"])
+    gm = ctx.get_params(h, R.BLOCK_GRAD_MLP)
+    errs, off = [], 0
+    for w in g["W"]:
+        errs.append(norm_rel(gm[off:off + w.size], w))
+        off += w.size
+    assert e_tab < GRAD_TOL, (e_tab, errs)
+    assert max(errs) < GRAD_TOL, (e_tab, errs)
+    return e_tab, errs
+
+
+def test_mixed_cfg0_grads(ctx):
+    sc = scenes.sphere_scene(0, depth_per_view=2)
+    h, st = make_pair(R, ctx, sc, CFG0M)
+    stats = ctx.forward_backward([h])[0]
+    L, g, dbg = O.loss_and_grads(st, 1)
+    rd = ctx.debug_dump(h, R.DUMP_RAYS)
+    assert np.array_equal(rd["t_near"].view(np.uint32), dbg["rays"]["tn"].view(np.uint32))
+    _check_grads(ctx, h, L, g, dbg, stats, 32)
+    ctx.destroy_object(h)
+
+
+def test_mixed_cfg1_shape_small(ctx):
+    sc = scenes.object_scene(1, n_views=20, W=160, H=120, f=131.25, depth_per_view=8)
+    kw = dict(CFG1M, rays_per_iter=301)
+    h, st = make_pair(R, ctx, sc, kw)
+    stats = ctx.forward_backward([h])[0]
+    L, g, dbg = O.loss_and_grads(st, 1)
+    _check_grads(ctx, h, L, g, dbg, stats, 64)
+    ctx.destroy_object(h)
+
+
+def test_mixed_cfg1_full_size(ctx):
+    # BASELINE cfg1 at full size in bench.py's launch configuration (4096 rays x 64,
+    # 20 keyframes of 640x480): gradients of every block within 2e-2
+    sc = scenes.object_scene(1, n_views=20)
+    h, st = make_pair(R, ctx, sc, CFG1M, avoid_kinks=False)
+    stats = ctx.forward_backward([h])[0]
+    L, g, dbg = O.loss_and_grads(st, 1)
+    assert stats["hit_rays"] == L["hit_rays"] and stats["samples"] == L["samples"]
+    _check_grads(ctx, h, L, g, dbg, stats, 64)
+    ctx.destroy_object(h)
+
+
+def test_mixed_multi_object_and_training(ctx):
+    sc = scenes.room_scene(4, n_objects=3, n_frames=6, W=160, H=120, f=131.25, room_half=1.5)
+    kw = dict(CFG0M, rays_per_iter=128, seed=4)
+    hs, sts = [], []
+    for k, ob in enumerate(sc.objects[:2]):
+        h, st = make_pair(R, ctx, sc, kw, param_seed=20 + k, inst=ob.instance_id, obj_id=200 + k)
+        hs.append(h)
+        sts.append(st)
+    stats = ctx.forward_backward(hs)
+    for k in range(2):
+        L, g, dbg = O.loss_and_grads(sts[k], 1)
+        _check_grads(ctx, hs[k], L, g, dbg, stats[k], 32)
+    # 10 mixed training steps track the oracle's losses
+    for it in range(10):
+        s = ctx.train_step(hs, 1)
+        for k in range(2):
+            o, _, _ = O.train_iteration(sts[k])
+            assert abs(s[k]["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (it, k, s[k], o)
+    for h in hs:
+        ctx.destroy_object(h)
+
+
+def test_mixed_rejects_bad_levels(ctx):
+    with pytest.raises(R.RomapError):
+        ctx.create_object([0, 0, 0], 0.0, [1, 1, 1], R.model_config(precision=1, levels=6), 1)
