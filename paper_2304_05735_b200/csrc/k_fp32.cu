@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
             for (int b = 0; b < 8; ++b) {
                 int e = corner_entry(cl, b, res, cfg.dense[l], cfg.T);
                 float w = corner_weight(cl, b);
-                atomicAdd(gt + cfg.off[l] + e, make_float2(w * dfeat[2 * l], w * dfeat[2 * l + 1]));
+                red_add_f2(gt + cfg.off[l] + e, w * dfeat[2 * l], w * dfeat[2 * l + 1]);
             }
         }
     }

@@ -178,29 +178,29 @@ __device__ void flush_object(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, M
             tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW1 + c0), v);
             tc::tmem_wait_ld();
             if (lane < 16)
-                for (int i = 0; i < 16; ++i) atomicAdd(gm + cfg.w_off[0] + row * cfg.LF + c0 + i, v[i] * inv);
+                for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[0] + row * cfg.LF + c0 + i, v[i] * inv);
         }
         for (int c0 = 0; c0 < 32; c0 += 16) {
             tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW3 + c0), v);
             tc::tmem_wait_ld();
             if (lane < 16)
-                for (int i = 0; i < 16; ++i) atomicAdd(gm + cfg.w_off[2] + row * 32 + c0 + i, v[i] * inv);
+                for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[2] + row * 32 + c0 + i, v[i] * inv);
         }
         for (int c0 = 0; c0 < 64; c0 += 16) {
             tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW4 + c0), v);
             tc::tmem_wait_ld();
             if (lane < 16)
-                for (int i = 0; i < 16; ++i) atomicAdd(gm + cfg.w_off[3] + row * 64 + c0 + i, v[i] * inv);
+                for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[3] + row * 64 + c0 + i, v[i] * inv);
         }
         // dW2^T [64 in x 16 out], dW5^T [64 in x 16 (3) out]: row = in feature
         tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW2), v);
         tc::tmem_wait_ld();
         if (lane < 16)
-            for (int o = 0; o < 16; ++o) atomicAdd(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
+            for (int o = 0; o < 16; ++o) red_add_f1(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
         tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW5), v);
         tc::tmem_wait_ld();
         if (lane < 16)
-            for (int o = 0; o < 3; ++o) atomicAdd(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
+            for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
     }
     __syncthreads();
     if (threadIdx.x < 4) {
@@ -296,27 +296,37 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             const __half2* tab = reinterpret_cast<const __half2*>(ob.p16);
             float f8[8];
 #pragma unroll
-            for (int l = 0; l < ROMAP_MAX_LEVELS; ++l) {
-                if (l >= cfg.L) break;
-                float a0 = 0.f, a1 = 0.f;
-                if (active) {
-                    const int res = cfg.res[l];
-                    Cell cl = grid_cell(u, res);
-                    const __half2* tb = tab + cfg.off[l];
-                    __half2 hv[8];
+            for (int lp = 0; lp < ROMAP_MAX_LEVELS; lp += 2) {
+                if (lp >= cfg.L) break;
+                // issue the 16 gathers of levels lp, lp+1 before consuming any
+                __half2 hv[2][8];
+                Cell cl[2];
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) hv[b] = __ldg(tb + corner_entry(cl, b, res, cfg.dense[l], cfg.T));
+                for (int q = 0; q < 2; ++q) {
+                    const int l = lp + q;
+                    const int res = cfg.res[l];
+                    cl[q] = grid_cell(u, res);
+                    const __half2* tb = tab + cfg.off[l];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        hv[q][b] = active ? __ldg(tb + corner_entry(cl[q], b, res, cfg.dense[l], cfg.T))
+                                          : __float2half2_rn(0.f);
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int l = lp + q;
+                    float a0 = 0.f, a1 = 0.f;
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
-                        float w = corner_weight(cl, b);
-                        float2 fv = __half22float2(hv[b]);
+                        float w = corner_weight(cl[q], b);
+                        float2 fv = __half22float2(hv[q][b]);
                         a0 += w * fv.x;
                         a1 += w * fv.y;
                     }
+                    f8[(2 * l) & 7] = a0;
+                    f8[(2 * l + 1) & 7] = a1;
                 }
-                f8[(2 * l) & 7] = a0;
-                f8[(2 * l + 1) & 7] = a1;
-                if ((l & 3) == 3) tc::st_chunk(X0, t, 2 * l - 6, LF, f8);
+                if ((lp & 3) == 2) tc::st_chunk(X0, t, 2 * lp - 4, LF, f8);
             }
             float sh[16];
             sh4(rr.d, sh);
@@ -609,7 +619,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
                     for (int b = 0; b < 8; ++b) {
                         const int e = corner_entry(cl, b, res, cfg.dense[l], cfg.T);
                         const float wb = corner_weight(cl, b);
-                        atomicAdd(gt + cfg.off[l] + e, make_float2(wb * g0, wb * g1));
+                        red_add_f2(gt + cfg.off[l] + e, wb * g0, wb * g1);
                     }
                 }
             }

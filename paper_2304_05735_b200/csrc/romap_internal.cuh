@@ -210,6 +210,15 @@ __device__ __forceinline__ float corner_weight(const Cell& cl, int b) {
     return __fmul_rn(__fmul_rn(wx, wy), wz);
 }
 
+// fire-and-forget vector atomic add (REDG.E.ADD.F32x2; no return value, so no
+// long-scoreboard wait on the L2 round trip)
+__device__ __forceinline__ void red_add_f2(float2* p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void red_add_f1(float* p, float a) {
+    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(p), "f"(a) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // real SH, bands 0..3 (R2), fp32
 __device__ __forceinline__ void sh4(const float d[3], float out[16]) {
