@@ -13,9 +13,12 @@
 //          the object (flushed once per CTA and object with fp32 atomics)
 //   a7     hash-grid backward: recomputed cells, fp32 float2 atomics
 //
-// One CTA = 4 warps = 128 threads; thread t owns sample t of the tile and TMEM
-// lane t.  Two CTAs per SM (110.6 KB shared memory, 256 TMEM columns each), so
-// one CTA's gathers / atomics overlap the other's tensor-core chain.
+// One CTA = 2 warpgroups = 256 threads per 128-sample tile: thread t works on
+// sample t % 128 (= TMEM lane t % 128; warps w and w+4 share lanes 32(w%4)..+31)
+// and on half t / 128 of the split work: hash levels [h*L/2, (h+1)*L/2) of the
+// gathers and scatters, accumulator columns [32h, 32h+32) of 64-wide epilogues.
+// Two CTAs per SM (110.6 KB shared memory, 256 TMEM columns each): 16 warps
+// per SM, one CTA's gathers / atomics overlap the other's tensor-core chain.
 // Loss scaling: every backward operand is multiplied by cfg.loss_scale (a power
 // of two, exact) and divided out before the fp32 atomics.
 #include "romap_internal.cuh"
@@ -25,7 +28,8 @@ bool fused_mixed_available() { return true; }
 
 namespace {
 
-constexpr int TILE = 128;
+constexpr int TILE = 128;                      // samples per tile
+constexpr int NT = 256;                        // threads per CTA (2 warpgroups)
 // shared-memory layout (bytes); every block is a multiple of 1024
 constexpr int OFF_W1 = 0;                      // 64 x LF(<=32)
 constexpr int OFF_W2 = OFF_W1 + 64 * 32 * 2;   // 16 x 64
@@ -41,7 +45,7 @@ constexpr int OFF_DC = OFF_G2 + TILE * 64 * 2;  // 128 x 16
 constexpr int OFF_DR = OFF_DC + TILE * 16 * 2;  // 128 x 16
 constexpr int OFF_DB = OFF_DR + TILE * 16 * 2;  // 128 x 64 (dg2 -> dg1 -> dh1)
 constexpr int OFF_MISC = OFF_DB + TILE * 64 * 2;
-constexpr int SMEM_BYTES = OFF_MISC + 256;
+constexpr int SMEM_BYTES = OFF_MISC + 384;
 
 // TMEM columns
 constexpr int TM_WK = 0;      // working accumulator (<= 64 cols)
@@ -57,7 +61,7 @@ struct Misc {
     uint32_t tmem;
     int pad;
     float loss[4];
-    float xw[4][8];           // cross-warp scan exchange
+    float xw[8][8];           // cross-warp scan exchange (per warp, 8 slots)
 };
 
 __device__ __forceinline__ void sync_for_mma() {
@@ -68,11 +72,11 @@ __device__ __forceinline__ void sync_for_mma() {
 }
 
 // ---------------------------------------------------------------------------
-// segmented scans over the N samples of each ray (thread t = sample t % N of ray t / N)
+// segmented scans over the N samples of each ray; each warpgroup scans its own
+// copy (thread t = sample (t % 128) % N of ray (t % 128) / N)
 template <bool MUL>
 __device__ __forceinline__ float op2(float a, float b) { return MUL ? a * b : a + b; }
 
-// exclusive scan (prefix) + ray total; xw: smem exchange row, idx selects the slot
 template <bool MUL>
 __device__ __forceinline__ float ray_scan_excl(float x, int N, float* xw, int slot, float& total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -92,7 +96,6 @@ __device__ __forceinline__ float ray_scan_excl(float x, int N, float* xw, int sl
         total = seg_total;
         return excl;
     }
-    // N = 64 / 128: combine warps of the same ray
     if (lane == 31) xw[warp * 8 + slot] = incl;
     __syncthreads();
     const int wpr = N >> 5;
@@ -108,7 +111,6 @@ __device__ __forceinline__ float ray_scan_excl(float x, int N, float* xw, int sl
     return op2<MUL>(carry, excl);
 }
 
-// exclusive suffix sum (sum over later samples of the ray)
 __device__ __forceinline__ float ray_suffix_excl(float x, int N, float* xw, int slot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sw = N < 32 ? N : 32;
@@ -149,13 +151,12 @@ __device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, co
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
         const int chunks = ls[k].srows * (ls[k].cols / 8);
-        for (int q = threadIdx.x; q < chunks; q += TILE) {
+        for (int q = threadIdx.x; q < chunks; q += NT) {
             int r = q / (ls[k].cols / 8), cb = q % (ls[k].cols / 8);
             uint4 v = make_uint4(0, 0, 0, 0);
             if (r < ls[k].rows) {
-                const __half* src = mlp16 + ls[k].off + r * ls[k].cols + cb * 8;
-                // weights are 4-byte aligned only in general: load as 4 x half2
-                const __half2* s2 = reinterpret_cast<const __half2*>(src);
+                // weights are only 4-byte aligned in general: load as 4 x half2
+                const __half2* s2 = reinterpret_cast<const __half2*>(mlp16 + ls[k].off + r * ls[k].cols + cb * 8);
                 __half2 h[4] = {s2[0], s2[1], s2[2], s2[3]};
                 v = *reinterpret_cast<uint4*>(h);
             }
@@ -164,43 +165,47 @@ __device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, co
     }
 }
 
-// flush dW accumulators (TMEM) and loss sums of one object
+// flush dW accumulators (TMEM) and loss sums of one object; warpgroup 0 takes
+// dW1, dW2, dW5, warpgroup 1 takes dW3, dW4
 __device__ void flush_object(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* misc, double* loss_acc,
                              int slot, bool have_dw) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wg = threadIdx.x >> 7;
+    const int q = warp & 3;
     const float inv = 1.0f / cfg.loss_scale;
     float* gm = ob.g32 + cfg.n_table;
     if (have_dw) {
-        const int row = warp * 16 + lane;   // M=64 accumulator row of this lane (lanes < 16)
+        const int row = q * 16 + lane;   // M=64 accumulator row held by this lane (lanes < 16)
         float v[16];
-        // dW1 [64 x LF], dW3 [64 x 32], dW4 [64 x 64]: row = out feature
-        for (int c0 = 0; c0 < cfg.LF; c0 += 16) {
-            tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW1 + c0), v);
+        if (wg == 0) {
+            for (int c0 = 0; c0 < cfg.LF; c0 += 16) {
+                tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW1 + c0), v);
+                tc::tmem_wait_ld();
+                if (lane < 16)
+                    for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[0] + row * cfg.LF + c0 + i, v[i] * inv);
+            }
+            // dW2^T [64 in x 16 out], dW5^T [64 in x 16 (3) out]: row = input feature
+            tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW2), v);
             tc::tmem_wait_ld();
             if (lane < 16)
-                for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[0] + row * cfg.LF + c0 + i, v[i] * inv);
-        }
-        for (int c0 = 0; c0 < 32; c0 += 16) {
-            tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW3 + c0), v);
+                for (int o = 0; o < 16; ++o) red_add_f1(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
+            tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW5), v);
             tc::tmem_wait_ld();
             if (lane < 16)
-                for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[2] + row * 32 + c0 + i, v[i] * inv);
+                for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
+        } else {
+            for (int c0 = 0; c0 < 32; c0 += 16) {
+                tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW3 + c0), v);
+                tc::tmem_wait_ld();
+                if (lane < 16)
+                    for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[2] + row * 32 + c0 + i, v[i] * inv);
+            }
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW4 + c0), v);
+                tc::tmem_wait_ld();
+                if (lane < 16)
+                    for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[3] + row * 64 + c0 + i, v[i] * inv);
+            }
         }
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW4 + c0), v);
-            tc::tmem_wait_ld();
-            if (lane < 16)
-                for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[3] + row * 64 + c0 + i, v[i] * inv);
-        }
-        // dW2^T [64 in x 16 out], dW5^T [64 in x 16 (3) out]: row = in feature
-        tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW2), v);
-        tc::tmem_wait_ld();
-        if (lane < 16)
-            for (int o = 0; o < 16; ++o) red_add_f1(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
-        tc::tmem_ld16(tc::taddr(tm, warp * 32, TM_DW5), v);
-        tc::tmem_wait_ld();
-        if (lane < 16)
-            for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
     }
     __syncthreads();
     if (threadIdx.x < 4) {
@@ -219,15 +224,39 @@ __device__ __forceinline__ void st16(uint8_t* buf, int r, int c0, int C, const f
     tc::st_chunk(buf, r, c0 + 8, C, v + 8);
 }
 
+// epilogue of a 64-wide layer: this warpgroup's 32 columns, ReLU (or mask) ->
+// fp16 -> smem; `relu` records the mask, otherwise `mask` is applied
+template <bool RELU>
+__device__ __forceinline__ void epi32(uint32_t wk, int wg, uint8_t* buf, int r, uint32_t& mask) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c0 = 32 * wg + 16 * h;
+        float v[16];
+        tc::tmem_ld16(wk + c0, v);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t bit = 1u << (16 * h + k);
+            if (RELU) {
+                if (v[k] > 0.f) mask |= bit; else v[k] = 0.f;
+            } else if (!(mask & bit)) {
+                v[k] = 0.f;
+            }
+        }
+        st16(buf, r, c0, 64, v);
+    }
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDev* __restrict__ objs,
-                                                         const RayRec* __restrict__ rays, int n_tiles,
-                                                         int tiles_per_cta, double* __restrict__ loss_acc,
-                                                         int* __restrict__ nonfinite, float* __restrict__ dbg) {
+__global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev* __restrict__ objs,
+                                                       const RayRec* __restrict__ rays, int n_tiles,
+                                                       int tiles_per_cta, double* __restrict__ loss_acc,
+                                                       int* __restrict__ nonfinite, float* __restrict__ dbg) {
     extern __shared__ __align__(1024) uint8_t smem[];
     Misc* misc = reinterpret_cast<Misc*>(smem + OFF_MISC);
-    const int t = threadIdx.x, warp = t >> 5;
+    const int t = threadIdx.x, warp = t >> 5, wg = t >> 7;
+    const int r = t & (TILE - 1);                 // sample row of the tile = TMEM lane
     const int N = cfg.N, LF = cfg.LF;
     const float scale = cfg.loss_scale, inv_scale = 1.0f / cfg.loss_scale;
 
@@ -241,7 +270,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
     __syncthreads();
     tc::fence_after();
     const uint32_t tm = misc->tmem;
-    const uint32_t wk_lane = tc::taddr(tm, warp * 32, 0);   // this warp's lanes, column 0
+    const uint32_t wk = tc::taddr(tm, (warp & 3) * 32, 0);   // this warp's TMEM lanes, column 0
     uint32_t phase = 0;
     const uint32_t sW1 = tc::smem_u32(smem + OFF_W1), sW2 = tc::smem_u32(smem + OFF_W2),
                    sW3 = tc::smem_u32(smem + OFF_W3), sW4 = tc::smem_u32(smem + OFF_W4),
@@ -258,6 +287,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
     uint8_t* DC = smem + OFF_DC;
     uint8_t* DR = smem + OFF_DR;
     uint8_t* DB = smem + OFF_DB;
+    float* xw = &misc->xw[0][0];
 
     auto mma_wait = [&]() {
         tc::mbar_wait(&misc->mbar, phase);
@@ -270,6 +300,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
     int cur = -1;
     bool dw_fresh = true;
     const int rays_per_tile = TILE / N;
+    const int LH = cfg.L >> 1;                    // hash levels per warpgroup
 
     for (int tile = tile0; tile < tile1; ++tile) {
         const int slot = rays[tile * rays_per_tile].slot;
@@ -280,7 +311,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             dw_fresh = true;
         }
         const ObjDev& ob = objs[slot];
-        const long long s = (long long)tile * TILE + t;
+        const long long s = (long long)tile * TILE + r;
         const int ray = (int)(s / N);
         const int i = (int)(s - (long long)ray * N);
         const RayRec rr = rays[ray];
@@ -296,14 +327,14 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             const __half2* tab = reinterpret_cast<const __half2*>(ob.p16);
             float f8[8];
 #pragma unroll
-            for (int lp = 0; lp < ROMAP_MAX_LEVELS; lp += 2) {
-                if (lp >= cfg.L) break;
-                // issue the 16 gathers of levels lp, lp+1 before consuming any
+            for (int lp = 0; lp < ROMAP_MAX_LEVELS / 2; lp += 2) {
+                if (lp >= LH) break;
+                // issue the 16 gathers of two levels before consuming any
                 __half2 hv[2][8];
                 Cell cl[2];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const int l = lp + q;
+                    const int l = wg * LH + lp + q;
                     const int res = cfg.res[l];
                     cl[q] = grid_cell(u, res);
                     const __half2* tb = tab + cfg.off[l];
@@ -314,23 +345,24 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
                 }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const int l = lp + q;
                     float a0 = 0.f, a1 = 0.f;
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
-                        float w = corner_weight(cl[q], b);
-                        float2 fv = __half22float2(hv[q][b]);
+                        const float w = corner_weight(cl[q], b);
+                        const float2 fv = __half22float2(hv[q][b]);
                         a0 += w * fv.x;
                         a1 += w * fv.y;
                     }
-                    f8[(2 * l) & 7] = a0;
-                    f8[(2 * l + 1) & 7] = a1;
+                    f8[2 * ((lp + q) & 3)] = a0;
+                    f8[2 * ((lp + q) & 3) + 1] = a1;
                 }
-                if ((lp & 3) == 2) tc::st_chunk(X0, t, 2 * lp - 4, LF, f8);
+                if ((lp & 3) == 2) tc::st_chunk(X0, r, 2 * (wg * LH + lp - 2), LF, f8);
             }
-            float sh[16];
-            sh4(rr.d, sh);
-            st16(CIN, t, 16, 32, sh);
+            if (wg == 1) {
+                float sh[16];
+                sh4(rr.d, sh);
+                st16(CIN, r, 16, 32, sh);
+            }
         }
         sync_for_mma();
 
@@ -343,18 +375,8 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-        unsigned long long m_h1 = 0, m_g1 = 0, m_g2 = 0;
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (v[k] > 0.f) m_h1 |= 1ull << (c0 + k); else v[k] = 0.f;
-            }
-            st16(H1, t, c0, 64, v);
-        }
+        uint32_t m_h1 = 0, m_g1 = 0, m_g2 = 0;
+        epi32<true>(wk, wg, H1, r, m_h1);
         sync_for_mma();
         // L2: WK[128 x 16] = H1 . W2^T
         if (t == 0) {
@@ -367,11 +389,11 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
         float sigma, r0;
         {
             float v[16];
-            tc::tmem_ld16(wk_lane, v);
+            tc::tmem_ld16(wk, v);
             tc::tmem_wait_ld();
             r0 = v[0];
             sigma = density_act(r0, cfg.density_act);
-            st16(CIN, t, 0, 32, v);
+            if (wg == 0) st16(CIN, r, 0, 32, v);
         }
         sync_for_mma();
         // L3: WK = CIN . W3^T
@@ -382,17 +404,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (v[k] > 0.f) m_g1 |= 1ull << (c0 + k); else v[k] = 0.f;
-            }
-            st16(G1, t, c0, 64, v);
-        }
+        epi32<true>(wk, wg, G1, r, m_g1);
         sync_for_mma();
         // L4: WK = G1 . W4^T
         if (t == 0) {
@@ -402,17 +414,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (v[k] > 0.f) m_g2 |= 1ull << (c0 + k); else v[k] = 0.f;
-            }
-            st16(G2, t, c0, 64, v);
-        }
+        epi32<true>(wk, wg, G2, r, m_g2);
         sync_for_mma();
         // L5: WK[128 x 16] = G2 . W5^T (rows 3..15 of W5 are zero)
         if (t == 0) {
@@ -425,14 +427,14 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
         float c[3];
         {
             float v[16];
-            tc::tmem_ld16(wk_lane, v);
+            tc::tmem_ld16(wk, v);
             tc::tmem_wait_ld();
 #pragma unroll
             for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[k]));
         }
 
-        // ---- a5: volume rendering + loss + render backward (segmented over each ray)
-        float* xw = &misc->xw[0][0];
+        // ---- a5: volume rendering + loss + render backward (both warpgroups,
+        // redundantly, so every thread holds dL/dsigma and dL/dc of its sample)
         const float x = active ? sigma * delta : 0.f;
         const float alpha = expf(-x);
         const float o = -expm1f(-x);
@@ -448,6 +450,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
         float gC[3] = {0.f, 0.f, 0.f};
         float gD = 0.f, gCb = 0.f;
         const int cls = rr.flags & RF_CLS_MASK;
+        const float invB = 1.0f / (float)ob.n_rays;
         if (active) {
             const bool has_depth = (rr.flags & RF_HAS_DEPTH) != 0;
             const float Cs[3] = {Cs0, Cs1, Cs2};
@@ -458,7 +461,6 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
                 e[k] = Cs[k] + TN * bgc[k] - (cls == CLS_OBJ ? rr.tgt[k] : rr.bg[k]);
             }
             const float ne = sqrtf(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
-            const float invB = 1.0f / (float)ob.n_rays;
 #pragma unroll
             for (int k = 0; k < 3; ++k) gC[k] = ne > 0.f ? e[k] / ne * invB : 0.f;
             float ed = 0.f;
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
                 gD = ed > 0.f ? cfg.lambda_depth * invB : (ed < 0.f ? -cfg.lambda_depth * invB : 0.f);
             }
             gCb = gC[0] * bgc[0] + gC[1] * bgc[1] + gC[2] * bgc[2];
-            if (i == 0) {
+            if (i == 0 && wg == 0) {
                 atomicAdd(&misc->loss[cls == CLS_OBJ ? 0 : 1], ne);
                 if (has_depth) atomicAdd(&misc->loss[2], fabsf(ed));
                 if (cls == CLS_BG) atomicAdd(&misc->loss[3], ssum);
@@ -479,25 +481,21 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
         const float Sd = ray_suffix_excl(w * dist, N, xw, 7);
         if (active) {
             const float Tn1 = Ti * alpha;
-            const float invB = 1.0f / (float)ob.n_rays;
             dsig = delta * (Tn1 * gc - S - TN * gCb) + delta * gD * (Tn1 * dist - Sd) +
                    (cls == CLS_BG ? cfg.lambda_density * invB : 0.f);
 #pragma unroll
             for (int k = 0; k < 3; ++k) dcol[k] = w * gC[k];
         }
-        if (dbg) {
-            float4 q = make_float4(dsig, dcol[0], dcol[1], dcol[2]);
-            *reinterpret_cast<float4*>(dbg + 4 * s) = q;
-        }
+        if (dbg && wg == 0) *reinterpret_cast<float4*>(dbg + 4 * s) = make_float4(dsig, dcol[0], dcol[1], dcol[2]);
 
         // ---- a6: MLP backward (scaled by loss_scale)
-        {
+        if (wg == 0) {
             float v[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k) v[k] = 0.f;
 #pragma unroll
             for (int k = 0; k < 3; ++k) v[k] = dcol[k] * c[k] * (1.f - c[k]) * scale;
-            st16(DC, t, 0, 16, v);
+            st16(DC, r, 0, 16, v);
         }
         const float dr0_extra = dsig * density_act_grad(r0, sigma, cfg.density_act) * scale;
         sync_for_mma();
@@ -511,16 +509,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (!((m_g2 >> (c0 + k)) & 1ull)) v[k] = 0.f;
-            st16(DB, t, c0, 64, v);
-        }
+        epi32<false>(wk, wg, DB, r, m_g2);
         sync_for_mma();
         // B4: WK = DB(dg2) . W4;  dW4[64 x 64] += DB^T . G1
         if (t == 0) {
@@ -533,16 +522,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (!((m_g1 >> (c0 + k)) & 1ull)) v[k] = 0.f;
-            st16(DB, t, c0, 64, v);
-        }
+        epi32<false>(wk, wg, DB, r, m_g1);
         sync_for_mma();
         // B3: WK[128 x 16] = DB(dg1) . W3[:, 0:16];  dW3[64 x 32] += DB^T . CIN
         if (t == 0) {
@@ -555,15 +535,15 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-        {
+        if (wg == 0) {
             float v[16];
-            tc::tmem_ld16(wk_lane, v);
+            tc::tmem_ld16(wk, v);
             tc::tmem_wait_ld();
             v[0] += dr0_extra;
             if (!active)
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
-            st16(DR, t, 0, 16, v);
+            st16(DR, r, 0, 16, v);
         }
         sync_for_mma();
         // B2: WK[128 x 64] = DR[128 x 16] . W2[16 x 64];  dW2^T[64 x 16] += H1^T . DR
@@ -576,16 +556,7 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
             tc::commit(&misc->mbar);
         }
         mma_wait();
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (!((m_h1 >> (c0 + k)) & 1ull)) v[k] = 0.f;
-            st16(DB, t, c0, 64, v);
-        }
+        epi32<false>(wk, wg, DB, r, m_h1);
         sync_for_mma();
         // B1: WK[128 x LF] = DB(dh1) . W1[64 x LF];  dW1[64 x LF] += DB^T . X0
         if (t == 0) {
@@ -600,20 +571,20 @@ __global__ void __launch_bounds__(TILE, 2) k_fused_mixed(CfgDev cfg, const ObjDe
         mma_wait();
         dw_fresh = false;
 
-        // ---- a7: hash-grid backward (fp32 float2 atomics)
-        float2* gt = reinterpret_cast<float2*>(ob.g32);
-#pragma unroll
-        for (int c0 = 0; c0 < 32; c0 += 16) {
-            if (c0 >= LF) break;
+        // ---- a7: hash-grid backward, this warpgroup's levels (fp32 REDG.F32x2)
+        {
+            // dfeat of levels [wg*LH, wg*LH + LH) = accumulator columns [2*wg*LH, +2*LH)
             float v[16];
-            tc::tmem_ld16(wk_lane + c0, v);
+            tc::tmem_ld16(wk + 2 * wg * LH, v);
             tc::tmem_wait_ld();
             if (active) {
+                float2* gt = reinterpret_cast<float2*>(ob.g32);
 #pragma unroll
                 for (int lq = 0; lq < 8; ++lq) {
-                    const int l = c0 / 2 + lq;
+                    if (lq >= LH) break;
+                    const int l = wg * LH + lq;
                     const int res = cfg.res[l];
-                    Cell cl = grid_cell(u, res);
+                    const Cell cl = grid_cell(u, res);
                     const float g0 = v[2 * lq] * inv_scale, g1 = v[2 * lq + 1] * inv_scale;
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
@@ -649,5 +620,5 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
     if (grid > n_tiles) grid = n_tiles;
     const int per = (n_tiles + grid - 1) / grid;
     grid = (n_tiles + per - 1) / per;
-    k_fused_mixed<<<grid, TILE, SMEM_BYTES, lc.st>>>(cfg, objs, rays, n_tiles, per, loss_acc, nonfinite, dbg);
+    k_fused_mixed<<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, n_tiles, per, loss_acc, nonfinite, dbg);
 }
