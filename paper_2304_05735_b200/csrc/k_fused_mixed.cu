@@ -301,16 +301,31 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
     bool dw_fresh = true;
     const int rays_per_tile = TILE / N;
     const int LH = cfg.L >> 1;                    // hash levels per warpgroup
+    // per-object values held in registers (re-read only when the object changes)
+    const __half2* tab = nullptr;
+    float2* gt = nullptr;
+    float ob_a[3] = {0.f, 0.f, 0.f};
+    int ob_ray_begin = 0;
+    float invB = 0.f;
+    unsigned long long pre = 0;
 
     for (int tile = tile0; tile < tile1; ++tile) {
         const int slot = rays[tile * rays_per_tile].slot;
         if (slot != cur) {
             if (cur >= 0) flush_object(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
-            load_weights(smem, objs[slot].p16 + cfg.n_table, cfg);
+            const ObjDev& ob = objs[slot];
+            load_weights(smem, ob.p16 + cfg.n_table, cfg);
             cur = slot;
             dw_fresh = true;
+            tab = reinterpret_cast<const __half2*>(ob.p16);
+            gt = reinterpret_cast<float2*>(ob.g32);
+            ob_a[0] = ob.a[0];
+            ob_a[1] = ob.a[1];
+            ob_a[2] = ob.a[2];
+            ob_ray_begin = ob.ray_begin;
+            invB = 1.0f / (float)ob.n_rays;
+            pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1);
         }
-        const ObjDev& ob = objs[slot];
         const long long s = (long long)tile * TILE + r;
         const int ray = (int)(s / N);
         const int i = (int)(s - (long long)ray * N);
@@ -319,12 +334,8 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
 
         // ---- a2/a3: sample + encode (fp16 table gathers, fp32 interpolation)
         float dist = 0.f, delta = 0.f, u[3] = {0.f, 0.f, 0.f};
-        if (active) {
-            unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1);
-            sample_geometry(rr, i, N, pre, ray - ob.ray_begin, ob.a, dist, delta, u);
-        }
+        if (active) sample_geometry(rr, i, N, pre, ray - ob_ray_begin, ob_a, dist, delta, u);
         {
-            const __half2* tab = reinterpret_cast<const __half2*>(ob.p16);
             float f8[8];
 #pragma unroll
             for (int lp = 0; lp < ROMAP_MAX_LEVELS / 2; lp += 2) {
@@ -450,7 +461,6 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
         float gC[3] = {0.f, 0.f, 0.f};
         float gD = 0.f, gCb = 0.f;
         const int cls = rr.flags & RF_CLS_MASK;
-        const float invB = 1.0f / (float)ob.n_rays;
         if (active) {
             const bool has_depth = (rr.flags & RF_HAS_DEPTH) != 0;
             const float Cs[3] = {Cs0, Cs1, Cs2};
@@ -578,7 +588,6 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
             tc::tmem_ld16(wk + 2 * wg * LH, v);
             tc::tmem_wait_ld();
             if (active) {
-                float2* gt = reinterpret_cast<float2*>(ob.g32);
 #pragma unroll
                 for (int lq = 0; lq < 8; ++lq) {
                     if (lq >= LH) break;

@@ -212,11 +212,13 @@ __device__ __forceinline__ float corner_weight(const Cell& cl, int b) {
 
 // fire-and-forget vector atomic add (REDG.E.ADD.F32x2; no return value, so no
 // long-scoreboard wait on the L2 round trip)
+// (no "memory" clobber: nothing in the kernel reads these addresses back, and a
+// clobber would force every cached global field to be re-loaded after each RED)
 __device__ __forceinline__ void red_add_f2(float2* p, float a, float b) {
-    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(a), "f"(b) : "memory");
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(a), "f"(b));
 }
 __device__ __forceinline__ void red_add_f1(float* p, float a) {
-    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(p), "f"(a) : "memory");
+    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(p), "f"(a));
 }
 
 // ---------------------------------------------------------------------------
