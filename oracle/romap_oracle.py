@@ -94,7 +94,9 @@ def level_table(cfg: ModelConfig) -> list[Level]:
 
     N_l = floor(N_min * b^l + 1e-6) with b = (N_max/N_min)^(1/(L-1)), in double,
     then min(N_l, res_cap).  Vertex lattice (N_l+1)^3.  A level is dense iff
-    (N_l+1)^3 <= T, else hashed into T entries.  Levels are stored back to back.
+    (N_l+1)^3 <= T, else hashed into T entries.  Levels are stored back to back,
+    each block padded to a multiple of 16 entries (R5; padding entries are never
+    addressed).
     """
     T = 1 << cfg.log2_T
     b = (cfg.finest_res / cfg.base_res) ** (1.0 / (cfg.levels - 1)) if cfg.levels > 1 else 1.0
@@ -106,13 +108,13 @@ def level_table(cfg: ModelConfig) -> list[Level]:
         dense = (n + 1) ** 3 <= T
         size = (n + 1) ** 3 if dense else T
         out.append(Level(n, dense, size, off))
-        off += size
+        off += (size + 15) // 16 * 16
     return out
 
 
 def table_entries(cfg: ModelConfig) -> int:
     lt = level_table(cfg)
-    return lt[-1].offset + lt[-1].size
+    return lt[-1].offset + (lt[-1].size + 15) // 16 * 16
 
 
 def mlp_shapes(cfg: ModelConfig) -> list[tuple[int, int]]:

@@ -31,7 +31,10 @@ def test_level_table_cfg1_hand_listed():
     lt = O.level_table(cfg)
     assert [l.res for l in lt] == [16, 20, 25, 32, 40, 50, 64, 80, 101, 128, 161, 203, 256, 322, 406, 512]
     assert [l.dense for l in lt] == [True] * 4 + [False] * 12      # 33^3 <= 65536 < 41^3
-    assert O.table_entries(cfg) == 17 ** 3 + 21 ** 3 + 26 ** 3 + 33 ** 3 + 12 * 65536 == 854119
+    # R5: level blocks padded to 16 entries: 4913->4928, 9261->9264, 17576->17584, 35937->35952
+    assert O.table_entries(cfg) == 4928 + 9264 + 17584 + 35952 + 12 * 65536 == 854160
+    assert [l.offset for l in lt[:5]] == [0, 4928, 4928 + 9264, 4928 + 9264 + 17584, 4928 + 9264 + 17584 + 35952]
+    assert sum(l.size for l in lt) == 854119                        # addressable entries
 
 
 # ---------------------------------------------------------------- O2 RNG
