@@ -340,8 +340,13 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
 #pragma unroll
             for (int lp = 0; lp < ROMAP_MAX_LEVELS / 2; lp += 2) {
                 if (lp >= LH) break;
-                // issue the 16 gathers of two levels before consuming any
-                __half2 hv[2][8];
+                // x-neighbour corners (b, b|1) share a 16-byte chunk of the fp16 table in
+                // 3 of 4 cases (dense: entries e, e+1; hashed: e ^ (x ^ (x+1)) with the
+                // x prime = 1), so each corner pair costs one 16-B gather (+ a 4-B one
+                // otherwise); level blocks are 16-entry aligned (R5).
+                uint4 qv[2][4];
+                uint32_t xv[2][4];
+                int e0[2][4], e1[2][4];
                 Cell cl[2];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -350,19 +355,29 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
                     cl[q] = grid_cell(u, res);
                     const __half2* tb = tab + cfg.off[l];
 #pragma unroll
-                    for (int b = 0; b < 8; ++b)
-                        hv[q][b] = active ? __ldg(tb + corner_entry(cl[q], b, res, cfg.dense[l], cfg.T))
-                                          : __float2half2_rn(0.f);
+                    for (int p = 0; p < 4; ++p) {
+                        e0[q][p] = corner_entry(cl[q], 2 * p, res, cfg.dense[l], cfg.T);
+                        e1[q][p] = corner_entry(cl[q], 2 * p + 1, res, cfg.dense[l], cfg.T);
+                        const bool same = (e0[q][p] >> 2) == (e1[q][p] >> 2);
+                        qv[q][p] = active ? ldg_v4(tb + (e0[q][p] & ~3)) : make_uint4(0, 0, 0, 0);
+                        xv[q][p] = (active && !same) ? ldg_u32(tb + e1[q][p]) : 0u;
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        const float w = corner_weight(cl[q], b);
-                        const float2 fv = __half22float2(hv[q][b]);
-                        a0 += w * fv.x;
-                        a1 += w * fv.y;
+                    for (int p = 0; p < 4; ++p) {
+                        const bool same = (e0[q][p] >> 2) == (e1[q][p] >> 2);
+                        const uint32_t h0 = sel4(qv[q][p], e0[q][p] & 3);
+                        const uint32_t h1 = same ? sel4(qv[q][p], e1[q][p] & 3) : xv[q][p];
+                        const float w0 = corner_weight(cl[q], 2 * p), w1 = corner_weight(cl[q], 2 * p + 1);
+                        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
+                        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
+                        a0 += w0 * f0.x;
+                        a1 += w0 * f0.y;
+                        a0 += w1 * f1.x;
+                        a1 += w1 * f1.y;
                     }
                     f8[2 * ((lp + q) & 3)] = a0;
                     f8[2 * ((lp + q) & 3) + 1] = a1;
@@ -595,11 +610,23 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
                     const int res = cfg.res[l];
                     const Cell cl = grid_cell(u, res);
                     const float g0 = v[2 * lq] * inv_scale, g1 = v[2 * lq + 1] * inv_scale;
+                    float2* gl = gt + cfg.off[l];
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        const int e = corner_entry(cl, b, res, cfg.dense[l], cfg.T);
-                        const float wb = corner_weight(cl, b);
-                        red_add_f2(gt + cfg.off[l] + e, wb * g0, wb * g1);
+                    for (int p = 0; p < 4; ++p) {
+                        // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
+                        // REDG.F32x4, else two REDG.F32x2
+                        const int ea = corner_entry(cl, 2 * p, res, cfg.dense[l], cfg.T);
+                        const int eb = corner_entry(cl, 2 * p + 1, res, cfg.dense[l], cfg.T);
+                        const float wa = corner_weight(cl, 2 * p), wb = corner_weight(cl, 2 * p + 1);
+                        if ((ea >> 1) == (eb >> 1)) {
+                            if (ea < eb)
+                                red_add_f4(reinterpret_cast<float4*>(gl + ea), wa * g0, wa * g1, wb * g0, wb * g1);
+                            else
+                                red_add_f4(reinterpret_cast<float4*>(gl + eb), wb * g0, wb * g1, wa * g0, wa * g1);
+                        } else {
+                            red_add_f2(gl + ea, wa * g0, wa * g1);
+                            red_add_f2(gl + eb, wb * g0, wb * g1);
+                        }
                     }
                 }
             }

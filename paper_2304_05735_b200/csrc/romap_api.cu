@@ -239,7 +239,7 @@ static romap_status build_cfg(const romap_model_config* cfg, CfgDev& cd) {
         cd.res[l] = (int)n;
         cd.dense[l] = dense ? 1 : 0;
         cd.off[l] = (int)off;
-        off += dense ? v : cd.T;
+        off += ((dense ? v : cd.T) + 15) / 16 * 16;   // R5: level blocks padded to 16 entries
     }
     cd.n_entries = (int)off;
     cd.n_table = (int)(off * cd.F);

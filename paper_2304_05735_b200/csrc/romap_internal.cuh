@@ -221,6 +221,15 @@ __device__ __forceinline__ void red_add_f1(float* p, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" :: "l"(p), "f"(a));
 }
 
+__device__ __forceinline__ void red_add_f4(float4* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
+}
+__device__ __forceinline__ uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+__device__ __forceinline__ uint32_t ldg_u32(const void* p) { return __ldg(reinterpret_cast<const unsigned*>(p)); }
+__device__ __forceinline__ uint32_t sel4(const uint4& q, int k) {
+    return (k & 2) ? ((k & 1) ? q.w : q.z) : ((k & 1) ? q.y : q.x);
+}
+
 // ---------------------------------------------------------------------------
 // real SH, bands 0..3 (R2), fp32
 __device__ __forceinline__ void sh4(const float d[3], float out[16]) {
