@@ -1,24 +1,32 @@
-// k_fused_mixed.cu -- the mixed-precision hot path: ONE persistent kernel per
-// iteration that runs, per 128-sample tile (whole rays of one object):
+// k_fused_mixed.cu -- the mixed-precision hot path: ONE persistent,
+// warp-specialised kernel per iteration (one CTA per SM) that runs, per
+// 128-sample tile (whole rays of one object):
 //
-//   a2-a3  stratified samples (bit-exact with the fp32 path) + hash-grid encode
-//          forward: fp16 table gathers, fp32 trilinear accumulation
-//   a4     fused MLP forward on the 5th-gen tensor cores: 5 tcgen05.mma layers
-//          (fp16 operands in shared memory, fp32 accumulators in TMEM), ReLU /
-//          exp / sigmoid epilogues from TMEM -> registers -> shared memory
+//   a3     hash-grid encode forward: fp16 table gathers, fp32 trilinear
+//          accumulation                                   [warpgroups G0, G1]
+//   a2/a4  SH(4) of the view direction + fused MLP forward on the 5th-gen
+//          tensor cores: 5 tcgen05.mma layers (fp16 operands in shared memory,
+//          fp32 accumulators in TMEM), ReLU / exp / sigmoid epilogues
+//                                                          [warpgroup M]
 //   a5     volume rendering (Eq. 6) + object-tailored loss (Eqs. 7-11) + render
-//          backward, segmented scans over each ray's samples
+//          backward, segmented scans over each ray's samples          [M]
 //   a6     MLP backward on tensor cores: dX = delta W per layer, and
 //          dW += delta^T X accumulated in TMEM across all tiles this CTA runs for
-//          the object (flushed once per CTA and object with fp32 atomics)
-//   a7     hash-grid backward: recomputed cells, fp32 float2 atomics
+//          the object (flushed once per CTA and object with fp32 REDs)   [M]
+//   a7     hash-grid backward: recomputed cells, fp32 vector REDs      [G0, G1]
 //
-// One CTA = 2 warpgroups = 256 threads per 128-sample tile: thread t works on
-// sample t % 128 (= TMEM lane t % 128; warps w and w+4 share lanes 32(w%4)..+31)
-// and on half t / 128 of the split work: hash levels [h*L/2, (h+1)*L/2) of the
-// gathers and scatters, accumulator columns [32h, 32h+32) of 64-wide epilogues.
-// Two CTAs per SM (110.6 KB shared memory, 256 TMEM columns each): 16 warps
-// per SM, one CTA's gathers / atomics overlap the other's tensor-core chain.
+// Pipeline.  G0 / G1 (threads 0-255) own hash levels [0, L/2) / [L/2, L) of
+// sample t % 128; M (threads 256-383) owns the whole MLP / render chain of
+// sample t - 256.  In G iteration `it` the gathers of tile `it` are interleaved,
+// level pair by level pair, with the fire-and-forget scatter of tile `it - 2`,
+// so the REDs fill the gathers' L2 latency; meanwhile M runs tile `it - 1`.
+// Hand-offs are mbarriers in shared memory (two slots, b = tile & 1):
+//   x0_full[b]   G -> M   encoded features of the tile are in X0[b]   (8 warp arrivals)
+//   tile_done[b] M -> G   the tile's last MMAs completed: dfeat is in TMEM DF[b]
+//                         and X0[b] is free                           (tcgen05.commit)
+//   df_empty[b]  G -> M   DF[b] has been read                         (8 warp arrivals)
+// Per-sample geometry (u, dist, delta) comes from k_raygen_samples (bit-exact
+// with the fp32 path), so neither role recomputes the RNG / IEEE divisions.
 // Loss scaling: every backward operand is multiplied by cfg.loss_scale (a power
 // of two, exact) and divided out before the fp32 atomics.
 #include "romap_internal.cuh"
@@ -29,15 +37,20 @@ bool fused_mixed_available() { return true; }
 namespace {
 
 constexpr int TILE = 128;                      // samples per tile
-constexpr int NT = 256;                        // threads per CTA (2 warpgroups)
+constexpr int NG = 256;                        // gather/scatter threads (G0, G1)
+constexpr int NM = 128;                        // MLP/render threads (M)
+constexpr int NT = NG + NM;
+constexpr int BAR_M = 1;                       // named barrier of M
+
 // shared-memory layout (bytes); every block is a multiple of 1024
 constexpr int OFF_W1 = 0;                      // 64 x LF(<=32)
 constexpr int OFF_W2 = OFF_W1 + 64 * 32 * 2;   // 16 x 64
 constexpr int OFF_W3 = OFF_W2 + 16 * 64 * 2;   // 64 x 32
 constexpr int OFF_W4 = OFF_W3 + 64 * 32 * 2;   // 64 x 64
 constexpr int OFF_W5 = OFF_W4 + 64 * 64 * 2;   // 16 x 64 (rows 3..15 zero)
-constexpr int OFF_X0 = OFF_W5 + 16 * 64 * 2;   // 128 x LF
-constexpr int OFF_H1 = OFF_X0 + TILE * 32 * 2; // 128 x 64
+constexpr int X0_BYTES = TILE * 32 * 2;
+constexpr int OFF_X0 = OFF_W5 + 16 * 64 * 2;   // 2 slots x 128 x LF
+constexpr int OFF_H1 = OFF_X0 + 2 * X0_BYTES;  // 128 x 64
 constexpr int OFF_CIN = OFF_H1 + TILE * 64 * 2;
 constexpr int OFF_G1 = OFF_CIN + TILE * 32 * 2;
 constexpr int OFF_G2 = OFF_G1 + TILE * 64 * 2;
@@ -45,43 +58,48 @@ constexpr int OFF_DC = OFF_G2 + TILE * 64 * 2;  // 128 x 16
 constexpr int OFF_DR = OFF_DC + TILE * 16 * 2;  // 128 x 16
 constexpr int OFF_DB = OFF_DR + TILE * 16 * 2;  // 128 x 64 (dg2 -> dg1 -> dh1)
 constexpr int OFF_MISC = OFF_DB + TILE * 64 * 2;
-constexpr int SMEM_BYTES = OFF_MISC + 384;
+constexpr int SMEM_BYTES = OFF_MISC + 1024;
 
-// TMEM columns
+// TMEM columns (one CTA per SM, so the whole 512-column allocation is free)
 constexpr int TM_WK = 0;      // working accumulator (<= 64 cols)
-constexpr int TM_DW1 = 64;    // dW1   [64 x LF]
-constexpr int TM_DW3 = 96;    // dW3   [64 x 32]
-constexpr int TM_DW4 = 128;   // dW4   [64 x 64]
-constexpr int TM_DW2 = 192;   // dW2^T [64 x 16]
-constexpr int TM_DW5 = 208;   // dW5^T [64 x 16]
-constexpr int TM_COLS = 256;
+constexpr int TM_DF = 64;     // 2 x 32: dfeat of tile slot b at TM_DF + 32 b
+constexpr int TM_DW1 = 128;   // dW1   [64 x LF]
+constexpr int TM_DW3 = 160;   // dW3   [64 x 32]
+constexpr int TM_DW4 = 192;   // dW4   [64 x 64]
+constexpr int TM_DW2 = 256;   // dW2^T [64 x 16]
+constexpr int TM_DW5 = 272;   // dW5^T [64 x 16]
+constexpr int TM_COLS = 512;
 
 struct Misc {
-    uint64_t mbar;
+    uint64_t mbar_mma;        // M: completion of its own MMA groups
+    uint64_t x0_full[2];
+    uint64_t tile_done[2];
+    uint64_t df_empty[2];
     uint32_t tmem;
     int pad;
     float loss[4];
-    float xw[8][8];           // cross-warp scan exchange (per warp, 8 slots)
+    float xw[4][8];           // M cross-warp scan exchange (per warp, 8 slots)
+    int4 lv[ROMAP_MAX_LEVELS];    // per level: res, y multiplier, z multiplier, dense (R5)
+    int lvoff[ROMAP_MAX_LEVELS];  // entry offset of the level
 };
+static_assert(sizeof(Misc) <= 1024, "misc block");
 
-__device__ __forceinline__ void sync_for_mma() {
+// fence generic smem writes for the tensor core, then sync M
+__device__ __forceinline__ void m_sync_for_mma() {
     tc::fence_async_smem();
     tc::fence_before();
-    __syncthreads();
+    tc::bar_sync(BAR_M, NM);
     tc::fence_after();
 }
 
 // ---------------------------------------------------------------------------
-// segmented scans over the N samples of each ray; each warpgroup scans its own
-// copy (thread t = sample (t % 128) % N of ray (t % 128) / N)
+// segmented scans over the N samples of each ray, on M's 128 threads
+// (thread m = sample m of the tile; a ray covers N consecutive threads)
 template <bool MUL>
 __device__ __forceinline__ float op2(float a, float b) { return MUL ? a * b : a + b; }
 
 template <bool MUL>
-__device__ __forceinline__ float ray_scan_excl(float x, int N, float* xw, int slot, float& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sw = N < 32 ? N : 32;
-    const float ident = MUL ? 1.f : 0.f;
+__device__ __forceinline__ float warp_incl(float x, int sw, int lane) {
     float incl = x;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -89,70 +107,104 @@ __device__ __forceinline__ float ray_scan_excl(float x, int N, float* xw, int sl
         float y = __shfl_up_sync(0xffffffffu, incl, off, sw);
         if ((lane & (sw - 1)) >= off) incl = op2<MUL>(incl, y);
     }
-    float excl = __shfl_up_sync(0xffffffffu, incl, 1, sw);
-    if ((lane & (sw - 1)) == 0) excl = ident;
-    float seg_total = __shfl_sync(0xffffffffu, incl, sw - 1, sw);
-    if (N <= 32) {
-        total = seg_total;
-        return excl;
-    }
-    if (lane == 31) xw[warp * 8 + slot] = incl;
-    __syncthreads();
-    const int wpr = N >> 5;
-    const int w0 = warp - (warp % wpr);
-    float carry = ident, tot = ident;
-    for (int w = w0; w < w0 + wpr; ++w) {
-        float v = xw[w * 8 + slot];
-        if (w < warp) carry = op2<MUL>(carry, v);
-        tot = op2<MUL>(tot, v);
-    }
-    __syncthreads();
-    total = tot;
-    return op2<MUL>(carry, excl);
+    return incl;
 }
 
-__device__ __forceinline__ float ray_suffix_excl(float x, int N, float* xw, int slot) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// exclusive product scan (transmittance T_i) and the ray total T_N
+__device__ __forceinline__ float m_scan_mul(float x, int N, float* xw, float& total) {
+    const int lane = threadIdx.x & 31, mw = (threadIdx.x - NG) >> 5;
     const int sw = N < 32 ? N : 32;
-    float incl = x;
+    const float incl = warp_incl<true>(x, sw, lane);
+    float excl = __shfl_up_sync(0xffffffffu, incl, 1, sw);
+    if ((lane & (sw - 1)) == 0) excl = 1.f;
+    if (N <= 32) {
+        total = __shfl_sync(0xffffffffu, incl, sw - 1, sw);
+        return excl;
+    }
+    if (lane == 31) xw[mw * 8 + 0] = incl;
+    tc::bar_sync(BAR_M, NM);
+    const int wpr = N >> 5, w0 = mw - (mw % wpr);
+    float carry = 1.f, tot = 1.f;
+    for (int w = w0; w < w0 + wpr; ++w) {
+        const float v = xw[w * 8 + 0];
+        if (w < mw) carry *= v;
+        tot *= v;
+    }
+    total = tot;
+    return carry * excl;
+}
+
+// ray totals of K values at once (one cross-warp exchange), slots 1..K
+template <int K>
+__device__ __forceinline__ void m_ray_sums(float (&v)[K], int N, float* xw) {
+    const int lane = threadIdx.x & 31, mw = (threadIdx.x - NG) >> 5;
+    const int sw = N < 32 ? N : 32;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+            if (off < sw) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off, sw);
+    if (N <= 32) return;
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) xw[mw * 8 + 1 + k] = v[k];
+    tc::bar_sync(BAR_M, NM);
+    const int wpr = N >> 5, w0 = mw - (mw % wpr);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        float tot = 0.f;
+        for (int w = w0; w < w0 + wpr; ++w) tot += xw[w * 8 + 1 + k];
+        v[k] = tot;
+    }
+}
+
+// two exclusive suffix sums (sum over later samples of the ray), slots 6, 7
+__device__ __forceinline__ void m_suffix2(float x0, float x1, int N, float* xw, float& s0, float& s1) {
+    const int lane = threadIdx.x & 31, mw = (threadIdx.x - NG) >> 5;
+    const int sw = N < 32 ? N : 32;
+    float i0 = x0, i1 = x1;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         if (off >= sw) break;
-        float y = __shfl_down_sync(0xffffffffu, incl, off, sw);
-        if ((lane & (sw - 1)) + off < sw) incl += y;
+        const float y0 = __shfl_down_sync(0xffffffffu, i0, off, sw);
+        const float y1 = __shfl_down_sync(0xffffffffu, i1, off, sw);
+        if ((lane & (sw - 1)) + off < sw) {
+            i0 += y0;
+            i1 += y1;
+        }
     }
-    float excl = __shfl_down_sync(0xffffffffu, incl, 1, sw);
-    if ((lane & (sw - 1)) == sw - 1) excl = 0.f;
-    if (N <= 32) return excl;
-    if (lane == 0) xw[warp * 8 + slot] = incl;
-    __syncthreads();
-    const int wpr = N >> 5;
-    const int w0 = warp - (warp % wpr);
-    float carry = 0.f;
-    for (int w = warp + 1; w < w0 + wpr; ++w) carry += xw[w * 8 + slot];
-    __syncthreads();
-    return carry + excl;
-}
-
-__device__ __forceinline__ float ray_sum(float x, int N, float* xw, int slot) {
-    float tot;
-    ray_scan_excl<false>(x, N, xw, slot, tot);
-    return tot;
+    float e0 = __shfl_down_sync(0xffffffffu, i0, 1, sw);
+    float e1 = __shfl_down_sync(0xffffffffu, i1, 1, sw);
+    if ((lane & (sw - 1)) == sw - 1) e0 = e1 = 0.f;
+    if (N > 32) {
+        if (lane == 0) {
+            xw[mw * 8 + 6] = i0;
+            xw[mw * 8 + 7] = i1;
+        }
+        tc::bar_sync(BAR_M, NM);
+        const int wpr = N >> 5, w0 = mw - (mw % wpr);
+        for (int w = mw + 1; w < w0 + wpr; ++w) {
+            e0 += xw[w * 8 + 6];
+            e1 += xw[w * 8 + 7];
+        }
+    }
+    s0 = e0;
+    s1 = e1;
 }
 
 // ---------------------------------------------------------------------------
-// copy one object's fp16 weights into the interleaved smem layout
-__device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, const CfgDev& cfg) {
-    const int LF = cfg.LF;
-    struct L { int off, rows, cols, srows, smem; };
-    const L ls[5] = {{cfg.w_off[0], 64, LF, 64, OFF_W1}, {cfg.w_off[1], 16, 64, 16, OFF_W2},
-                     {cfg.w_off[2], 64, 32, 64, OFF_W3}, {cfg.w_off[3], 64, 64, 64, OFF_W4},
-                     {cfg.w_off[4], 3, 64, 16, OFF_W5}};
+// copy one object's fp16 weights into the interleaved smem layout (M threads)
+__device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, const CfgDev& cfg, int LF) {
+    struct Lw { int off, rows, cols, srows, smem; };
+    const Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, OFF_W1}, {cfg.w_off[1], 16, 64, 16, OFF_W2},
+                      {cfg.w_off[2], 64, 32, 64, OFF_W3}, {cfg.w_off[3], 64, 64, 64, OFF_W4},
+                      {cfg.w_off[4], 3, 64, 16, OFF_W5}};
+    const int m = threadIdx.x - NG;
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
         const int chunks = ls[k].srows * (ls[k].cols / 8);
-        for (int q = threadIdx.x; q < chunks; q += NT) {
-            int r = q / (ls[k].cols / 8), cb = q % (ls[k].cols / 8);
+        for (int q = m; q < chunks; q += NM) {
+            const int r = q / (ls[k].cols / 8), cb = q % (ls[k].cols / 8);
             uint4 v = make_uint4(0, 0, 0, 0);
             if (r < ls[k].rows) {
                 // weights are only 4-byte aligned in general: load as 4 x half2
@@ -165,56 +217,50 @@ __device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, co
     }
 }
 
-// flush dW accumulators (TMEM) and loss sums of one object; warpgroup 0 takes
-// dW1, dW2, dW5, warpgroup 1 takes dW3, dW4
-__device__ void flush_object(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* misc, double* loss_acc,
-                             int slot, bool have_dw) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wg = threadIdx.x >> 7;
-    const int q = warp & 3;
+// flush the dW accumulators (TMEM) and loss sums of one object (M threads).
+// M=64 accumulators: row i lives in TMEM lane 32 (i / 16) + i % 16.
+template <int LF>
+__device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* misc, double* loss_acc, int slot,
+                        bool have_dw) {
+    const int m = threadIdx.x - NG, mw = m >> 5, lane = m & 31;
     const float inv = 1.0f / cfg.loss_scale;
     float* gm = ob.g32 + cfg.n_table;
     if (have_dw) {
-        const int row = q * 16 + lane;   // M=64 accumulator row held by this lane (lanes < 16)
+        const int row = mw * 16 + lane;
+        const bool on = lane < 16;
         float v[16];
-        if (wg == 0) {
-            for (int c0 = 0; c0 < cfg.LF; c0 += 16) {
-                tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW1 + c0), v);
-                tc::tmem_wait_ld();
-                if (lane < 16)
-                    for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[0] + row * cfg.LF + c0 + i, v[i] * inv);
-            }
-            // dW2^T [64 in x 16 out], dW5^T [64 in x 16 (3) out]: row = input feature
-            tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW2), v);
-            tc::tmem_wait_ld();
-            if (lane < 16)
-                for (int o = 0; o < 16; ++o) red_add_f1(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
-            tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW5), v);
-            tc::tmem_wait_ld();
-            if (lane < 16)
-                for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
-        } else {
-            for (int c0 = 0; c0 < 32; c0 += 16) {
-                tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW3 + c0), v);
-                tc::tmem_wait_ld();
-                if (lane < 16)
-                    for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[2] + row * 32 + c0 + i, v[i] * inv);
-            }
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-                tc::tmem_ld16(tc::taddr(tm, q * 32, TM_DW4 + c0), v);
-                tc::tmem_wait_ld();
-                if (lane < 16)
-                    for (int i = 0; i < 16; ++i) red_add_f1(gm + cfg.w_off[3] + row * 64 + c0 + i, v[i] * inv);
-            }
-        }
+        auto rows4 = [&](int col, float* dst) {   // 16 contiguous columns of row `row`
+            tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, col), v);
+            if (on)
+#pragma unroll
+                for (int k = 0; k < 16; k += 4)
+                    red_add_f4(reinterpret_cast<float4*>(dst + k), v[k] * inv, v[k + 1] * inv, v[k + 2] * inv,
+                               v[k + 3] * inv);
+        };
+#pragma unroll
+        for (int c0 = 0; c0 < LF; c0 += 16) rows4(TM_DW1 + c0, gm + cfg.w_off[0] + row * LF + c0);
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += 16) rows4(TM_DW3 + c0, gm + cfg.w_off[2] + row * 32 + c0);
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) rows4(TM_DW4 + c0, gm + cfg.w_off[3] + row * 64 + c0);
+        // dW2^T [64 in x 16 out], dW5^T [64 in x 16 (3) out]: row = input feature
+        tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, TM_DW2), v);
+        if (on)
+#pragma unroll
+            for (int o = 0; o < 16; ++o) red_add_f1(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
+        tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, TM_DW5), v);
+        if (on)
+#pragma unroll
+            for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
     }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        float l = misc->loss[threadIdx.x];
-        if (l != 0.f) atomicAdd(loss_acc + 4 * slot + threadIdx.x, (double)l);
-        misc->loss[threadIdx.x] = 0.f;
+    tc::bar_sync(BAR_M, NM);
+    if (m < 4) {
+        const float l = misc->loss[m];
+        if (l != 0.f) atomicAdd(loss_acc + 4 * slot + m, (double)l);
+        misc->loss[m] = 0.f;
     }
     tc::fence_before();
-    __syncthreads();
+    tc::bar_sync(BAR_M, NM);
     tc::fence_after();
 }
 
@@ -224,153 +270,187 @@ __device__ __forceinline__ void st16(uint8_t* buf, int r, int c0, int C, const f
     tc::st_chunk(buf, r, c0 + 8, C, v + 8);
 }
 
-// epilogue of a 64-wide layer: this warpgroup's 32 columns, ReLU (or mask) ->
-// fp16 -> smem; `relu` records the mask, otherwise `mask` is applied
-template <bool RELU>
-__device__ __forceinline__ void epi32(uint32_t wk, int wg, uint8_t* buf, int r, uint32_t& mask) {
+// forward epilogue of a 64-wide layer (M thread, row r): TMEM -> fp16 ->
+// ReLU on packed halves (relu(round(v)) = round(relu(v))) -> smem
+__device__ __forceinline__ void epi_relu64(uint32_t wk, uint8_t* buf, int r) {
+    const __half2 z = __float2half2_rn(0.f);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const int c0 = 32 * wg + 16 * h;
-        float v[16];
-        tc::tmem_ld16(wk + c0, v);
-        tc::tmem_wait_ld();
+        float v[32];
+        tc::tmem_ld32_sync(wk + 32 * h, v);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const uint32_t bit = 1u << (16 * h + k);
-            if (RELU) {
-                if (v[k] > 0.f) mask |= bit; else v[k] = 0.f;
-            } else if (!(mask & bit)) {
-                v[k] = 0.f;
-            }
+        for (int c = 0; c < 4; ++c) {
+            __half2 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = __hmax2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), z);
+            *reinterpret_cast<uint4*>(buf + tc::il_offset(r, 32 * h + 8 * c, 64)) = *reinterpret_cast<uint4*>(q);
         }
-        st16(buf, r, c0, 64, v);
     }
 }
 
-}  // namespace
-
-__global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev* __restrict__ objs,
-                                                       const RayRec* __restrict__ rays, int n_tiles,
-                                                       int tiles_per_cta, double* __restrict__ loss_acc,
-                                                       int* __restrict__ nonfinite, float* __restrict__ dbg) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    Misc* misc = reinterpret_cast<Misc*>(smem + OFF_MISC);
-    const int t = threadIdx.x, warp = t >> 5, wg = t >> 7;
-    const int r = t & (TILE - 1);                 // sample row of the tile = TMEM lane
-    const int N = cfg.N, LF = cfg.LF;
-    const float scale = cfg.loss_scale, inv_scale = 1.0f / cfg.loss_scale;
-
-    if (warp == 0) tc::tmem_alloc(&misc->tmem, TM_COLS);
-    if (t == 0) {
-        tc::mbar_init(&misc->mbar, 1);
-        tc::fence_mbar_init();
-    }
-    if (t < 4) misc->loss[t] = 0.f;
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const uint32_t tm = misc->tmem;
-    const uint32_t wk = tc::taddr(tm, (warp & 3) * 32, 0);   // this warp's TMEM lanes, column 0
-    uint32_t phase = 0;
-    const uint32_t sW1 = tc::smem_u32(smem + OFF_W1), sW2 = tc::smem_u32(smem + OFF_W2),
-                   sW3 = tc::smem_u32(smem + OFF_W3), sW4 = tc::smem_u32(smem + OFF_W4),
-                   sW5 = tc::smem_u32(smem + OFF_W5), sX0 = tc::smem_u32(smem + OFF_X0),
-                   sH1 = tc::smem_u32(smem + OFF_H1), sCIN = tc::smem_u32(smem + OFF_CIN),
-                   sG1 = tc::smem_u32(smem + OFF_G1), sG2 = tc::smem_u32(smem + OFF_G2),
-                   sDC = tc::smem_u32(smem + OFF_DC), sDR = tc::smem_u32(smem + OFF_DR),
-                   sDB = tc::smem_u32(smem + OFF_DB);
-    uint8_t* X0 = smem + OFF_X0;
-    uint8_t* H1 = smem + OFF_H1;
-    uint8_t* CIN = smem + OFF_CIN;
-    uint8_t* G1 = smem + OFF_G1;
-    uint8_t* G2 = smem + OFF_G2;
-    uint8_t* DC = smem + OFF_DC;
-    uint8_t* DR = smem + OFF_DR;
-    uint8_t* DB = smem + OFF_DB;
-    float* xw = &misc->xw[0][0];
-
-    auto mma_wait = [&]() {
-        tc::mbar_wait(&misc->mbar, phase);
-        phase ^= 1;
-        tc::fence_after();
-    };
-
-    const int tile0 = blockIdx.x * tiles_per_cta;
-    const int tile1 = min(tile0 + tiles_per_cta, n_tiles);
-    int cur = -1;
-    bool dw_fresh = true;
-    const int rays_per_tile = TILE / N;
-    const int LH = cfg.L >> 1;                    // hash levels per warpgroup
-    // per-object values held in registers (re-read only when the object changes)
-    const __half2* tab = nullptr;
-    float2* gt = nullptr;
-    float ob_a[3] = {0.f, 0.f, 0.f};
-    int ob_ray_begin = 0;
-    float invB = 0.f;
-    unsigned long long pre = 0;
-
-    for (int tile = tile0; tile < tile1; ++tile) {
-        const int slot = rays[tile * rays_per_tile].slot;
-        if (slot != cur) {
-            if (cur >= 0) flush_object(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
-            const ObjDev& ob = objs[slot];
-            load_weights(smem, ob.p16 + cfg.n_table, cfg);
-            cur = slot;
-            dw_fresh = true;
-            tab = reinterpret_cast<const __half2*>(ob.p16);
-            gt = reinterpret_cast<float2*>(ob.g32);
-            ob_a[0] = ob.a[0];
-            ob_a[1] = ob.a[1];
-            ob_a[2] = ob.a[2];
-            ob_ray_begin = ob.ray_begin;
-            invB = 1.0f / (float)ob.n_rays;
-            pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1);
+// backward epilogue: dX (TMEM) masked by the ReLU derivative of the forward
+// activation `act` (its fp16 ReLU output in smem: relu' = act > 0) -> fp16 -> smem
+__device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint8_t* act, int r) {
+    const __half2 z = __float2half2_rn(0.f);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        float v[32];
+        tc::tmem_ld32_sync(wk + 32 * h, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t off = tc::il_offset(r, 32 * h + 8 * c, 64);
+            uint4 a4 = *reinterpret_cast<const uint4*>(act + off);
+            const __half2* a = reinterpret_cast<const __half2*>(&a4);
+            __half2 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                q[k] = __hmul2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), __hgt2(a[k], z));
+            *reinterpret_cast<uint4*>(out + off) = *reinterpret_cast<uint4*>(q);
         }
-        const long long s = (long long)tile * TILE + r;
-        const int ray = (int)(s / N);
-        const int i = (int)(s - (long long)ray * N);
-        const RayRec rr = rays[ray];
-        const bool active = (rr.flags & RF_ACTIVE) != 0;
+    }
+}
 
-        // ---- a2/a3: sample + encode (fp16 table gathers, fp32 interpolation)
-        float dist = 0.f, delta = 0.f, u[3] = {0.f, 0.f, 0.f};
-        if (active) sample_geometry(rr, i, N, pre, ray - ob_ray_begin, ob_a, dist, delta, u);
-        {
-            float f8[8];
+// cell and the 8 corner entries (relative to the level block) of one level
+// (R5): P = {res, y multiplier, z multiplier, dense}; dense: x + (N+1) y +
+// (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^ z * 805459861) & (T - 1).
+// Corner b: bit k -> +1 on axis k.
+__device__ __forceinline__ void level_entries(const float u[3], const int4 P, unsigned hmask, Cell& cl, int (&e)[8]) {
+    cl = grid_cell(u, P.x);
+    const unsigned my = (unsigned)P.y, mz = (unsigned)P.z;
+    const unsigned x0 = (unsigned)cl.c[0], x1 = x0 + 1u;
+    const unsigned ty0 = (unsigned)cl.c[1] * my, ty1 = ty0 + my;
+    const unsigned tz0 = (unsigned)cl.c[2] * mz, tz1 = tz0 + mz;
+    if (P.w) {
+        const unsigned yz[4] = {ty0 + tz0, ty1 + tz0, ty0 + tz1, ty1 + tz1};
 #pragma unroll
-            for (int lp = 0; lp < ROMAP_MAX_LEVELS / 2; lp += 2) {
-                if (lp >= LH) break;
-                // x-neighbour corners (b, b|1) share a 16-byte chunk of the fp16 table in
-                // 3 of 4 cases (dense: entries e, e+1; hashed: e ^ (x ^ (x+1)) with the
-                // x prime = 1), so each corner pair costs one 16-B gather (+ a 4-B one
-                // otherwise); level blocks are 16-entry aligned (R5).
-                uint4 qv[2][4];
-                uint32_t xv[2][4];
-                int e0[2][4], e1[2][4];
-                Cell cl[2];
+        for (int k = 0; k < 4; ++k) {
+            e[2 * k] = (int)(x0 + yz[k]);
+            e[2 * k + 1] = (int)(x1 + yz[k]);
+        }
+    } else {
+        const unsigned yz[4] = {ty0 ^ tz0, ty1 ^ tz0, ty0 ^ tz1, ty1 ^ tz1};
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int l = wg * LH + lp + q;
-                    const int res = cfg.res[l];
-                    cl[q] = grid_cell(u, res);
-                    const __half2* tb = tab + cfg.off[l];
+        for (int k = 0; k < 4; ++k) {
+            e[2 * k] = (int)((x0 ^ yz[k]) & hmask);
+            e[2 * k + 1] = (int)((x1 ^ yz[k]) & hmask);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// G: gathers of tile `it` interleaved with the scatter of tile `it - 2`
+// (warpgroup WG owns levels [WG L/2, (WG + 1) L/2); one code path for both
+// warpgroups, level loop not unrolled: the body stays in the instruction cache)
+template <int L>
+__device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
+                                       const RayRec* __restrict__ rays, const float4* __restrict__ srec, int tile0,
+                                       int n, uint8_t* smem, Misc* misc, uint32_t tm) {
+    constexpr int LH = L / 2;                 // levels of this warpgroup
+    constexpr int LF = 2 * L;
+    const int t = threadIdx.x, r = t & (TILE - 1), lane = t & 31, q4 = (t >> 5) & 3, WG = t >> 7;
+    const int N = cfg.N;
+    const unsigned hmask = (unsigned)cfg.T - 1u;
+    const float inv_scale = 1.0f / cfg.loss_scale;
+    const uint32_t df_lane = tc::taddr(tm, q4 * 32, TM_DF);
+
+    float4 u_next = srec[(long long)tile0 * TILE + r];
+    int slot_next = rays[(int)(((long long)tile0 * TILE) / N)].slot;
+    int slot_tab = -1;
+    const __half2* tab = nullptr;
+    float2* g_cur = nullptr;
+    float um1[3] = {-1.f, -1.f, -1.f}, um2[3] = {-1.f, -1.f, -1.f};
+    float2* g_m1 = nullptr;
+    float2* g_m2 = nullptr;
+
+    for (int it = 0; it < n + 2; ++it) {
+        const bool dg = it < n, ds = it >= 2;
+        const int b = it & 1;
+        const float ug[3] = {u_next.x, u_next.y, u_next.z};
+        const int slot_g = slot_next;
+        if (it + 1 < n) {
+            u_next = srec[(long long)(tile0 + it + 1) * TILE + r];
+            slot_next = rays[(int)(((long long)(tile0 + it + 1) * TILE) / N)].slot;
+        }
+        if (dg && slot_g != slot_tab) {
+            tab = reinterpret_cast<const __half2*>(objs[slot_g].p16);
+            g_cur = reinterpret_cast<float2*>(objs[slot_g].g32);
+            slot_tab = slot_g;
+        }
+        if (ds) {                                     // dfeat of tile it-2 is in DF[b]
+            tc::mbar_wait(&misc->tile_done[b], ((it - 2) >> 1) & 1);
+            tc::fence_after();
+        }
+        const bool ag = dg && ug[0] >= 0.f;          // sample of an active ray (k_raygen_samples)
+        const bool as = ds && um2[0] >= 0.f;
+        uint8_t* X0 = smem + OFF_X0 + b * X0_BYTES;
+#pragma unroll 1
+        for (int lp = 0; lp < LH; lp += 2) {
+            const int l = WG * LH + lp;
+            const int4 P[2] = {misc->lv[l], misc->lv[l + 1]};
+            const int off[2] = {misc->lvoff[l], misc->lvoff[l + 1]};
+            // (1) gathers of levels l, l+1 of tile it.  x-neighbour corners (b, b|1)
+            // share a 16-byte chunk of the fp16 table in 3 of 4 cases (dense:
+            // entries e, e+1; hashed: e ^ (x ^ (x+1)) with the x prime = 1), so each
+            // corner pair is one 16-B gather (+ a 4-B one otherwise); level blocks
+            // are 16-entry aligned (R5).
+            uint4 qv[2][4];
+            uint32_t xv[2][4];
+            int e[2][8];
+            Cell cl[2];
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        e0[q][p] = corner_entry(cl[q], 2 * p, res, cfg.dense[l], cfg.T);
-                        e1[q][p] = corner_entry(cl[q], 2 * p + 1, res, cfg.dense[l], cfg.T);
-                        const bool same = (e0[q][p] >> 2) == (e1[q][p] >> 2);
-                        qv[q][p] = active ? ldg_v4(tb + (e0[q][p] & ~3)) : make_uint4(0, 0, 0, 0);
-                        xv[q][p] = (active && !same) ? ldg_u32(tb + e1[q][p]) : 0u;
+            for (int q = 0; q < 2; ++q) {
+                level_entries(ug, P[q], hmask, cl[q], e[q]);
+                const __half2* tb = tab + off[q];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
+                    qv[q][p] = ag ? ldg_v4(tb + (e[q][2 * p] & ~3)) : make_uint4(0, 0, 0, 0);
+                    xv[q][p] = (ag && !same) ? ldg_u32(tb + e[q][2 * p + 1]) : 0u;
+                }
+            }
+            // (2) scatter of the same levels of tile it-2 (fire-and-forget REDs)
+            if (ds) {
+                float g[4];
+                tc::tmem_ld4_sync(df_lane + 32 * b + 2 * l, g);
+                if (as) {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        Cell cs;
+                        int es[8];
+                        level_entries(um2, P[q], hmask, cs, es);
+                        const float g0 = g[2 * q] * inv_scale, g1 = g[2 * q + 1] * inv_scale;
+                        float2* gl = g_m2 + off[q];
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) {
+                            // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
+                            // REDG.F32x4, else two REDG.F32x2
+                            const int ea = es[2 * p], eb = es[2 * p + 1];
+                            const float wa = corner_weight(cs, 2 * p), wb = corner_weight(cs, 2 * p + 1);
+                            if ((ea >> 1) == (eb >> 1)) {
+                                if (ea < eb)
+                                    red_add_f4(reinterpret_cast<float4*>(gl + ea), wa * g0, wa * g1, wb * g0, wb * g1);
+                                else
+                                    red_add_f4(reinterpret_cast<float4*>(gl + eb), wb * g0, wb * g1, wa * g0, wa * g1);
+                            } else {
+                                red_add_f2(gl + ea, wa * g0, wa * g1);
+                                red_add_f2(gl + eb, wb * g0, wb * g1);
+                            }
+                        }
                     }
                 }
+            }
+            // (3) interpolate the gathered corners -> 4 features (2 levels) -> X0[b]
+            if (dg) {
+                float f[4];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     float a0 = 0.f, a1 = 0.f;
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
-                        const bool same = (e0[q][p] >> 2) == (e1[q][p] >> 2);
-                        const uint32_t h0 = sel4(qv[q][p], e0[q][p] & 3);
-                        const uint32_t h1 = same ? sel4(qv[q][p], e1[q][p] & 3) : xv[q][p];
+                        const int ea = e[q][2 * p], eb = e[q][2 * p + 1];
+                        const bool same = (ea >> 2) == (eb >> 2);
+                        const uint32_t h0 = sel4(qv[q][p], ea & 3);
+                        const uint32_t h1 = same ? sel4(qv[q][p], eb & 3) : xv[q][p];
                         const float w0 = corner_weight(cl[q], 2 * p), w1 = corner_weight(cl[q], 2 * p + 1);
                         const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
                         const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
@@ -379,131 +459,212 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
                         a0 += w1 * f1.x;
                         a1 += w1 * f1.y;
                     }
-                    f8[2 * ((lp + q) & 3)] = a0;
-                    f8[2 * ((lp + q) & 3) + 1] = a1;
+                    f[2 * q] = a0;
+                    f[2 * q + 1] = a1;
                 }
-                if ((lp & 3) == 2) tc::st_chunk(X0, r, 2 * (wg * LH + lp - 2), LF, f8);
-            }
-            if (wg == 1) {
-                float sh[16];
-                sh4(rr.d, sh);
-                st16(CIN, r, 16, 32, sh);
+                __half2 hq[2] = {__floats2half2_rn(f[0], f[1]), __floats2half2_rn(f[2], f[3])};
+                *reinterpret_cast<uint2*>(X0 + tc::il_offset(r, 2 * l, LF)) = *reinterpret_cast<uint2*>(hq);
             }
         }
-        sync_for_mma();
+        if (ds) {                                     // DF[b] read: M may overwrite it (tile it)
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&misc->df_empty[b]);
+        }
+        if (dg) {
+            tc::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&misc->x0_full[b]);
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            um2[k] = um1[k];
+            um1[k] = dg ? ug[k] : -1.f;
+        }
+        g_m2 = g_m1;
+        g_m1 = g_cur;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// M: SH + MLP forward + render/loss + MLP backward of tile j
+template <int L>
+__device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
+                                       const RayRec* __restrict__ rays, const float4* __restrict__ srec,
+                                       const float* __restrict__ sdelta, int tile0, int n, uint8_t* smem, Misc* misc,
+                                       uint32_t tm, double* __restrict__ loss_acc, int* __restrict__ nonfinite,
+                                       float* __restrict__ dbg) {
+    constexpr int LF = 2 * L;
+    const int m = threadIdx.x - NG, mw = m >> 5;
+    const bool leader = m == 0;
+    const int N = cfg.N;
+    const float scale = cfg.loss_scale;
+    const uint32_t wk = tc::taddr(tm, mw * 32, TM_WK);
+    const uint32_t sW1 = tc::smem_u32(smem + OFF_W1), sW2 = tc::smem_u32(smem + OFF_W2),
+                   sW3 = tc::smem_u32(smem + OFF_W3), sW4 = tc::smem_u32(smem + OFF_W4),
+                   sW5 = tc::smem_u32(smem + OFF_W5), sH1 = tc::smem_u32(smem + OFF_H1),
+                   sCIN = tc::smem_u32(smem + OFF_CIN), sG1 = tc::smem_u32(smem + OFF_G1),
+                   sG2 = tc::smem_u32(smem + OFF_G2), sDC = tc::smem_u32(smem + OFF_DC),
+                   sDR = tc::smem_u32(smem + OFF_DR), sDB = tc::smem_u32(smem + OFF_DB);
+    uint8_t* H1 = smem + OFF_H1;
+    uint8_t* CIN = smem + OFF_CIN;
+    uint8_t* G1 = smem + OFF_G1;
+    uint8_t* G2 = smem + OFF_G2;
+    uint8_t* DC = smem + OFF_DC;
+    uint8_t* DR = smem + OFF_DR;
+    uint8_t* DB = smem + OFF_DB;
+    float* xw = &misc->xw[0][0];
+    uint32_t phase = 0;
+    auto mma_wait = [&]() {
+        tc::mbar_wait(&misc->mbar_mma, phase);
+        phase ^= 1;
+        tc::fence_after();
+    };
+
+    int cur = -1;
+    bool dw_fresh = true;
+    float invB = 0.f;
+    for (int j = 0; j < n; ++j) {
+        const int tile = tile0 + j, b = j & 1;
+        const long long s = (long long)tile * TILE + m;
+        const int ray = (int)(s / N);
+        const int i = (int)(s - (long long)ray * N);
+        const RayRec rr = rays[ray];
+        const float4 sr = srec[s];
+        const float delta = sdelta[s];
+        const bool active = (rr.flags & RF_ACTIVE) != 0;
+        if (rr.slot != cur) {                      // uniform: a tile holds rays of one object
+            if (cur >= 0) {
+                // every MMA of the previous tile (they read W and write dW) has completed
+                tc::mbar_wait(&misc->tile_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                tc::fence_after();
+                m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
+            }
+            const ObjDev& ob = objs[rr.slot];
+            load_weights(smem, ob.p16 + cfg.n_table, cfg, LF);
+            cur = rr.slot;
+            dw_fresh = true;
+            invB = 1.0f / (float)ob.n_rays;
+        }
+        {
+            float sh[16];
+            sh4(rr.d, sh);
+            st16(CIN, m, 16, 32, sh);
+        }
+        tc::mbar_wait(&misc->x0_full[b], (j >> 1) & 1);
+        m_sync_for_mma();
+        const uint32_t sX0 = tc::smem_u32(smem + OFF_X0 + b * X0_BYTES);
 
         // ---- a4: MLP forward
         // L1: WK[128 x 64] = X0[128 x LF] . W1^T
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < LF / 16; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sX0, LF, ks), tc::desc_kmajor(sW1, LF, ks),
                             tc::idesc_f16(128, 64, false, false), ks > 0);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        uint32_t m_h1 = 0, m_g1 = 0, m_g2 = 0;
-        epi32<true>(wk, wg, H1, r, m_h1);
-        sync_for_mma();
+        epi_relu64(wk, H1, m);
+        m_sync_for_mma();
         // L2: WK[128 x 16] = H1 . W2^T
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < 4; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sH1, 64, ks), tc::desc_kmajor(sW2, 64, ks),
                             tc::idesc_f16(128, 16, false, false), ks > 0);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
         float sigma, r0;
         {
             float v[16];
-            tc::tmem_ld16(wk, v);
-            tc::tmem_wait_ld();
+            tc::tmem_ld16_sync(wk, v);
             r0 = v[0];
             sigma = density_act(r0, cfg.density_act);
-            if (wg == 0) st16(CIN, r, 0, 32, v);
+            st16(CIN, m, 0, 32, v);
         }
-        sync_for_mma();
+        m_sync_for_mma();
         // L3: WK = CIN . W3^T
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < 2; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sCIN, 32, ks), tc::desc_kmajor(sW3, 32, ks),
                             tc::idesc_f16(128, 64, false, false), ks > 0);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi32<true>(wk, wg, G1, r, m_g1);
-        sync_for_mma();
+        epi_relu64(wk, G1, m);
+        m_sync_for_mma();
         // L4: WK = G1 . W4^T
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < 4; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sG1, 64, ks), tc::desc_kmajor(sW4, 64, ks),
                             tc::idesc_f16(128, 64, false, false), ks > 0);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi32<true>(wk, wg, G2, r, m_g2);
-        sync_for_mma();
+        epi_relu64(wk, G2, m);
+        m_sync_for_mma();
         // L5: WK[128 x 16] = G2 . W5^T (rows 3..15 of W5 are zero)
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < 4; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sG2, 64, ks), tc::desc_kmajor(sW5, 64, ks),
                             tc::idesc_f16(128, 16, false, false), ks > 0);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
         float c[3];
         {
             float v[16];
-            tc::tmem_ld16(wk, v);
-            tc::tmem_wait_ld();
+            tc::tmem_ld16_sync(wk, v);
 #pragma unroll
             for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[k]));
         }
 
-        // ---- a5: volume rendering + loss + render backward (both warpgroups,
-        // redundantly, so every thread holds dL/dsigma and dL/dc of its sample)
+        // ---- a5: volume rendering + loss + render backward
+        const float dist = sr.w;
         const float x = active ? sigma * delta : 0.f;
         const float alpha = expf(-x);
         const float o = -expm1f(-x);
         float TN;
-        const float Ti = ray_scan_excl<true>(alpha, N, xw, 0, TN);
+        const float Ti = m_scan_mul(alpha, N, xw, TN);
         const float w = active ? Ti * o : 0.f;
-        const float Cs0 = ray_sum(w * c[0], N, xw, 1);
-        const float Cs1 = ray_sum(w * c[1], N, xw, 2);
-        const float Cs2 = ray_sum(w * c[2], N, xw, 3);
-        const float D = ray_sum(w * dist, N, xw, 4);
-        const float ssum = ray_sum(active ? sigma : 0.f, N, xw, 5);
+        float sums[5] = {w * c[0], w * c[1], w * c[2], w * dist, active ? sigma : 0.f};
+        m_ray_sums<5>(sums, N, xw);
         float dsig = 0.f, dcol[3] = {0.f, 0.f, 0.f};
         float gC[3] = {0.f, 0.f, 0.f};
         float gD = 0.f, gCb = 0.f;
         const int cls = rr.flags & RF_CLS_MASK;
         if (active) {
             const bool has_depth = (rr.flags & RF_HAS_DEPTH) != 0;
-            const float Cs[3] = {Cs0, Cs1, Cs2};
             float e[3], bgc[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 bgc[k] = (cls == CLS_OBJ && cfg.obj_bg == 1) ? 0.f : rr.bg[k];
-                e[k] = Cs[k] + TN * bgc[k] - (cls == CLS_OBJ ? rr.tgt[k] : rr.bg[k]);
+                e[k] = sums[k] + TN * bgc[k] - (cls == CLS_OBJ ? rr.tgt[k] : rr.bg[k]);
             }
             const float ne = sqrtf(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
 #pragma unroll
             for (int k = 0; k < 3; ++k) gC[k] = ne > 0.f ? e[k] / ne * invB : 0.f;
             float ed = 0.f;
             if (has_depth) {
-                ed = D - rr.depth;
+                ed = sums[3] - rr.depth;
                 gD = ed > 0.f ? cfg.lambda_depth * invB : (ed < 0.f ? -cfg.lambda_depth * invB : 0.f);
             }
             gCb = gC[0] * bgc[0] + gC[1] * bgc[1] + gC[2] * bgc[2];
-            if (i == 0 && wg == 0) {
+            if (i == 0) {
                 atomicAdd(&misc->loss[cls == CLS_OBJ ? 0 : 1], ne);
                 if (has_depth) atomicAdd(&misc->loss[2], fabsf(ed));
-                if (cls == CLS_BG) atomicAdd(&misc->loss[3], ssum);
-                if (!isfinite(ne) || !isfinite(ssum)) atomicOr(nonfinite, 1);
+                if (cls == CLS_BG) atomicAdd(&misc->loss[3], sums[4]);
+                if (!isfinite(ne) || !isfinite(sums[4])) atomicOr(nonfinite, 1);
             }
         }
         const float gc = gC[0] * c[0] + gC[1] * c[1] + gC[2] * c[2];
-        const float S = ray_suffix_excl(w * gc, N, xw, 6);
-        const float Sd = ray_suffix_excl(w * dist, N, xw, 7);
+        float S, Sd;
+        m_suffix2(w * gc, w * dist, N, xw, S, Sd);
         if (active) {
             const float Tn1 = Ti * alpha;
             dsig = delta * (Tn1 * gc - S - TN * gCb) + delta * gD * (Tn1 * dist - Sd) +
@@ -511,150 +672,174 @@ __global__ void __launch_bounds__(NT, 2) k_fused_mixed(CfgDev cfg, const ObjDev*
 #pragma unroll
             for (int k = 0; k < 3; ++k) dcol[k] = w * gC[k];
         }
-        if (dbg && wg == 0) *reinterpret_cast<float4*>(dbg + 4 * s) = make_float4(dsig, dcol[0], dcol[1], dcol[2]);
+        if (dbg) *reinterpret_cast<float4*>(dbg + 4 * s) = make_float4(dsig, dcol[0], dcol[1], dcol[2]);
 
         // ---- a6: MLP backward (scaled by loss_scale)
-        if (wg == 0) {
+        {
             float v[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k) v[k] = 0.f;
 #pragma unroll
             for (int k = 0; k < 3; ++k) v[k] = dcol[k] * c[k] * (1.f - c[k]) * scale;
-            st16(DC, r, 0, 16, v);
+            st16(DC, m, 0, 16, v);
         }
         const float dr0_extra = dsig * density_act_grad(r0, sigma, cfg.density_act) * scale;
-        sync_for_mma();
+        m_sync_for_mma();
         // B5: WK[128 x 64] = DC[128 x 16] . W5[16 x 64];  dW5^T[64 x 16] += G2^T . DC
-        if (t == 0) {
+        if (leader) {
             tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDC, 16, 0), tc::desc_mnmajor(sW5, 64, 0),
                         tc::idesc_f16(128, 64, false, true), 0);
+#pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW5, tc::desc_mnmajor(sG2, 64, ks), tc::desc_mnmajor(sDC, 16, ks),
                             tc::idesc_f16(64, 16, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi32<false>(wk, wg, DB, r, m_g2);
-        sync_for_mma();
+        epi_mask64(wk, DB, G2, m);
+        m_sync_for_mma();
         // B4: WK = DB(dg2) . W4;  dW4[64 x 64] += DB^T . G1
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < 4; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW4, 64, ks),
                             tc::idesc_f16(128, 64, false, true), ks > 0);
+#pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW4, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sG1, 64, ks),
                             tc::idesc_f16(64, 64, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi32<false>(wk, wg, DB, r, m_g1);
-        sync_for_mma();
+        epi_mask64(wk, DB, G1, m);
+        m_sync_for_mma();
         // B3: WK[128 x 16] = DB(dg1) . W3[:, 0:16];  dW3[64 x 32] += DB^T . CIN
-        if (t == 0) {
+        if (leader) {
+#pragma unroll
             for (int ks = 0; ks < 4; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW3, 32, ks),
                             tc::idesc_f16(128, 16, false, true), ks > 0);
+#pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW3, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sCIN, 32, ks),
                             tc::idesc_f16(64, 32, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        if (wg == 0) {
+        {
             float v[16];
-            tc::tmem_ld16(wk, v);
-            tc::tmem_wait_ld();
+            tc::tmem_ld16_sync(wk, v);
             v[0] += dr0_extra;
             if (!active)
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
-            st16(DR, r, 0, 16, v);
+            st16(DR, m, 0, 16, v);
         }
-        sync_for_mma();
+        m_sync_for_mma();
         // B2: WK[128 x 64] = DR[128 x 16] . W2[16 x 64];  dW2^T[64 x 16] += H1^T . DR
-        if (t == 0) {
+        if (leader) {
             tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDR, 16, 0), tc::desc_mnmajor(sW2, 64, 0),
                         tc::idesc_f16(128, 64, false, true), 0);
+#pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW2, tc::desc_mnmajor(sH1, 64, ks), tc::desc_mnmajor(sDR, 16, ks),
                             tc::idesc_f16(64, 16, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi32<false>(wk, wg, DB, r, m_h1);
-        sync_for_mma();
-        // B1: WK[128 x LF] = DB(dh1) . W1[64 x LF];  dW1[64 x LF] += DB^T . X0
-        if (t == 0) {
+        epi_mask64(wk, DB, H1, m);
+        m_sync_for_mma();
+        // B1: DF[b][128 x LF] = DB(dh1) . W1[64 x LF];  dW1[64 x LF] += DB^T . X0[b]
+        // (DF[b] must have been read by G: scatter of tile j-2)
+        if (leader) {
+            if (j >= 2) tc::mbar_wait(&misc->df_empty[b], ((j - 2) >> 1) & 1);
+            tc::fence_after();
+#pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-                tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW1, LF, ks),
+                tc::mma_f16(tm + TM_DF + 32 * b, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW1, LF, ks),
                             tc::idesc_f16(128, LF, false, true), ks > 0);
+#pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW1, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sX0, LF, ks),
                             tc::idesc_f16(64, LF, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar);
+            tc::commit(&misc->tile_done[b]);
         }
-        mma_wait();
         dw_fresh = false;
-
-        // ---- a7: hash-grid backward, this warpgroup's levels (fp32 REDG.F32x2)
-        {
-            // dfeat of levels [wg*LH, wg*LH + LH) = accumulator columns [2*wg*LH, +2*LH)
-            float v[16];
-            tc::tmem_ld16(wk + 2 * wg * LH, v);
-            tc::tmem_wait_ld();
-            if (active) {
-#pragma unroll
-                for (int lq = 0; lq < 8; ++lq) {
-                    if (lq >= LH) break;
-                    const int l = wg * LH + lq;
-                    const int res = cfg.res[l];
-                    const Cell cl = grid_cell(u, res);
-                    const float g0 = v[2 * lq] * inv_scale, g1 = v[2 * lq + 1] * inv_scale;
-                    float2* gl = gt + cfg.off[l];
-#pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
-                        // REDG.F32x4, else two REDG.F32x2
-                        const int ea = corner_entry(cl, 2 * p, res, cfg.dense[l], cfg.T);
-                        const int eb = corner_entry(cl, 2 * p + 1, res, cfg.dense[l], cfg.T);
-                        const float wa = corner_weight(cl, 2 * p), wb = corner_weight(cl, 2 * p + 1);
-                        if ((ea >> 1) == (eb >> 1)) {
-                            if (ea < eb)
-                                red_add_f4(reinterpret_cast<float4*>(gl + ea), wa * g0, wa * g1, wb * g0, wb * g1);
-                            else
-                                red_add_f4(reinterpret_cast<float4*>(gl + eb), wb * g0, wb * g1, wa * g0, wa * g1);
-                        } else {
-                            red_add_f2(gl + ea, wa * g0, wa * g1);
-                            red_add_f2(gl + eb, wb * g0, wb * g1);
-                        }
-                    }
-                }
-            }
-        }
-        // all TMEM reads of WK done before the next tile's first MMA overwrites it
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
     }
-    if (cur >= 0) flush_object(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
+    if (cur >= 0) {
+        tc::mbar_wait(&misc->tile_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
+        tc::fence_after();
+        m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
+    }
+}
+
+}  // namespace
+
+template <int L>
+__global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev* __restrict__ objs,
+                                                       const RayRec* __restrict__ rays,
+                                                       const float4* __restrict__ srec,
+                                                       const float* __restrict__ sdelta, int n_tiles,
+                                                       int tiles_per_cta, double* __restrict__ loss_acc,
+                                                       int* __restrict__ nonfinite, float* __restrict__ dbg) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    Misc* misc = reinterpret_cast<Misc*>(smem + OFF_MISC);
+    const int t = threadIdx.x, warp = t >> 5;
+    if (warp == 0) tc::tmem_alloc(&misc->tmem, TM_COLS);
+    if (t == 32) {
+        tc::mbar_init(&misc->mbar_mma, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&misc->x0_full[b], 8);
+            tc::mbar_init(&misc->tile_done[b], 1);
+            tc::mbar_init(&misc->df_empty[b], 8);
+        }
+        tc::fence_mbar_init();
+    }
+    if (t < 4) misc->loss[t] = 0.f;
+    if (t < L) {
+        const int res = cfg.res[t];
+        const bool dense = cfg.dense[t] != 0;
+        const unsigned n1 = (unsigned)res + 1u;
+        misc->lv[t] = make_int4(res, (int)(dense ? n1 : 2654435761u), (int)(dense ? n1 * n1 : 805459861u), dense ? 1 : 0);
+        misc->lvoff[t] = cfg.off[t];
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tm = misc->tmem;
+    const int tile0 = blockIdx.x * tiles_per_cta;
+    const int n = min(tiles_per_cta, n_tiles - tile0);
+    if (n > 0) {
+        if (warp < 8)
+            g_loop<L>(cfg, objs, rays, srec, tile0, n, smem, misc, tm);
+        else
+            m_loop<L>(cfg, objs, rays, srec, sdelta, tile0, n, smem, misc, tm, loss_acc, nonfinite, dbg);
+    }
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc(tm, TM_COLS);
 }
 
-void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
-                        double* loss_acc, int* nonfinite, float* dbg) {
+void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
+                        const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
+                        float* dbg) {
     const long long S = (long long)n_rays * cfg.N;
     const int n_tiles = (int)(S / TILE);
     if (n_tiles == 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_fused_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_fused_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_fused_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         attr = true;
     }
-    int grid = 2 * lc.num_sms;
+    int grid = lc.num_sms;
     if (grid > n_tiles) grid = n_tiles;
     const int per = (n_tiles + grid - 1) / grid;
     grid = (n_tiles + per - 1) / per;
-    k_fused_mixed<<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, n_tiles, per, loss_acc, nonfinite, dbg);
+    if (cfg.L == 16)
+        k_fused_mixed<16><<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc,
+                                                            nonfinite, dbg);
+    else
+        k_fused_mixed<8><<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc,
+                                                           nonfinite, dbg);
 }

@@ -8,11 +8,11 @@
 // Thread per ray slot.  All geometry is bit-exact fp32 (romap_internal.cuh).
 #include "romap_internal.cuh"
 
-__global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
-                                                int total_slots, RayRec* __restrict__ rays,
-                                                unsigned long long* __restrict__ hit_count) {
-    int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= total_slots) return;
+// one ray slot g: object lookup, pixel draw, class, ray, slab test, targets,
+// background colour (R8-R14, R17); returns the object slot and whether the ray
+// is active (hit and supervised)
+__device__ __forceinline__ int make_ray_rec(const CfgDev& cfg, const ObjDev* __restrict__ objs, int n_objs, int g,
+                                            RayRec& rr, bool& active) {
     // object owning slot g (objects are sorted by ray_begin)
     int lo = 0, hi = n_objs - 1;
     while (lo < hi) {
@@ -21,14 +21,13 @@ __global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __rest
     }
     const ObjDev& ob = objs[lo];
     int r = g - ob.ray_begin;
-    RayRec rr;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { rr.o[k] = 0.f; rr.d[k] = 0.f; rr.tgt[k] = 0.f; rr.bg[k] = 0.f; }
     rr.tn = rr.tf = rr.depth = 0.f;
     rr.flags = 0;
     rr.slot = lo;
     rr.kf = rr.px = rr.py = -1;
-    bool active = false;
+    active = false;
     if (r < ob.n_rays) {
         long long t = *ob.step + 1;                       // the Adam step this iteration feeds (R13)
         unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, t);
@@ -74,8 +73,11 @@ __global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __rest
         rr.px = px;
         rr.py = py;
     }
-    rays[g] = rr;
-    // warp-aggregated hit counter per object slot
+    return lo;
+}
+
+// warp-aggregated hit counter per object slot
+__device__ __forceinline__ void count_hit(unsigned long long* hit_count, int lo, bool active) {
     unsigned m = __ballot_sync(__activemask(), active);
     if (active) {
         unsigned same = __match_any_sync(m, lo);
@@ -83,10 +85,62 @@ __global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __rest
     }
 }
 
+__global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
+                                                int total_slots, RayRec* __restrict__ rays,
+                                                unsigned long long* __restrict__ hit_count) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= total_slots) return;
+    RayRec rr;
+    bool active;
+    int lo = make_ray_rec(cfg, objs, n_objs, g, rr, active);
+    rays[g] = rr;
+    count_hit(hit_count, lo, active);
+}
+
+// mixed path: thread per SAMPLE.  The N threads of a ray rebuild its record
+// (identical loads, broadcast), thread i = 0 stores it and counts the hit, and
+// every thread stores its sample's geometry (R12, R6): srec[s] = (u, dist) with
+// u = (-1, -1, -1) for samples of inactive rays, sdelta[s] = delta.  Bit-exact
+// with the per-sample recomputation of the fp32 path (same device functions).
+__global__ void __launch_bounds__(128) k_raygen_samples(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
+                                                        int total_slots, RayRec* __restrict__ rays,
+                                                        float4* __restrict__ srec, float* __restrict__ sdelta,
+                                                        unsigned long long* __restrict__ hit_count) {
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int N = cfg.N;
+    const int g = (int)(s / N);
+    if (g >= total_slots) return;
+    const int i = (int)(s - (long long)g * N);
+    RayRec rr;
+    bool active;
+    int lo = make_ray_rec(cfg, objs, n_objs, g, rr, active);
+    if (i == 0) rays[g] = rr;
+    count_hit(hit_count, lo, active && i == 0);
+    float4 o = make_float4(-1.f, -1.f, -1.f, 0.f);
+    float delta = 0.f;
+    if (active) {
+        const ObjDev& ob = objs[lo];
+        unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1);
+        float dist, u[3];
+        sample_geometry(rr, i, N, pre, g - ob.ray_begin, ob.a, dist, delta, u);
+        o = make_float4(u[0], u[1], u[2], dist);
+    }
+    srec[s] = o;
+    sdelta[s] = delta;
+}
+
 void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
                    RayRec* rays, unsigned long long* hit_count) {
     int blocks = (total_slots + 127) / 128;
     if (blocks > 0) k_raygen<<<blocks, 128, 0, lc.st>>>(cfg, objs, n_objs, total_slots, rays, hit_count);
+}
+
+void launch_raygen_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
+                           RayRec* rays, float4* srec, float* sdelta, unsigned long long* hit_count) {
+    long long S = (long long)total_slots * cfg.N;
+    unsigned blocks = (unsigned)((S + 127) / 128);
+    if (blocks > 0)
+        k_raygen_samples<<<blocks, 128, 0, lc.st>>>(cfg, objs, n_objs, total_slots, rays, srec, sdelta, hit_count);
 }
 
 // inference rays: every pixel of a W x H image from pose `cam` (R12, R20)

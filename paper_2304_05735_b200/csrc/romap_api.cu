@@ -17,8 +17,9 @@
 #include "../../include/romap.h"
 #include "romap_internal.cuh"
 
-void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
-                        double* loss_acc, int* nonfinite, float* dbg_ray_grads);
+void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
+                        const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
+                        float* dbg_ray_grads);
 bool fused_mixed_available();
 
 static thread_local std::string g_err;
@@ -101,6 +102,8 @@ struct romap_ctx {
     size_t rays_cap = 0;
     float* samp = nullptr;       // sigma | rgb(3) | dist | delta | dsigma | drgb(3) : 10 floats per sample
     size_t samp_cap = 0;
+    float* srec = nullptr;       // mixed path: (u, dist) float4 | delta : 5 floats per sample (k_raygen_samples)
+    size_t srec_cap = 0;
     float* act = nullptr;
     size_t act_cap = 0;
     ObjDev* objdev_d = nullptr;
@@ -361,6 +364,7 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     for (auto& kv : ctx->objs) free_object(ctx, kv.second);
     dfree(ctx, ctx->rays);
     dfree(ctx, ctx->samp);
+    dfree(ctx, ctx->srec);
     dfree(ctx, ctx->act);
     dfree(ctx, ctx->objdev_d);
     dfree(ctx, ctx->single_d);
@@ -658,6 +662,7 @@ static romap_status upload_batch(romap_ctx* ctx, Batch& b, bool train_scratch) {
             if (!grow(ctx, ctx->act, ctx->act_cap, S * rows)) return fail(ROMAP_E_OOM, "activation buffer allocation failed");
         } else {
             if (!grow(ctx, ctx->samp, ctx->samp_cap, S * 4)) return fail(ROMAP_E_OOM, "sample buffer allocation failed");
+            if (!grow(ctx, ctx->srec, ctx->srec_cap, S * 5)) return fail(ROMAP_E_OOM, "sample record allocation failed");
         }
     }
     CK(cudaMemcpyAsync(ctx->objdev_d, b.dev.data(), n * sizeof(ObjDev), cudaMemcpyHostToDevice, ctx->st));
@@ -687,11 +692,15 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             CK(cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st));
             stage_end(ctx, ST_FLUSH, e0);
         }
-        STAGE(ST_RAYGEN, launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d));
         if (b.mixed) {
-            STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, ctx->loss_d,
-                                               ctx->nonfinite_d, adam ? nullptr : ctx->samp));
+            float4* srec = reinterpret_cast<float4*>(ctx->srec);
+            float* sdelta = ctx->srec + 4 * S;
+            STAGE(ST_RAYGEN, launch_raygen_samples(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, srec, sdelta,
+                                                   ctx->hits_d));
+            STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays, srec, sdelta, b.total_slots,
+                                               ctx->loss_d, ctx->nonfinite_d, adam ? nullptr : ctx->samp));
         } else {
+            STAGE(ST_RAYGEN, launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d));
             STAGE(ST_FWD, launch_fwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, true, false, sigma, rgb,
                                           dist, delta, ctx->act, (long long)S));
             STAGE(ST_RENDER_LOSS, launch_render_loss(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb,
