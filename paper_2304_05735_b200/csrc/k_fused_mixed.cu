@@ -34,10 +34,31 @@
 
 bool fused_mixed_available() { return true; }
 
+// optional phase timing (build with -DROMAP_FUSED_PROF): clock64 cycles per
+// phase summed over CTAs, read back with romap_debug_fused_prof
+#ifdef ROMAP_FUSED_PROF
+__device__ unsigned long long g_fprof[16];
+#define FP_MARK(var) const long long var = clock64()
+#define FP_ACC(slot, a, b) do { if (fp_on) atomicAdd(&g_fprof[slot], (unsigned long long)((b) - (a))); } while (0)
+extern "C" __attribute__((visibility("default"))) int romap_debug_fused_prof(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_fprof, sizeof(g_fprof));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_fprof, z, sizeof z);
+    }
+    return 0;
+}
+#else
+#define FP_MARK(var)
+#define FP_ACC(slot, a, b)
+#endif
+
 namespace {
 
 constexpr int TILE = 128;                      // samples per tile
-constexpr int NG = 256;                        // gather/scatter threads (G0, G1)
+constexpr int NGW = 2;                         // gather/scatter warpgroups
+constexpr int NG = 128 * NGW;                  // gather/scatter threads
 constexpr int NM = 128;                        // MLP/render threads (M)
 constexpr int NT = NG + NM;
 constexpr int BAR_M = 1;                       // named barrier of M
@@ -310,29 +331,30 @@ __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint
     }
 }
 
-// cell and the 8 corner entries (relative to the level block) of one level
-// (R5): P = {res, y multiplier, z multiplier, dense}; dense: x + (N+1) y +
-// (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^ z * 805459861) & (T - 1).
-// Corner b: bit k -> +1 on axis k.
-__device__ __forceinline__ void level_entries(const float u[3], const int4 P, unsigned hmask, Cell& cl, int (&e)[8]) {
+// cell and the 8 corner entries of one level (R5), as absolute entry indices
+// (level offset `off` added): P = {res, y multiplier, z multiplier, dense};
+// dense: x + (N+1) y + (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^
+// z * 805459861) & (T - 1).  Corner b: bit k -> +1 on axis k.
+__device__ __forceinline__ void level_entries(const float u[3], const int4 P, unsigned off, unsigned hmask, Cell& cl,
+                                              unsigned (&e)[8]) {
     cl = grid_cell(u, P.x);
     const unsigned my = (unsigned)P.y, mz = (unsigned)P.z;
     const unsigned x0 = (unsigned)cl.c[0], x1 = x0 + 1u;
     const unsigned ty0 = (unsigned)cl.c[1] * my, ty1 = ty0 + my;
     const unsigned tz0 = (unsigned)cl.c[2] * mz, tz1 = tz0 + mz;
     if (P.w) {
-        const unsigned yz[4] = {ty0 + tz0, ty1 + tz0, ty0 + tz1, ty1 + tz1};
+        const unsigned yz[4] = {ty0 + tz0 + off, ty1 + tz0 + off, ty0 + tz1 + off, ty1 + tz1 + off};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            e[2 * k] = (int)(x0 + yz[k]);
-            e[2 * k + 1] = (int)(x1 + yz[k]);
+            e[2 * k] = x0 + yz[k];
+            e[2 * k + 1] = x1 + yz[k];
         }
     } else {
         const unsigned yz[4] = {ty0 ^ tz0, ty1 ^ tz0, ty0 ^ tz1, ty1 ^ tz1};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            e[2 * k] = (int)((x0 ^ yz[k]) & hmask);
-            e[2 * k + 1] = (int)((x1 ^ yz[k]) & hmask);
+            e[2 * k] = ((x0 ^ yz[k]) & hmask) + off;
+            e[2 * k + 1] = ((x1 ^ yz[k]) & hmask) + off;
         }
     }
 }
@@ -345,7 +367,6 @@ template <int L>
 __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
                                        const RayRec* __restrict__ rays, const float4* __restrict__ srec, int tile0,
                                        int n, uint8_t* smem, Misc* misc, uint32_t tm) {
-    constexpr int LH = L / 2;                 // levels of this warpgroup
     constexpr int LF = 2 * L;
     const int t = threadIdx.x, r = t & (TILE - 1), lane = t & 31, q4 = (t >> 5) & 3, WG = t >> 7;
     const int N = cfg.N;
@@ -356,12 +377,16 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     float4 u_next = srec[(long long)tile0 * TILE + r];
     int slot_next = rays[(int)(((long long)tile0 * TILE) / N)].slot;
     int slot_tab = -1;
-    const __half2* tab = nullptr;
+    const uint32_t* tab = nullptr;                // fp16 table: one 4-byte (half2) word per entry
     float2* g_cur = nullptr;
     float um1[3] = {-1.f, -1.f, -1.f}, um2[3] = {-1.f, -1.f, -1.f};
     float2* g_m1 = nullptr;
     float2* g_m2 = nullptr;
 
+#ifdef ROMAP_FUSED_PROF
+    const bool fp_on = (t & 127) == 0;
+#endif
+    FP_MARK(g_start);
     for (int it = 0; it < n + 2; ++it) {
         const bool dg = it < n, ds = it >= 2;
         const int b = it & 1;
@@ -372,22 +397,31 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             slot_next = rays[(int)(((long long)(tile0 + it + 1) * TILE) / N)].slot;
         }
         if (dg && slot_g != slot_tab) {
-            tab = reinterpret_cast<const __half2*>(objs[slot_g].p16);
+            tab = reinterpret_cast<const uint32_t*>(objs[slot_g].p16);
             g_cur = reinterpret_cast<float2*>(objs[slot_g].g32);
             slot_tab = slot_g;
         }
+        FP_MARK(g_w0);
         if (ds) {                                     // dfeat of tile it-2 is in DF[b]
             tc::mbar_wait(&misc->tile_done[b], ((it - 2) >> 1) & 1);
             tc::fence_after();
         }
+        FP_MARK(g_w1);
+        FP_ACC(9, g_w0, g_w1);
         const bool ag = dg && ug[0] >= 0.f;          // sample of an active ray (k_raygen_samples)
         const bool as = ds && um2[0] >= 0.f;
+        const unsigned flags_it = (dg ? 1u : 0u) | (ds ? 2u : 0u) | (ag ? 4u : 0u) | (as ? 8u : 0u);
         uint8_t* X0 = smem + OFF_X0 + b * X0_BYTES;
 #pragma unroll 1
-        for (int lp = 0; lp < LH; lp += 2) {
-            const int l = WG * LH + lp;
+        for (int pp = WG; pp < L / 2; pp += NGW) {   // level pairs of this warpgroup
+            // opaque copy of the iteration flags: keeps the compiler from
+            // unswitching this loop into one copy per flag combination
+            unsigned fl;
+            asm volatile("mov.b32 %0, %1;" : "=r"(fl) : "r"(flags_it));
+            const bool dg_ = fl & 1u, ds_ = fl & 2u, ag_ = fl & 4u, as_ = fl & 8u;
+            const int l = 2 * pp;
             const int4 P[2] = {misc->lv[l], misc->lv[l + 1]};
-            const int off[2] = {misc->lvoff[l], misc->lvoff[l + 1]};
+            const unsigned off[2] = {(unsigned)misc->lvoff[l], (unsigned)misc->lvoff[l + 1]};
             // (1) gathers of levels l, l+1 of tile it.  x-neighbour corners (b, b|1)
             // share a 16-byte chunk of the fp16 table in 3 of 4 cases (dense:
             // entries e, e+1; hashed: e ^ (x ^ (x+1)) with the x prime = 1), so each
@@ -395,75 +429,72 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             // are 16-entry aligned (R5).
             uint4 qv[2][4];
             uint32_t xv[2][4];
-            int e[2][8];
+            unsigned e[2][8];
             Cell cl[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                level_entries(ug, P[q], hmask, cl[q], e[q]);
-                const __half2* tb = tab + off[q];
+                level_entries(ug, P[q], off[q], hmask, cl[q], e[q]);
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
-                    qv[q][p] = ag ? ldg_v4(tb + (e[q][2 * p] & ~3)) : make_uint4(0, 0, 0, 0);
-                    xv[q][p] = (ag && !same) ? ldg_u32(tb + e[q][2 * p + 1]) : 0u;
+                    qv[q][p] = ag_ ? ldg_v4(tab + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+                    xv[q][p] = (ag_ && !same) ? ldg_u32(tab + e[q][2 * p + 1]) : 0u;
                 }
             }
             // (2) scatter of the same levels of tile it-2 (fire-and-forget REDs)
-            if (ds) {
+            if (ds_) {
                 float g[4];
                 tc::tmem_ld4_sync(df_lane + 32 * b + 2 * l, g);
-                if (as) {
+                if (as_) {
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         Cell cs;
-                        int es[8];
-                        level_entries(um2, P[q], hmask, cs, es);
+                        unsigned es[8];
+                        level_entries(um2, P[q], off[q], hmask, cs, es);
                         const float g0 = g[2 * q] * inv_scale, g1 = g[2 * q + 1] * inv_scale;
-                        float2* gl = g_m2 + off[q];
 #pragma unroll
                         for (int p = 0; p < 4; ++p) {
                             // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
                             // REDG.F32x4, else two REDG.F32x2
-                            const int ea = es[2 * p], eb = es[2 * p + 1];
+                            const unsigned ea = es[2 * p], eb = es[2 * p + 1];
                             const float wa = corner_weight(cs, 2 * p), wb = corner_weight(cs, 2 * p + 1);
                             if ((ea >> 1) == (eb >> 1)) {
                                 if (ea < eb)
-                                    red_add_f4(reinterpret_cast<float4*>(gl + ea), wa * g0, wa * g1, wb * g0, wb * g1);
+                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + ea), wa * g0, wa * g1, wb * g0, wb * g1);
                                 else
-                                    red_add_f4(reinterpret_cast<float4*>(gl + eb), wb * g0, wb * g1, wa * g0, wa * g1);
+                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + eb), wb * g0, wb * g1, wa * g0, wa * g1);
                             } else {
-                                red_add_f2(gl + ea, wa * g0, wa * g1);
-                                red_add_f2(gl + eb, wb * g0, wb * g1);
+                                red_add_f2(g_m2 + ea, wa * g0, wa * g1);
+                                red_add_f2(g_m2 + eb, wb * g0, wb * g1);
                             }
                         }
                     }
                 }
             }
-            // (3) interpolate the gathered corners -> 4 features (2 levels) -> X0[b]
-            if (dg) {
-                float f[4];
+            // (3) trilinear interpolation of the gathered corners in packed fp16
+            // (x, then y, then z lerps of the 2 features) -> X0[b]
+            if (dg_) {
+                __half2 fq[2];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    float a0 = 0.f, a1 = 0.f;
+                    const __half2 fx = __float2half2_rn(cl[q].f[0]), fy = __float2half2_rn(cl[q].f[1]),
+                                  fz = __float2half2_rn(cl[q].f[2]);
+                    __half2 vx[4];
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
-                        const int ea = e[q][2 * p], eb = e[q][2 * p + 1];
+                        const unsigned ea = e[q][2 * p], eb = e[q][2 * p + 1];
                         const bool same = (ea >> 2) == (eb >> 2);
                         const uint32_t h0 = sel4(qv[q][p], ea & 3);
                         const uint32_t h1 = same ? sel4(qv[q][p], eb & 3) : xv[q][p];
-                        const float w0 = corner_weight(cl[q], 2 * p), w1 = corner_weight(cl[q], 2 * p + 1);
-                        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h0));
-                        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h1));
-                        a0 += w0 * f0.x;
-                        a1 += w0 * f0.y;
-                        a0 += w1 * f1.x;
-                        a1 += w1 * f1.y;
+                        const __half2 a = *reinterpret_cast<const __half2*>(&h0);
+                        const __half2 c = *reinterpret_cast<const __half2*>(&h1);
+                        vx[p] = __hfma2(fx, __hsub2(c, a), a);
                     }
-                    f[2 * q] = a0;
-                    f[2 * q + 1] = a1;
+                    const __half2 vy0 = __hfma2(fy, __hsub2(vx[1], vx[0]), vx[0]);
+                    const __half2 vy1 = __hfma2(fy, __hsub2(vx[3], vx[2]), vx[2]);
+                    fq[q] = __hfma2(fz, __hsub2(vy1, vy0), vy0);
                 }
-                __half2 hq[2] = {__floats2half2_rn(f[0], f[1]), __floats2half2_rn(f[2], f[3])};
-                *reinterpret_cast<uint2*>(X0 + tc::il_offset(r, 2 * l, LF)) = *reinterpret_cast<uint2*>(hq);
+                *reinterpret_cast<uint2*>(X0 + tc::il_offset(r, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
             }
         }
         if (ds) {                                     // DF[b] read: M may overwrite it (tile it)
@@ -483,7 +514,35 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
         }
         g_m2 = g_m1;
         g_m1 = g_cur;
+        FP_MARK(g_w2);
+        FP_ACC(10, g_w1, g_w2);
     }
+    FP_MARK(g_end);
+    FP_ACC(8, g_start, g_end);
+}
+
+// per-sample inputs of M, loaded one tile ahead (plain loads placed before the
+// tile's barriers, so they are issued early and their latency overlaps a tile)
+struct MIn {
+    float d[3], tgt[3], bg[3], depth, dist, delta;
+    int flags, slot;
+};
+__device__ __forceinline__ MIn m_load(const RayRec* __restrict__ rays, const float4* __restrict__ srec,
+                                      const float* __restrict__ sdelta, long long s, int N) {
+    const RayRec* rp = rays + (int)(s / N);
+    MIn v;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        v.d[k] = rp->d[k];
+        v.tgt[k] = rp->tgt[k];
+        v.bg[k] = rp->bg[k];
+    }
+    v.depth = rp->depth;
+    v.flags = rp->flags;
+    v.slot = rp->slot;
+    v.dist = srec[s].w;
+    v.delta = sdelta[s];
+    return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -524,14 +583,19 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     int cur = -1;
     bool dw_fresh = true;
     float invB = 0.f;
+#ifdef ROMAP_FUSED_PROF
+    const bool fp_on = m == 0;
+#endif
+    FP_MARK(m_start);
+    MIn nx = m_load(rays, srec, sdelta, (long long)tile0 * TILE + m, N);
     for (int j = 0; j < n; ++j) {
+        FP_MARK(m_t0);
         const int tile = tile0 + j, b = j & 1;
         const long long s = (long long)tile * TILE + m;
-        const int ray = (int)(s / N);
-        const int i = (int)(s - (long long)ray * N);
-        const RayRec rr = rays[ray];
-        const float4 sr = srec[s];
-        const float delta = sdelta[s];
+        const int i = (int)(s % N);
+        const MIn rr = nx;
+        if (j + 1 < n) nx = m_load(rays, srec, sdelta, s + TILE, N);
+        const float delta = rr.delta;
         const bool active = (rr.flags & RF_ACTIVE) != 0;
         if (rr.slot != cur) {                      // uniform: a tile holds rays of one object
             if (cur >= 0) {
@@ -551,7 +615,9 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             sh4(rr.d, sh);
             st16(CIN, m, 16, 32, sh);
         }
+        FP_MARK(m_t1);
         tc::mbar_wait(&misc->x0_full[b], (j >> 1) & 1);
+        FP_MARK(m_t2);
         m_sync_for_mma();
         const uint32_t sX0 = tc::smem_u32(smem + OFF_X0 + b * X0_BYTES);
 
@@ -624,16 +690,22 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[k]));
         }
 
+        FP_MARK(m_t3);
         // ---- a5: volume rendering + loss + render backward
-        const float dist = sr.w;
+        const float dist = rr.dist;
         const float x = active ? sigma * delta : 0.f;
         const float alpha = expf(-x);
         const float o = -expm1f(-x);
         float TN;
+        FP_MARK(m_r0);
         const float Ti = m_scan_mul(alpha, N, xw, TN);
+        FP_MARK(m_r1);
+        FP_ACC(11, m_r0, m_r1);
         const float w = active ? Ti * o : 0.f;
         float sums[5] = {w * c[0], w * c[1], w * c[2], w * dist, active ? sigma : 0.f};
         m_ray_sums<5>(sums, N, xw);
+        FP_MARK(m_r2);
+        FP_ACC(12, m_r1, m_r2);
         float dsig = 0.f, dcol[3] = {0.f, 0.f, 0.f};
         float gC[3] = {0.f, 0.f, 0.f};
         float gD = 0.f, gCb = 0.f;
@@ -664,7 +736,11 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         }
         const float gc = gC[0] * c[0] + gC[1] * c[1] + gC[2] * c[2];
         float S, Sd;
+        FP_MARK(m_r3);
+        FP_ACC(13, m_r2, m_r3);
         m_suffix2(w * gc, w * dist, N, xw, S, Sd);
+        FP_MARK(m_r4);
+        FP_ACC(14, m_r3, m_r4);
         if (active) {
             const float Tn1 = Ti * alpha;
             dsig = delta * (Tn1 * gc - S - TN * gCb) + delta * gD * (Tn1 * dist - Sd) +
@@ -673,6 +749,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             for (int k = 0; k < 3; ++k) dcol[k] = w * gC[k];
         }
         if (dbg) *reinterpret_cast<float4*>(dbg + 4 * s) = make_float4(dsig, dcol[0], dcol[1], dcol[2]);
+        FP_MARK(m_t4);
 
         // ---- a6: MLP backward (scaled by loss_scale)
         {
@@ -765,12 +842,20 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::commit(&misc->tile_done[b]);
         }
         dw_fresh = false;
+        FP_MARK(m_t5);
+        FP_ACC(6, m_t0, m_t1);
+        FP_ACC(1, m_t1, m_t2);
+        FP_ACC(2, m_t2, m_t3);
+        FP_ACC(3, m_t3, m_t4);
+        FP_ACC(4, m_t4, m_t5);
     }
     if (cur >= 0) {
         tc::mbar_wait(&misc->tile_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
         tc::fence_after();
         m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
     }
+    FP_MARK(m_end);
+    FP_ACC(0, m_start, m_end);
 }
 
 }  // namespace
@@ -789,9 +874,9 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     if (t == 32) {
         tc::mbar_init(&misc->mbar_mma, 1);
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&misc->x0_full[b], 8);
+            tc::mbar_init(&misc->x0_full[b], NG / 32);
             tc::mbar_init(&misc->tile_done[b], 1);
-            tc::mbar_init(&misc->df_empty[b], 8);
+            tc::mbar_init(&misc->df_empty[b], NG / 32);
         }
         tc::fence_mbar_init();
     }
@@ -810,7 +895,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     const int tile0 = blockIdx.x * tiles_per_cta;
     const int n = min(tiles_per_cta, n_tiles - tile0);
     if (n > 0) {
-        if (warp < 8)
+        if (warp < NG / 32)
             g_loop<L>(cfg, objs, rays, srec, tile0, n, smem, misc, tm);
         else
             m_loop<L>(cfg, objs, rays, srec, sdelta, tile0, n, smem, misc, tm, loss_acc, nonfinite, dbg);
