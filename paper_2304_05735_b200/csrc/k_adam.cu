@@ -7,6 +7,38 @@
 // fp16 w, g zero) -- see DESIGN.md "Kernels".
 #include "romap_internal.cuh"
 
+// one Adam update of 4 consecutive parameters (i0 .. i0+3, all < total)
+__device__ __forceinline__ bool adam4(float4& pp, float4& mm, float4& vv, const float4 gg, int i0, int n_table,
+                                      float b1, float b2, float omb1, float omb2, float bc1, float bc2, float lr,
+                                      float eps, bool& bad) {
+    float g[4] = {gg.x, gg.y, gg.z, gg.w}, p[4] = {pp.x, pp.y, pp.z, pp.w}, m[4] = {mm.x, mm.y, mm.z, mm.w},
+          v[4] = {vv.x, vv.y, vv.z, vv.w};
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float gj = g[j];
+        if (i0 + j < n_table && gj == 0.f) continue;      // sparse tables (R18)
+        any = true;
+        bad |= !isfinite(gj);
+        const float mj = b1 * m[j] + omb1 * gj;
+        const float vj = b2 * v[j] + omb2 * gj * gj;
+        const float mh = mj / bc1;
+        const float vh = vj / bc2;
+        p[j] = p[j] - lr * mh / (sqrtf(vh) + eps);
+        m[j] = mj;
+        v[j] = vj;
+    }
+    pp = make_float4(p[0], p[1], p[2], p[3]);
+    mm = make_float4(m[0], m[1], m[2], m[3]);
+    vv = make_float4(v[0], v[1], v[2], v[3]);
+    return any;
+}
+
+// grid (bx, n_objs): every block updates a strided share of one object's
+// parameters (g, p, m, v loaded together, two float4 groups in flight per
+// thread); the last block of the object to finish advances its Adam step
+// counter (step_d[0]; step_d[1] counts finished blocks), so no separate launch
+// is needed for the step increment.
 __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restrict__ objs, int* __restrict__ nonfinite,
                                               int write_half) {
     const ObjDev& ob = objs[blockIdx.y];
@@ -18,76 +50,72 @@ __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restri
     const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
     const int n_table = cfg.n_table;
     const int total = cfg.n_table + cfg.n_mlp;
-    // vectorised over 4 params (n_table is even; handle tails scalar)
     const int n4 = total / 4;
     float4* p4 = reinterpret_cast<float4*>(ob.p32);
     float4* g4 = reinterpret_cast<float4*>(ob.g32);
     float4* m4 = reinterpret_cast<float4*>(ob.m);
     float4* v4 = reinterpret_cast<float4*>(ob.v);
     bool bad = false;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n4 + (total - n4 * 4); q += gridDim.x * blockDim.x) {
-        int i0, cnt;
-        float g[4], p[4], m[4], v[4];
-        if (q < n4) {
-            i0 = 4 * q;
-            cnt = 4;
-            float4 gg = g4[q];
-            g[0] = gg.x; g[1] = gg.y; g[2] = gg.z; g[3] = gg.w;
-            if (gg.x == 0.f && gg.y == 0.f && gg.z == 0.f && gg.w == 0.f && i0 + 4 <= n_table) continue;
-            float4 pp = p4[q], mm = m4[q], vv = v4[q];
-            p[0] = pp.x; p[1] = pp.y; p[2] = pp.z; p[3] = pp.w;
-            m[0] = mm.x; m[1] = mm.y; m[2] = mm.z; m[3] = mm.w;
-            v[0] = vv.x; v[1] = vv.y; v[2] = vv.z; v[3] = vv.w;
-        } else {
-            i0 = 4 * n4 + (q - n4);
-            cnt = 1;
-            g[0] = ob.g32[i0];
-            p[0] = ob.p32[i0];
-            m[0] = ob.m[i0];
-            v[0] = ob.v[i0];
+    const int stride = gridDim.x * blockDim.x;
+    auto store = [&](int q, const float4& pp, const float4& mm, const float4& vv) {
+        p4[q] = pp;
+        m4[q] = mm;
+        v4[q] = vv;
+        g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (write_half) {
+            __half2* h2 = reinterpret_cast<__half2*>(ob.p16 + 4 * q);
+            h2[0] = __floats2half2_rn(pp.x, pp.y);
+            h2[1] = __floats2half2_rn(pp.z, pp.w);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (j >= cnt) break;
-            int i = i0 + j;
-            float gj = g[j];
-            if (i < n_table && gj == 0.f) continue;      // sparse tables (R18)
-            bad |= !isfinite(gj);
-            float mj = b1 * m[j] + omb1 * gj;
-            float vj = b2 * v[j] + omb2 * gj * gj;
-            float mh = mj / bc1;
-            float vh = vj / bc2;
-            p[j] = p[j] - lr * mh / (sqrtf(vh) + eps);
-            m[j] = mj;
-            v[j] = vj;
-        }
-        if (cnt == 4) {
-            p4[q] = make_float4(p[0], p[1], p[2], p[3]);
-            m4[q] = make_float4(m[0], m[1], m[2], m[3]);
-            v4[q] = make_float4(v[0], v[1], v[2], v[3]);
-            g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (write_half) {
-                __half2* h2 = reinterpret_cast<__half2*>(ob.p16 + i0);
-                h2[0] = __floats2half2_rn(p[0], p[1]);
-                h2[1] = __floats2half2_rn(p[2], p[3]);
-            }
-        } else {
-            ob.p32[i0] = p[0];
-            ob.m[i0] = m[0];
-            ob.v[i0] = v[0];
-            ob.g32[i0] = 0.f;
-            if (write_half) ob.p16[i0] = __float2half_rn(p[0]);
-        }
+    };
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + stride < n4; q += 2 * stride) {
+        const int q2 = q + stride;
+        const float4 ga = g4[q], gb = g4[q2];
+        float4 pa = p4[q], ma = m4[q], va = v4[q];
+        float4 pb = p4[q2], mb = m4[q2], vb = v4[q2];
+        if (adam4(pa, ma, va, ga, 4 * q, n_table, b1, b2, omb1, omb2, bc1, bc2, lr, eps, bad)) store(q, pa, ma, va);
+        if (adam4(pb, mb, vb, gb, 4 * q2, n_table, b1, b2, omb1, omb2, bc1, bc2, lr, eps, bad)) store(q2, pb, mb, vb);
+    }
+    if (q < n4) {
+        const float4 ga = g4[q];
+        float4 pa = p4[q], ma = m4[q], va = v4[q];
+        if (adam4(pa, ma, va, ga, 4 * q, n_table, b1, b2, omb1, omb2, bc1, bc2, lr, eps, bad)) store(q, pa, ma, va);
+    }
+    // scalar tail (total % 4 parameters; MLP, dense)
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gt < total - 4 * n4) {
+        const int i = 4 * n4 + gt;
+        const float gj = ob.g32[i];
+        bad |= !isfinite(gj);
+        const float mj = b1 * ob.m[i] + omb1 * gj;
+        const float vj = b2 * ob.v[i] + omb2 * gj * gj;
+        const float p = ob.p32[i] - lr * (mj / bc1) / (sqrtf(vj / bc2) + eps);
+        ob.p32[i] = p;
+        ob.m[i] = mj;
+        ob.v[i] = vj;
+        ob.g32[i] = 0.f;
+        if (write_half) ob.p16[i] = __float2half_rn(p);
     }
     if (bad) atomicOr(nonfinite, 2);
+    // every thread of this block has read the step counter: count the block
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned long long* done = reinterpret_cast<unsigned long long*>(ob.step + 1);
+        if (atomicAdd(done, 1ull) == (unsigned long long)(gridDim.x - 1)) {
+            *ob.step = t;
+            *done = 0ull;
+        }
+    }
 }
 
 void launch_adam(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int* nonfinite,
                  bool write_half) {
     if (n_objs == 0) return;
     long long total = (long long)cfg.n_table + cfg.n_mlp;
-    int per_obj = (int)((total / 4 + 255) / 256);
-    // a few waves over the SMs in total
+    int per_obj = (int)((total / 4 + 511) / 512);
+    // one full wave (8 blocks of 256 threads per SM) in total
     int target = (lc.num_sms * 8 + n_objs - 1) / n_objs;
     int bx = per_obj < target ? per_obj : target;
     if (bx < 1) bx = 1;

@@ -12,7 +12,7 @@
 // background colour (R8-R14, R17); returns the object slot and whether the ray
 // is active (hit and supervised)
 __device__ __forceinline__ int make_ray_rec(const CfgDev& cfg, const ObjDev* __restrict__ objs, int n_objs, int g,
-                                            RayRec& rr, bool& active) {
+                                            int iter_off, RayRec& rr, bool& active) {
     // object owning slot g (objects are sorted by ray_begin)
     int lo = 0, hi = n_objs - 1;
     while (lo < hi) {
@@ -29,7 +29,7 @@ __device__ __forceinline__ int make_ray_rec(const CfgDev& cfg, const ObjDev* __r
     rr.kf = rr.px = rr.py = -1;
     active = false;
     if (r < ob.n_rays) {
-        long long t = *ob.step + 1;                       // the Adam step this iteration feeds (R13)
+        long long t = *ob.step + 1 + iter_off;            // the Adam step this iteration feeds (R13)
         unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, t);
         // R9: uniform over the union of in-box pixels of all keyframes
         unsigned u = rng_u32(pre, r, 0);
@@ -92,41 +92,46 @@ __global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __rest
     if (g >= total_slots) return;
     RayRec rr;
     bool active;
-    int lo = make_ray_rec(cfg, objs, n_objs, g, rr, active);
+    int lo = make_ray_rec(cfg, objs, n_objs, g, 0, rr, active);
     rays[g] = rr;
     count_hit(hit_count, lo, active);
 }
 
-// mixed path: thread per SAMPLE.  The N threads of a ray rebuild its record
-// (identical loads, broadcast), thread i = 0 stores it and counts the hit, and
-// every thread stores its sample's geometry (R12, R6): srec[s] = (u, dist) with
-// u = (-1, -1, -1) for samples of inactive rays, sdelta[s] = delta.  Bit-exact
-// with the per-sample recomputation of the fp32 path (same device functions).
+// mixed path: thread per SAMPLE, for a chunk of consecutive iterations
+// (blockIdx.y = k: the iteration `step + 1 + k`, R13).  The N threads of a ray
+// rebuild its record (identical loads, broadcast), thread i = 0 stores it and
+// counts the hit, and every thread stores its sample's geometry (R12, R6):
+// srec[s] = (u, dist) with u = (-1, -1, -1) for samples of inactive rays,
+// sdelta[s] = delta.  Bit-exact with the per-sample recomputation of the fp32
+// path (same device functions).  Output slice k starts at rays + k * slots and
+// srec / sdelta + k * slots * N.
 __global__ void __launch_bounds__(128) k_raygen_samples(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
                                                         int total_slots, RayRec* __restrict__ rays,
                                                         float4* __restrict__ srec, float* __restrict__ sdelta,
                                                         unsigned long long* __restrict__ hit_count) {
-    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int N = cfg.N;
+    const int k = blockIdx.y;
+    const long long S = (long long)total_slots * N;
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int g = (int)(s / N);
     if (g >= total_slots) return;
     const int i = (int)(s - (long long)g * N);
     RayRec rr;
     bool active;
-    int lo = make_ray_rec(cfg, objs, n_objs, g, rr, active);
-    if (i == 0) rays[g] = rr;
+    int lo = make_ray_rec(cfg, objs, n_objs, g, k, rr, active);
+    if (i == 0) rays[(long long)k * total_slots + g] = rr;
     count_hit(hit_count, lo, active && i == 0);
     float4 o = make_float4(-1.f, -1.f, -1.f, 0.f);
     float delta = 0.f;
     if (active) {
         const ObjDev& ob = objs[lo];
-        unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1);
+        unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1 + k);
         float dist, u[3];
         sample_geometry(rr, i, N, pre, g - ob.ray_begin, ob.a, dist, delta, u);
         o = make_float4(u[0], u[1], u[2], dist);
     }
-    srec[s] = o;
-    sdelta[s] = delta;
+    srec[k * S + s] = o;
+    sdelta[k * S + s] = delta;
 }
 
 void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
@@ -136,11 +141,11 @@ void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, i
 }
 
 void launch_raygen_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
-                           RayRec* rays, float4* srec, float* sdelta, unsigned long long* hit_count) {
+                           int n_iters, RayRec* rays, float4* srec, float* sdelta, unsigned long long* hit_count) {
     long long S = (long long)total_slots * cfg.N;
-    unsigned blocks = (unsigned)((S + 127) / 128);
-    if (blocks > 0)
-        k_raygen_samples<<<blocks, 128, 0, lc.st>>>(cfg, objs, n_objs, total_slots, rays, srec, sdelta, hit_count);
+    dim3 grid((unsigned)((S + 127) / 128), (unsigned)n_iters);
+    if (grid.x > 0 && n_iters > 0)
+        k_raygen_samples<<<grid, 128, 0, lc.st>>>(cfg, objs, n_objs, total_slots, rays, srec, sdelta, hit_count);
 }
 
 // inference rays: every pixel of a W x H image from pose `cam` (R12, R20)

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/romap.h"
@@ -102,8 +103,9 @@ struct romap_ctx {
     size_t rays_cap = 0;
     float* samp = nullptr;       // sigma | rgb(3) | dist | delta | dsigma | drgb(3) : 10 floats per sample
     size_t samp_cap = 0;
-    float* srec = nullptr;       // mixed path: (u, dist) float4 | delta : 5 floats per sample (k_raygen_samples)
+    float* srec = nullptr;       // mixed path: K slices of (u, dist) float4, then K slices of delta (k_raygen_samples)
     size_t srec_cap = 0;
+    size_t last_ray_base = 0;    // ray slot of slice holding the last iteration's rays
     float* act = nullptr;
     size_t act_cap = 0;
     ObjDev* objdev_d = nullptr;
@@ -407,7 +409,7 @@ static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const roma
     ob->m = (float*)dalloc(ctx, n * 4);
     ob->v = (float*)dalloc(ctx, n * 4);
     ob->p16 = (__half*)dalloc(ctx, n * 2 + 16);
-    ob->step_d = (long long*)dalloc(ctx, 8);
+    ob->step_d = (long long*)dalloc(ctx, 16);   // [Adam step, finished-block counter of k_adam]
     if (!ob->p32 || !ob->g32 || !ob->m || !ob->v || !ob->p16 || !ob->step_d) {
         free_object(ctx, ob);
         return fail(ROMAP_E_OOM, "parameter allocation failed");
@@ -430,7 +432,7 @@ static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const roma
     if (e == cudaSuccess) e = cudaMemsetAsync(ob->g32, 0, n * 4, ctx->st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ob->m, 0, n * 4, ctx->st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ob->v, 0, n * 4, ctx->st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ob->step_d, 0, 8, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ob->step_d, 0, 16, ctx->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
     if (e != cudaSuccess) {
         ctx->poisoned = true;
@@ -662,7 +664,6 @@ static romap_status upload_batch(romap_ctx* ctx, Batch& b, bool train_scratch) {
             if (!grow(ctx, ctx->act, ctx->act_cap, S * rows)) return fail(ROMAP_E_OOM, "activation buffer allocation failed");
         } else {
             if (!grow(ctx, ctx->samp, ctx->samp_cap, S * 4)) return fail(ROMAP_E_OOM, "sample buffer allocation failed");
-            if (!grow(ctx, ctx->srec, ctx->srec_cap, S * 5)) return fail(ROMAP_E_OOM, "sample record allocation failed");
         }
     }
     CK(cudaMemcpyAsync(ctx->objdev_d, b.dev.data(), n * sizeof(ObjDev), cudaMemcpyHostToDevice, ctx->st));
@@ -678,6 +679,19 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     for (auto* ob : b.obs) dirty |= ob->grads_dirty;
     if (dirty) STAGE(ST_ZERO_GRADS, launch_zero_grads(lc, b.cfg, ctx->objdev_d, n));
     const size_t S = (size_t)b.total_slots * b.cfg.N;
+    // mixed path: rays and sample records of up to K iterations are generated by
+    // one k_raygen_samples launch (slices k = it % K), ~64 MB of records at most
+    int K = 1;
+    if (b.mixed) {
+        const size_t per_iter = (size_t)b.total_slots * sizeof(RayRec) + S * 5 * sizeof(float);
+        K = (int)std::max<size_t>(1, std::min<size_t>(16, (64u << 20) / per_iter));
+        K = std::min(K, n_iters);
+        if (!grow(ctx, ctx->rays, ctx->rays_cap, (size_t)K * b.total_slots))
+            return fail(ROMAP_E_OOM, "ray buffer allocation failed");
+        if (!grow(ctx, ctx->srec, ctx->srec_cap, (size_t)K * S * 5))
+            return fail(ROMAP_E_OOM, "sample record allocation failed");
+    }
+    ctx->last_ray_base = (size_t)((n_iters - 1) % K) * b.total_slots;
     float* sigma = ctx->samp;
     float* rgb = sigma + S;
     float* dist = rgb + 3 * S;
@@ -693,11 +707,15 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             stage_end(ctx, ST_FLUSH, e0);
         }
         if (b.mixed) {
+            const int k = it % K;
             float4* srec = reinterpret_cast<float4*>(ctx->srec);
-            float* sdelta = ctx->srec + 4 * S;
-            STAGE(ST_RAYGEN, launch_raygen_samples(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, srec, sdelta,
-                                                   ctx->hits_d));
-            STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays, srec, sdelta, b.total_slots,
+            float* sdelta = ctx->srec + 4 * S * K;
+            if (k == 0)
+                STAGE(ST_RAYGEN, launch_raygen_samples(lc, b.cfg, ctx->objdev_d, n, b.total_slots,
+                                                       std::min(K, n_iters - it), ctx->rays, srec, sdelta,
+                                                       ctx->hits_d));
+            STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays + (size_t)k * b.total_slots,
+                                               srec + (size_t)k * S, sdelta + (size_t)k * S, b.total_slots,
                                                ctx->loss_d, ctx->nonfinite_d, adam ? nullptr : ctx->samp));
         } else {
             STAGE(ST_RAYGEN, launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d));
@@ -708,10 +726,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             STAGE(ST_BWD, launch_bwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dsigma, drgb,
                                           ctx->act, (long long)S));
         }
-        if (adam) {
-            STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed));
-            STAGE(ST_STEP_INC, launch_step_inc(lc, ctx->objdev_d, n));
-        }
+        if (adam) STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed));
         CK(cudaGetLastError());
     }
     std::vector<double> loss(4 * n);
@@ -786,7 +801,6 @@ romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n
     LaunchCtx lc{ctx->st, ctx->num_sms};
     CK(cudaMemsetAsync(ctx->nonfinite_d, 0, sizeof(int), ctx->st));
     STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, (int)b.dev.size(), ctx->nonfinite_d, b.mixed));
-    STAGE(ST_STEP_INC, launch_step_inc(lc, ctx->objdev_d, (int)b.dev.size()));
     CK(cudaGetLastError());
     int nf = 0;
     CK(cudaMemcpyAsync(&nf, ctx->nonfinite_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
@@ -1007,7 +1021,8 @@ romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* b
     const int R = ob->last_n_rays, begin = ob->last_ray_begin;
     if (what == ROMAP_DUMP_RAYS) {
         std::vector<RayRec> rr(R);
-        CK(cudaMemcpyAsync(rr.data(), ctx->rays + begin, R * sizeof(RayRec), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(rr.data(), ctx->rays + ctx->last_ray_base + begin, R * sizeof(RayRec),
+                           cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         romap_ray_dump* o = (romap_ray_dump*)buf;
         for (int i = 0; i < R; ++i) {

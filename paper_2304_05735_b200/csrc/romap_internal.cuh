@@ -288,7 +288,7 @@ struct LaunchCtx {
 void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
                    RayRec* rays, unsigned long long* hit_count);
 void launch_raygen_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
-                           RayRec* rays, float4* srec, float* sdelta, unsigned long long* hit_count);
+                           int n_iters, RayRec* rays, float4* srec, float* sdelta, unsigned long long* hit_count);
 void launch_fwd_fp32(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
                      bool train, bool midpoint, float* sigma, float* rgb, float* dist, float* delta, float* act,
                      long long act_stride);
