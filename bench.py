@@ -282,9 +282,13 @@ def run_ours(args):
     ctx.train_step(objs, args.warmup)
     torch.cuda.synchronize()
 
-    # timed region: exactly K iterations, L2 flushed before each by the library hook
+    # timed region: exactly K iterations, L2 flushed before each by the library hook.
+    # Only the flush (subtracted) and the dominant kernel (roofline) are bracketed
+    # with CUDA events here; the full per-stage breakdown comes from a separate
+    # short profiled pass after the timed region.
     ctx.set_l2_flush(FLUSH_BYTES)
-    ctx.profile_enable(True)
+    dominant = "fused_mixed" if precision == 1 else "bwd_fp32"
+    ctx.profile_enable(True, stages=[dominant, "l2_flush"])
     sampler, spath = start_clock_sampler(visible_index(local))
     time.sleep(0.3)
     stream = torch.cuda.current_stream()
@@ -300,13 +304,17 @@ def run_ours(args):
         pg.barrier()
     clocks = stop_clock_sampler(sampler, spath)
     prof = ctx.profile_read()
+    # separate, untimed pass: every stage bracketed with events (breakdown only)
+    ctx.profile_enable(True)
+    n_brk = min(10, args.steps)
+    ctx.train_step(objs, n_brk)
+    prof_all = ctx.profile_read()
     ctx.profile_enable(False)
     ctx.set_l2_flush(0)
     total_ms = ev0.elapsed_time(ev1)
     flush_ms = prof.get("l2_flush", {}).get("ms", 0.0)
     step_ms = (total_ms - flush_ms) / args.steps
     samples = sum(s["samples"] for s in stats)
-    kernel_ms = sum(v["ms"] for k, v in prof.items() if k != "l2_flush")
     launches = sum(v["launches"] for k, v in prof.items() if k != "l2_flush")
 
     # e2e: the paper's online unit through the public API with HOST buffers: one new
@@ -372,8 +380,9 @@ def run_ours(args):
             "paper_context": {"samples_per_s": PAPER_SAMPLES_PER_S, "ms_per_iteration": 0.706,
                               "note": "RTX 4090, N=32, position-only 1x64 MLP (PAPER.md:222,307); not this workload"},
             "hit_samples_per_step": samples / args.steps,
-            "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"] or v["ms"]},
-            "kernel_ms_per_step": kernel_ms / args.steps,
+            "stage_ms_per_step": {k: v["ms"] / n_brk for k, v in prof_all.items() if v["launches"] or v["ms"]},
+            "stage_ms_note": f"separate {n_brk}-iteration pass with every stage bracketed by events (not the timed region)",
+            "kernel_ms_per_step": sum(v["ms"] for k, v in prof_all.items() if k != "l2_flush") / n_brk,
             "gpu_launches": launches,
             "roofline": rf,
             "cpu_baseline": cpu,

@@ -253,6 +253,11 @@ typedef struct {
     double ms;
 } romap_stage_time;
 romap_status romap_profile_enable(romap_ctx* ctx, int32_t on);
+/* Like enable(ctx, 1) but only the stages whose bit is set in stage_mask (bit i
+ * = stage i in romap_profile_read order) are bracketed with events; the others
+ * only count launches.  Fewer events per iteration = less timing overhead in the
+ * measured region.  0 disables. */
+romap_status romap_profile_stages(romap_ctx* ctx, uint32_t stage_mask);
 romap_status romap_profile_read(romap_ctx* ctx, romap_stage_time* out, int32_t max_stages, int32_t* n_stages);
 
 /* Measurement hook (bench.py timing rules): when bytes > 0, train_step writes a

@@ -7,9 +7,10 @@
 // fp16 w, g zero) -- see DESIGN.md "Kernels".
 #include "romap_internal.cuh"
 
-// one Adam update of 4 consecutive parameters (i0 .. i0+3, all < total)
+// one Adam update of 4 consecutive parameters (i0 .. i0+3, all < total);
+// returns whether any of them changed (tables are sparse, R18)
 __device__ __forceinline__ bool adam4(float4& pp, float4& mm, float4& vv, const float4 gg, int i0, int n_table,
-                                      float b1, float b2, float omb1, float omb2, float bc1, float bc2, float lr,
+                                      float b1, float b2, float omb1, float omb2, float ibc1, float ibc2, float lr,
                                       float eps, bool& bad) {
     float g[4] = {gg.x, gg.y, gg.z, gg.w}, p[4] = {pp.x, pp.y, pp.z, pp.w}, m[4] = {mm.x, mm.y, mm.z, mm.w},
           v[4] = {vv.x, vv.y, vv.z, vv.w};
@@ -22,9 +23,8 @@ __device__ __forceinline__ bool adam4(float4& pp, float4& mm, float4& vv, const 
         bad |= !isfinite(gj);
         const float mj = b1 * m[j] + omb1 * gj;
         const float vj = b2 * v[j] + omb2 * gj * gj;
-        const float mh = mj / bc1;
-        const float vh = vj / bc2;
-        p[j] = p[j] - lr * mh / (sqrtf(vh) + eps);
+        // p -= lr * m_hat / (sqrt(v_hat) + eps), m_hat = m / (1 - b1^t), v_hat = v / (1 - b2^t)
+        p[j] = p[j] - lr * (mj * ibc1) / (sqrtf(vj * ibc2) + eps);
         m[j] = mj;
         v[j] = vj;
     }
@@ -34,18 +34,27 @@ __device__ __forceinline__ bool adam4(float4& pp, float4& mm, float4& vv, const 
     return any;
 }
 
-// grid (bx, n_objs): every block updates a strided share of one object's
-// parameters (g, p, m, v loaded together, two float4 groups in flight per
-// thread); the last block of the object to finish advances its Adam step
-// counter (step_d[0]; step_d[1] counts finished blocks), so no separate launch
-// is needed for the step increment.
+constexpr int ADAM_G = 4;   // float4 groups per thread (all loads issued before any math)
+
+// grid (bx, n_objs): block x of object y updates float4 groups
+// [x * 256 * ADAM_G, (x + 1) * 256 * ADAM_G) of that object's parameters (g, p,
+// m, v of all ADAM_G groups loaded together); the last block of the object to
+// finish advances its Adam step counter (step_d[0]; step_d[1] counts finished
+// blocks), so no separate launch is needed for the step increment.
 __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restrict__ objs, int* __restrict__ nonfinite,
                                               int write_half) {
     const ObjDev& ob = objs[blockIdx.y];
-    const long long t = *ob.step + 1;
-    // bias corrections in double, rounded once
-    const float bc1 = (float)(1.0 - pow((double)cfg.b1, (double)t));
-    const float bc2 = (float)(1.0 - pow((double)cfg.b2, (double)t));
+    __shared__ float sc[2];
+    __shared__ long long st;
+    if (threadIdx.x == 0) {
+        const long long t = *ob.step + 1;
+        st = t;
+        // bias corrections in double, rounded once
+        sc[0] = (float)(1.0 / (1.0 - pow((double)cfg.b1, (double)t)));
+        sc[1] = (float)(1.0 / (1.0 - pow((double)cfg.b2, (double)t)));
+    }
+    __syncthreads();
+    const float ibc1 = sc[0], ibc2 = sc[1];
     const float b1 = cfg.b1, b2 = cfg.b2, lr = cfg.lr, eps = cfg.eps;
     const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
     const int n_table = cfg.n_table;
@@ -56,31 +65,32 @@ __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restri
     float4* m4 = reinterpret_cast<float4*>(ob.m);
     float4* v4 = reinterpret_cast<float4*>(ob.v);
     bool bad = false;
-    const int stride = gridDim.x * blockDim.x;
-    auto store = [&](int q, const float4& pp, const float4& mm, const float4& vv) {
-        p4[q] = pp;
-        m4[q] = mm;
-        v4[q] = vv;
-        g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (write_half) {
-            __half2* h2 = reinterpret_cast<__half2*>(ob.p16 + 4 * q);
-            h2[0] = __floats2half2_rn(pp.x, pp.y);
-            h2[1] = __floats2half2_rn(pp.z, pp.w);
+    const int q0 = blockIdx.x * blockDim.x * ADAM_G + threadIdx.x;
+    float4 gg[ADAM_G], pp[ADAM_G], mm[ADAM_G], vv[ADAM_G];
+#pragma unroll
+    for (int j = 0; j < ADAM_G; ++j) {
+        const int q = q0 + j * blockDim.x;
+        if (q < n4) {
+            gg[j] = g4[q];
+            pp[j] = p4[q];
+            mm[j] = m4[q];
+            vv[j] = v4[q];
         }
-    };
-    int q = blockIdx.x * blockDim.x + threadIdx.x;
-    for (; q + stride < n4; q += 2 * stride) {
-        const int q2 = q + stride;
-        const float4 ga = g4[q], gb = g4[q2];
-        float4 pa = p4[q], ma = m4[q], va = v4[q];
-        float4 pb = p4[q2], mb = m4[q2], vb = v4[q2];
-        if (adam4(pa, ma, va, ga, 4 * q, n_table, b1, b2, omb1, omb2, bc1, bc2, lr, eps, bad)) store(q, pa, ma, va);
-        if (adam4(pb, mb, vb, gb, 4 * q2, n_table, b1, b2, omb1, omb2, bc1, bc2, lr, eps, bad)) store(q2, pb, mb, vb);
     }
-    if (q < n4) {
-        const float4 ga = g4[q];
-        float4 pa = p4[q], ma = m4[q], va = v4[q];
-        if (adam4(pa, ma, va, ga, 4 * q, n_table, b1, b2, omb1, omb2, bc1, bc2, lr, eps, bad)) store(q, pa, ma, va);
+#pragma unroll
+    for (int j = 0; j < ADAM_G; ++j) {
+        const int q = q0 + j * blockDim.x;
+        if (q < n4 && adam4(pp[j], mm[j], vv[j], gg[j], 4 * q, n_table, b1, b2, omb1, omb2, ibc1, ibc2, lr, eps, bad)) {
+            p4[q] = pp[j];
+            m4[q] = mm[j];
+            v4[q] = vv[j];
+            g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (write_half) {
+                __half2* h2 = reinterpret_cast<__half2*>(ob.p16 + 4 * q);
+                h2[0] = __floats2half2_rn(pp[j].x, pp[j].y);
+                h2[1] = __floats2half2_rn(pp[j].z, pp[j].w);
+            }
+        }
     }
     // scalar tail (total % 4 parameters; MLP, dense)
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
@@ -90,7 +100,7 @@ __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restri
         bad |= !isfinite(gj);
         const float mj = b1 * ob.m[i] + omb1 * gj;
         const float vj = b2 * ob.v[i] + omb2 * gj * gj;
-        const float p = ob.p32[i] - lr * (mj / bc1) / (sqrtf(vj / bc2) + eps);
+        const float p = ob.p32[i] - lr * (mj * ibc1) / (sqrtf(vj * ibc2) + eps);
         ob.p32[i] = p;
         ob.m[i] = mj;
         ob.v[i] = vj;
@@ -98,13 +108,12 @@ __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restri
         if (write_half) ob.p16[i] = __float2half_rn(p);
     }
     if (bad) atomicOr(nonfinite, 2);
-    // every thread of this block has read the step counter: count the block
-    __syncthreads();
+    // every block read the step counter before its first __syncthreads: count it
     if (threadIdx.x == 0) {
         __threadfence();
         unsigned long long* done = reinterpret_cast<unsigned long long*>(ob.step + 1);
         if (atomicAdd(done, 1ull) == (unsigned long long)(gridDim.x - 1)) {
-            *ob.step = t;
+            *ob.step = st;
             *done = 0ull;
         }
     }
@@ -114,10 +123,8 @@ void launch_adam(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int
                  bool write_half) {
     if (n_objs == 0) return;
     long long total = (long long)cfg.n_table + cfg.n_mlp;
-    int per_obj = (int)((total / 4 + 511) / 512);
-    // one full wave (8 blocks of 256 threads per SM) in total
-    int target = (lc.num_sms * 8 + n_objs - 1) / n_objs;
-    int bx = per_obj < target ? per_obj : target;
+    // every float4 group of the object covered: 256 threads x ADAM_G groups per block
+    int bx = (int)((total / 4 + 256 * ADAM_G - 1) / (256 * ADAM_G));
     if (bx < 1) bx = 1;
     dim3 grid(bx, n_objs);
     k_adam<<<grid, 256, 0, lc.st>>>(cfg, objs, nonfinite, write_half ? 1 : 0);

@@ -76,6 +76,7 @@ static const char* kStageNames[ST_COUNT] = {"raygen", "fwd_fp32", "render_loss",
 // per-stage launch counters and (optional) CUDA-event timing on the ctx stream
 struct Profiler {
     bool on = false;
+    uint32_t mask = 0xffffffffu;  // stages bracketed with events when on
     long long launches[ST_COUNT] = {};
     double ms[ST_COUNT] = {};
     std::vector<cudaEvent_t> pool;
@@ -116,6 +117,8 @@ struct romap_ctx {
     unsigned long long* hits_d = nullptr;
     int* nonfinite_d = nullptr;
     size_t stat_cap = 0;
+    float* scene_d = nullptr;    // render_scene: per object C (rgb), A, D, t_near, HW floats each
+    size_t scene_cap = 0;
     float* io_d = nullptr;       // render / query staging
     size_t io_cap = 0;
     // last batch
@@ -131,7 +134,7 @@ struct romap_ctx {
 // bracket one launch: stage_begin returns the start event (or null)
 static cudaEvent_t stage_begin(romap_ctx* ctx, int stage) {
     ctx->prof.launches[stage]++;
-    if (!ctx->prof.on) return nullptr;
+    if (!ctx->prof.on || !((ctx->prof.mask >> stage) & 1u)) return nullptr;
     cudaEvent_t e = ctx->prof.get();
     cudaEventRecord(e, ctx->st);
     return e;
@@ -367,6 +370,7 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->rays);
     dfree(ctx, ctx->samp);
     dfree(ctx, ctx->srec);
+    dfree(ctx, ctx->scene_d);
     dfree(ctx, ctx->act);
     dfree(ctx, ctx->objdev_d);
     dfree(ctx, ctx->single_d);
@@ -701,7 +705,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     for (int it = 0; it < n_iters; ++it) {
         if (it == n_iters - 1) CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
         if (ctx->flush_bytes) {
-            cudaEvent_t e0 = ctx->prof.on ? ctx->prof.get() : nullptr;
+            cudaEvent_t e0 = (ctx->prof.on && ((ctx->prof.mask >> ST_FLUSH) & 1u)) ? ctx->prof.get() : nullptr;
             if (e0) cudaEventRecord(e0, ctx->st);
             CK(cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st));
             stage_end(ctx, ST_FLUSH, e0);
@@ -879,8 +883,45 @@ romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, 
                                 const romap_intrinsics* K, int32_t samples_per_segment, float* rgb, float* depth,
                                 float* opacity, int32_t flags) {
     CHECK_CTX();
-    (void)objs; (void)n; (void)T_wc; (void)K; (void)samples_per_segment; (void)rgb; (void)depth; (void)opacity; (void)flags;
-    return fail(ROMAP_E_INVALID, "render_scene is not implemented in this version");
+    if (!objs || n < 1) return fail(ROMAP_E_INVALID, "empty object list");
+    if (!T_wc || !K || K->width < 1 || K->height < 1 || !(K->fx > 0) || !(K->fy > 0))
+        return fail(ROMAP_E_INVALID, "bad pose / intrinsics");
+    const int N = samples_per_segment;
+    if (N < 1 || N > 128) return fail(ROMAP_E_INVALID, "samples_per_segment must be in [1,128]");
+    std::vector<Object*> obs;
+    for (int i = 0; i < n; ++i) {
+        Object* ob = find(ctx, objs[i]);
+        if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", objs[i]);
+        for (int j = 0; j < i; ++j)
+            if (objs[j] == objs[i]) return fail(ROMAP_E_INVALID, "object %d listed twice", objs[i]);
+        obs.push_back(ob);
+    }
+    // R20 tie-break: equal t_near -> smaller object id first; slices in id order
+    std::sort(obs.begin(), obs.end(), [](const Object* a, const Object* b) { return a->id < b->id; });
+    const long long HW = (long long)K->width * K->height;
+    if (!grow(ctx, ctx->scene_d, ctx->scene_cap, (size_t)6 * HW * obs.size()))
+        return fail(ROMAP_E_OOM, "scene segment buffer");
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    for (size_t o = 0; o < obs.size(); ++o) {
+        float* sl = ctx->scene_d + 6 * HW * o;   // C (3 HW, interleaved rgb), A, D, t_near
+        romap_status st = render_one(ctx, obs[o], T_wc, K, N, sl, sl + 4 * HW, sl + 3 * HW, ROMAP_DEVICE_PTRS);
+        if (st) return st;
+        launch_seg_tnear(lc, ctx->rays, HW, sl + 5 * HW);
+    }
+    if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)HW * 5)) return fail(ROMAP_E_OOM, "output buffer");
+    const bool dev = flags & ROMAP_DEVICE_PTRS;
+    float* o_rgb = dev ? rgb : (rgb ? ctx->io_d : nullptr);
+    float* o_dep = dev ? depth : (depth ? ctx->io_d + 3 * HW : nullptr);
+    float* o_opa = dev ? opacity : (opacity ? ctx->io_d + 4 * HW : nullptr);
+    launch_scene_composite(lc, (int)obs.size(), HW, ctx->scene_d, o_rgb, o_dep, o_opa);
+    CK(cudaGetLastError());
+    if (!dev) {
+        if (rgb) CK(cudaMemcpyAsync(rgb, o_rgb, HW * 3 * 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (depth) CK(cudaMemcpyAsync(depth, o_dep, HW * 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (opacity) CK(cudaMemcpyAsync(opacity, o_opa, HW * 4, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+    }
+    return ROMAP_OK;
 }
 
 romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, int64_t n, float* sigma,
@@ -1082,6 +1123,17 @@ romap_status romap_profile_enable(romap_ctx* ctx, int32_t on) {
     CK(cudaStreamSynchronize(ctx->st));
     prof_collect(ctx);
     ctx->prof.on = on != 0;
+    ctx->prof.mask = 0xffffffffu;
+    for (int i = 0; i < ST_COUNT; ++i) { ctx->prof.launches[i] = 0; ctx->prof.ms[i] = 0.0; }
+    return ROMAP_OK;
+}
+
+romap_status romap_profile_stages(romap_ctx* ctx, uint32_t stage_mask) {
+    CHECK_CTX();
+    CK(cudaStreamSynchronize(ctx->st));
+    prof_collect(ctx);
+    ctx->prof.on = stage_mask != 0;
+    ctx->prof.mask = stage_mask;
     for (int i = 0; i < ST_COUNT; ++i) { ctx->prof.launches[i] = 0; ctx->prof.ms[i] = 0.0; }
     return ROMAP_OK;
 }

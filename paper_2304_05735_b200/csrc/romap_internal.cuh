@@ -306,6 +306,9 @@ void launch_render_rays(const LaunchCtx& lc, const ObjDev* obj, const KfDev* cam
 void launch_composite(const LaunchCtx& lc, int N, const RayRec* rays, int n_rays, const float* sigma,
                       const float* rgb, const float* dist, const float* delta, float* out_rgb, float* out_depth,
                       float* out_opacity);
+void launch_seg_tnear(const LaunchCtx& lc, const RayRec* rays, long long n, float* tn);
+void launch_scene_composite(const LaunchCtx& lc, int n_obj, long long HW, const float* seg, float* rgb, float* depth,
+                            float* opa);
 void launch_query_density(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz, long long n,
                           float* sigma);
 void launch_debug_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,

@@ -101,6 +101,7 @@ _SIGS = {
     "romap_sync": [_P],
     "romap_profile_enable": [_P, _I],
     "romap_profile_read": [_P, _P, _I, C.POINTER(_I)],
+    "romap_profile_stages": [_P, C.c_uint32],
     "romap_set_l2_flush": [_P, C.c_int64],
 }
 
@@ -318,8 +319,16 @@ class Context:
     def set_l2_flush(self, nbytes: int):
         _check(_lib.romap_set_l2_flush(self._h, int(nbytes)))
 
-    def profile_enable(self, on: bool = True):
-        _check(_lib.romap_profile_enable(self._h, 1 if on else 0))
+    def profile_enable(self, on: bool = True, stages=None):
+        """Per-stage event timing; `stages` (names) restricts the events to those stages."""
+        if stages is None or not on:
+            _check(_lib.romap_profile_enable(self._h, 1 if on else 0))
+            return
+        names = list(self.profile_read().keys())
+        mask = 0
+        for s in stages:
+            mask |= 1 << names.index(s)
+        _check(_lib.romap_profile_stages(self._h, mask))
 
     def profile_read(self) -> dict:
         arr = (StageTime * 16)()

@@ -1,0 +1,147 @@
+// Microbenchmark: per-SM throughput of random 16-byte gathers / reductions over
+// an L2-resident table, via (A) LDG.128, (B) RED.v4.f32, (C) TMA gather4,
+// (D) TMA reduce-scatter4.  Decides whether the hash-grid gather/scatter should
+// leave the L1TEX path.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+__device__ __forceinline__ uint32_t hsh(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
+}
+
+constexpr int PER = 1024;   // accesses per thread
+
+__global__ void k_ldg(const uint4* __restrict__ tab, uint32_t rows, uint32_t* out) {
+    uint32_t acc = 0, seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER; ++i) {
+        uint4 v = __ldg(tab + (hsh(seed * PER + i) % rows));
+        acc += v.x ^ v.w;
+    }
+    if (acc == 0x12345) out[0] = acc;
+}
+
+__global__ void k_red(float4* tab, uint32_t rows) {
+    uint32_t seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER; ++i) {
+        float4* p = tab + (hsh(seed * PER + i) % rows);
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %1, %1, %1};" :: "l"(p), "f"(1.0f));
+    }
+}
+
+// TMA gather4: one elected lane per warp issues 32*PER/4 gather4 (same number of
+// 16-B rows as the warp's 32*PER LDGs) into a per-warp smem ring
+__global__ void k_tma_gather(const __grid_constant__ CUtensorMap tm, uint32_t rows, uint32_t* out) {
+    __shared__ __align__(128) uint8_t ring[8][8][128];   // warp, slot, 4 rows x 16 B (128-B aligned slots)
+    __shared__ __align__(8) uint64_t mbar[8];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = 32 * PER / 4;
+    if (lane == 0) {
+        uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar[w]);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        uint32_t seed = (blockIdx.x * 8 + w) * n;
+        uint32_t phase = 0;
+        for (int i = 0; i < n; i += 8) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(8 * 64));
+            for (int j = 0; j < 8; ++j) {
+                uint32_t s = (uint32_t)__cvta_generic_to_shared(&ring[w][j][0]);
+                int r0 = hsh(seed + 4 * (i + j)) % rows, r1 = hsh(seed + 4 * (i + j) + 1) % rows;
+                int r2 = hsh(seed + 4 * (i + j) + 2) % rows, r3 = hsh(seed + 4 * (i + j) + 3) % rows;
+                asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                             :: "r"(s), "l"(&tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(mb) : "memory");
+            }
+            asm volatile("{\n.reg .pred P;\nW: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W;\n}" :: "r"(mb), "r"(phase) : "memory");
+            phase ^= 1;
+        }
+        if (ring[w][0][0] == 0x7b) out[0] = 1;
+    }
+}
+
+__global__ void k_tma_reduce(const __grid_constant__ CUtensorMap tm, uint32_t rows) {
+    __shared__ __align__(128) float src[8][32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 8 * 32; i += blockDim.x) (&src[0][0])[i] = 1.0f;
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    const int n = 32 * PER / 4;
+    if (lane == 0) {
+        uint32_t s = (uint32_t)__cvta_generic_to_shared(&src[w][0]);
+        uint32_t seed = (blockIdx.x * 8 + w) * n;
+        for (int i = 0; i < n; ++i) {
+            int r0 = hsh(seed + 4 * i) % rows, r1 = hsh(seed + 4 * i + 1) % rows;
+            int r2 = hsh(seed + 4 * i + 2) % rows, r3 = hsh(seed + 4 * i + 3) % rows;
+            asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+                         :: "l"(&tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(s) : "memory");
+            if ((i & 31) == 31) {
+                asm volatile("cp.async.bulk.commit_group;");
+                asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+            }
+        }
+        asm volatile("cp.async.bulk.commit_group;");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+    const uint32_t rows = (4u << 20) / 16;   // 4 MB table (L2-resident)
+    void* tab;
+    CK(cudaMalloc(&tab, (size_t)rows * 16));
+    CK(cudaMemset(tab, 0, (size_t)rows * 16));
+    uint32_t* out;
+    CK(cudaMalloc(&out, 16));
+    EncodeFn enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q));
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {4, rows};
+    cuuint64_t strides[1] = {16};
+    cuuint32_t box[2] = {4, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, tab, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int clk;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double accesses = (double)sms * 256 * PER;   // 16-B rows touched per launch
+    for (int blocks_per_sm : {1, 2, 4}) {
+        const int grid = sms * blocks_per_sm;
+        const double acc = accesses * blocks_per_sm;
+        for (int mode = 0; mode < 4; ++mode) {
+            float best = 1e30f;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(e0);
+                if (mode == 0) k_ldg<<<grid, 256>>>((const uint4*)tab, rows, out);
+                if (mode == 1) k_red<<<grid, 256>>>((float4*)tab, rows);
+                if (mode == 2) k_tma_gather<<<grid, 256>>>(tm, rows, out);
+                if (mode == 3) k_tma_reduce<<<grid, 256>>>(tm, rows);
+                cudaEventRecord(e1);
+                CK(cudaEventSynchronize(e1));
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (ms < best) best = ms;
+            }
+            CK(cudaGetLastError());
+            const char* names[4] = {"LDG.128 gather", "RED.v4.f32", "TMA gather4", "TMA reduce scatter4"};
+            double per_cyc = acc / (best * 1e-3) / ((double)clk * 1e3) / sms;
+            printf("%d CTA/SM %-20s %8.3f ms  %6.3f rows(16B)/cycle/SM  %7.1f GB/s\n", blocks_per_sm, names[mode], best,
+                   per_cyc, acc * 16 / (best * 1e-3) / 1e9);
+        }
+    }
+    return 0;
+}
