@@ -62,6 +62,7 @@ constexpr int NG = 128 * NGW;                  // gather/scatter threads
 constexpr int NM = 128;                        // MLP/render threads (M)
 constexpr int NT = NG + NM;
 constexpr int BAR_M = 1;                       // named barrier of M
+constexpr int MERGE_RES = 64;                  // levels below this resolution merge same-cell scatters
 
 // shared-memory layout (bytes); every block is a multiple of 1024
 constexpr int OFF_W1 = 0;                      // 64 x LF(<=32)
@@ -441,31 +442,67 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                     xv[q][p] = (ag_ && !same) ? ldg_u32(tab + e[q][2 * p + 1]) : 0u;
                 }
             }
-            // (2) scatter of the same levels of tile it-2 (fire-and-forget REDs)
+            // (2) scatter of the same levels of tile it-2 (fire-and-forget REDs).
+            // Coarse levels (res < MERGE_RES): consecutive samples of a ray often
+            // share a cell, i.e. all 8 corners; a 2-step warp segmented sum over
+            // runs of equal cells lets one lane per 4 run members issue the REDs
+            // (RED requests, not bytes, bound this kernel).
             if (ds_) {
                 float g[4];
                 tc::tmem_ld4_sync(df_lane + 32 * b + 2 * l, g);
-                if (as_) {
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        Cell cs;
-                        unsigned es[8];
-                        level_entries(um2, P[q], off[q], hmask, cs, es);
-                        const float g0 = g[2 * q] * inv_scale, g1 = g[2 * q + 1] * inv_scale;
+                for (int q = 0; q < 2; ++q) {
+                    Cell cs;
+                    unsigned es[8];
+                    level_entries(um2, P[q], off[q], hmask, cs, es);
+                    const float g0 = as_ ? g[2 * q] * inv_scale : 0.f, g1 = as_ ? g[2 * q + 1] * inv_scale : 0.f;
+                    float v[16];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        const float wa = corner_weight(cs, 2 * p), wb = corner_weight(cs, 2 * p + 1);
+                        v[4 * p] = wa * g0;
+                        v[4 * p + 1] = wa * g1;
+                        v[4 * p + 2] = wb * g0;
+                        v[4 * p + 3] = wb * g1;
+                    }
+                    bool issue = as_;
+                    if (P[q].x < MERGE_RES) {                     // warp-uniform
+                        const unsigned key = as_ ? ((unsigned)cs.c[0] | ((unsigned)cs.c[1] << 10) |
+                                                    ((unsigned)cs.c[2] << 20))
+                                                 : (0x80000000u | (unsigned)lane);
+#pragma unroll
+                        for (int o = 1; o <= 2; o <<= 1) {
+                            const unsigned ko = __shfl_down_sync(0xffffffffu, key, o);
+                            const bool mg = lane + o < 32 && ko == key;
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const float w = __shfl_down_sync(0xffffffffu, v[k], o);
+                                if (mg) v[k] += w;
+                            }
+                        }
+                        // lane holds the sum over [lane, lane + 4) of its run; the
+                        // lanes at run start + 4 m issue
+                        const unsigned kp = __shfl_up_sync(0xffffffffu, key, 1);
+                        const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || kp != key);
+                        const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+                        issue = issue && ((lane - run0) & 3) == 0;
+                    }
+                    if (issue) {
 #pragma unroll
                         for (int p = 0; p < 4; ++p) {
                             // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
                             // REDG.F32x4, else two REDG.F32x2
                             const unsigned ea = es[2 * p], eb = es[2 * p + 1];
-                            const float wa = corner_weight(cs, 2 * p), wb = corner_weight(cs, 2 * p + 1);
                             if ((ea >> 1) == (eb >> 1)) {
                                 if (ea < eb)
-                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + ea), wa * g0, wa * g1, wb * g0, wb * g1);
+                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + ea), v[4 * p], v[4 * p + 1],
+                                               v[4 * p + 2], v[4 * p + 3]);
                                 else
-                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + eb), wb * g0, wb * g1, wa * g0, wa * g1);
+                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + eb), v[4 * p + 2], v[4 * p + 3],
+                                               v[4 * p], v[4 * p + 1]);
                             } else {
-                                red_add_f2(g_m2 + ea, wa * g0, wa * g1);
-                                red_add_f2(g_m2 + eb, wb * g0, wb * g1);
+                                red_add_f2(g_m2 + ea, v[4 * p], v[4 * p + 1]);
+                                red_add_f2(g_m2 + eb, v[4 * p + 2], v[4 * p + 3]);
                             }
                         }
                     }

@@ -35,6 +35,45 @@ __global__ void k_red(float4* tab, uint32_t rows) {
     }
 }
 
+__global__ void k_ldg256(const float* __restrict__ tab, uint32_t rows32, uint32_t* out) {
+    float acc = 0.f;
+    uint32_t seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER; ++i) {
+        const float* p = tab + 8ull * (hsh(seed * PER + i) % rows32);
+        float a0, a1, a2, a3, a4, a5, a6, a7;
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(a4), "=f"(a5), "=f"(a6), "=f"(a7) : "l"(p));
+        acc += a0 + a7;
+    }
+    if (acc == 1234.5f) out[0] = 1;
+}
+
+__global__ void k_ldg32(const uint32_t* __restrict__ tab, uint32_t rows4, uint32_t* out) {
+    uint32_t acc = 0, seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER; ++i) acc += __ldg(tab + (hsh(seed * PER + i) % rows4));
+    if (acc == 0x12345) out[0] = acc;
+}
+
+__global__ void k_red2(float2* tab, uint32_t rows8) {
+    uint32_t seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER; ++i) {
+        float2* p = tab + (hsh(seed * PER + i) % rows8);
+        asm volatile("red.global.add.v2.f32 [%0], {%1, %1};" :: "l"(p), "f"(1.0f));
+    }
+}
+
+__global__ void k_redh(uint4* tab, uint32_t rows) {
+    uint32_t seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER; ++i) {
+        uint4* p = tab + (hsh(seed * PER + i) % rows);
+        asm volatile("red.global.add.noftz.v4.f16x2 [%0], {%1, %1, %1, %1};" :: "l"(p), "r"(0x3c003c00u));
+    }
+}
+
 // TMA gather4: one elected lane per warp issues 32*PER/4 gather4 (same number of
 // 16-B rows as the warp's 32*PER LDGs) into a per-warp smem ring
 __global__ void k_tma_gather(const __grid_constant__ CUtensorMap tm, uint32_t rows, uint32_t* out) {
@@ -119,10 +158,10 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const double accesses = (double)sms * 256 * PER;   // 16-B rows touched per launch
-    for (int blocks_per_sm : {1, 2, 4}) {
+    for (int blocks_per_sm : {2}) {
         const int grid = sms * blocks_per_sm;
         const double acc = accesses * blocks_per_sm;
-        for (int mode = 0; mode < 4; ++mode) {
+        for (int mode = 0; mode < 8; ++mode) {
             float best = 1e30f;
             for (int rep = 0; rep < 5; ++rep) {
                 cudaEventRecord(e0);
@@ -130,6 +169,10 @@ int main() {
                 if (mode == 1) k_red<<<grid, 256>>>((float4*)tab, rows);
                 if (mode == 2) k_tma_gather<<<grid, 256>>>(tm, rows, out);
                 if (mode == 3) k_tma_reduce<<<grid, 256>>>(tm, rows);
+                if (mode == 4) k_ldg256<<<grid, 256>>>((const float*)tab, rows / 2, out);
+                if (mode == 5) k_ldg32<<<grid, 256>>>((const uint32_t*)tab, rows * 4, out);
+                if (mode == 6) k_red2<<<grid, 256>>>((float2*)tab, rows * 2);
+                if (mode == 7) k_redh<<<grid, 256>>>((uint4*)tab, rows);
                 cudaEventRecord(e1);
                 CK(cudaEventSynchronize(e1));
                 float ms;
@@ -137,10 +180,10 @@ int main() {
                 if (ms < best) best = ms;
             }
             CK(cudaGetLastError());
-            const char* names[4] = {"LDG.128 gather", "RED.v4.f32", "TMA gather4", "TMA reduce scatter4"};
+            const char* names[8] = {"LDG.128 gather", "RED.v4.f32", "TMA gather4", "TMA reduce scatter4",
+                                    "LDG.256 gather", "LDG.32 gather", "RED.v2.f32", "RED.v4.f16x2"};
             double per_cyc = acc / (best * 1e-3) / ((double)clk * 1e3) / sms;
-            printf("%d CTA/SM %-20s %8.3f ms  %6.3f rows(16B)/cycle/SM  %7.1f GB/s\n", blocks_per_sm, names[mode], best,
-                   per_cyc, acc * 16 / (best * 1e-3) / 1e9);
+            printf("%d CTA/SM %-20s %8.3f ms  %6.3f accesses/cycle/SM\n", blocks_per_sm, names[mode], best, per_cyc);
         }
     }
     return 0;

@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = {"k_raygen": "raygen", "k_fwd_fp32": "fwd_fp32", "k_render_loss": "render_loss", "k_bwd_fp32": "bwd_fp32",
+STAGE = {"k_raygen_samples": "raygen", "k_raygen": "raygen", "k_fwd_fp32": "fwd_fp32", "k_render_loss": "render_loss", "k_bwd_fp32": "bwd_fp32",
          "k_fused_mixed": "fused_mixed", "k_adam": "adam", "k_step_inc": "step_inc", "k_zero_grads": "zero_grads"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -22,6 +22,14 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
 
 
+def norm(name):
+    """'void k_fused_mixed<16>(CfgDev, ...)' -> 'k_fused_mixed'"""
+    n = name.split("(")[0].strip()
+    if n.startswith("void "):
+        n = n[5:]
+    return n.split("<")[0].strip()
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
@@ -30,7 +38,7 @@ def launches(path):
     agg = collections.defaultdict(list)
     unit = None
     for r in rows[hi + 1:]:
-        agg[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
+        agg[norm(r[ki])].append(float(r[vi].replace(",", "")))
         unit = r[ui]
     scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}.get(unit, 1e-3)
     tot = sum(sum(v) for v in agg.values())
@@ -43,7 +51,7 @@ def full(path):
     hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
-        d = {"kernel": r[hdr.index("Kernel Name")].split("(")[0]}
+        d = {"kernel": norm(r[hdr.index("Kernel Name")])}
         for m in METRICS:
             if m in hdr:
                 d[m] = r[hdr.index(m)] + " " + units[hdr.index(m)]
