@@ -62,7 +62,14 @@ constexpr int NG = 128 * NGW;                  // gather/scatter threads
 constexpr int NM = 128;                        // MLP/render threads (M)
 constexpr int NT = NG + NM;
 constexpr int BAR_M = 1;                       // named barrier of M
-constexpr int MERGE_RES = 64;                  // levels below this resolution merge same-cell scatters
+#ifndef ROMAP_MERGE_RES
+#define ROMAP_MERGE_RES 64
+#endif
+#ifndef ROMAP_MERGE8_RES
+#define ROMAP_MERGE8_RES 0
+#endif
+constexpr int MERGE_RES = ROMAP_MERGE_RES;     // levels below this resolution merge same-cell scatters
+constexpr int MERGE8_RES = ROMAP_MERGE8_RES;   // ... and below this one over windows of 8 (3 steps)
 
 // shared-memory layout (bytes); every block is a multiple of 1024
 constexpr int OFF_W1 = 0;                      // 64 x LF(<=32)
@@ -332,6 +339,23 @@ __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint
     }
 }
 
+// 32-byte gather (LDG.E.256) of 8 table words, zeros when !on
+__device__ __forceinline__ void ldg_v8(const uint32_t* p, bool on, uint32_t (&w)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = 0u;
+    if (on)
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                     : "l"(p));
+}
+// word k (0..7) of 8 by a 3-level select tree
+__device__ __forceinline__ uint32_t sel8(const uint32_t (&w)[8], unsigned k) {
+    const bool b0 = k & 1u, b1 = k & 2u, b2 = k & 4u;
+    const uint32_t a0 = b0 ? w[1] : w[0], a1 = b0 ? w[3] : w[2], a2 = b0 ? w[5] : w[4], a3 = b0 ? w[7] : w[6];
+    const uint32_t c0 = b1 ? a1 : a0, c1 = b1 ? a3 : a2;
+    return b2 ? c1 : c0;
+}
+
 // cell and the 8 corner entries of one level (R5), as absolute entry indices
 // (level offset `off` added): P = {res, y multiplier, z multiplier, dense};
 // dense: x + (N+1) y + (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^
@@ -409,8 +433,12 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
         }
         FP_MARK(g_w1);
         FP_ACC(9, g_w0, g_w1);
+#ifdef ROMAP_EXP_NOG
+        const bool ag = false, as = false;            // experiment: G without memory traffic
+#else
         const bool ag = dg && ug[0] >= 0.f;          // sample of an active ray (k_raygen_samples)
         const bool as = ds && um2[0] >= 0.f;
+#endif
         const unsigned flags_it = (dg ? 1u : 0u) | (ds ? 2u : 0u) | (ag ? 4u : 0u) | (as ? 8u : 0u);
         uint8_t* X0 = smem + OFF_X0 + b * X0_BYTES;
 #pragma unroll 1
@@ -428,7 +456,13 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             // entries e, e+1; hashed: e ^ (x ^ (x+1)) with the x prime = 1), so each
             // corner pair is one 16-B gather (+ a 4-B one otherwise); level blocks
             // are 16-entry aligned (R5).
+#ifdef ROMAP_LDG256
+            // 32-byte gathers: the aligned 8-entry group holds the x-neighbour in
+            // 7 of 8 cases (hashed: e ^ 1, e ^ 3, e ^ 7; dense: e + 1)
+            uint32_t qw[2][4][8];
+#else
             uint4 qv[2][4];
+#endif
             uint32_t xv[2][4];
             unsigned e[2][8];
             Cell cl[2];
@@ -437,8 +471,13 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                 level_entries(ug, P[q], off[q], hmask, cl[q], e[q]);
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
+#ifdef ROMAP_LDG256
+                    const bool same = (e[q][2 * p] >> 3) == (e[q][2 * p + 1] >> 3);
+                    ldg_v8(tab + (e[q][2 * p] & ~7u), ag_, qw[q][p]);
+#else
                     const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
                     qv[q][p] = ag_ ? ldg_v4(tab + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+#endif
                     xv[q][p] = (ag_ && !same) ? ldg_u32(tab + e[q][2 * p + 1]) : 0u;
                 }
             }
@@ -470,8 +509,11 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const unsigned key = as_ ? ((unsigned)cs.c[0] | ((unsigned)cs.c[1] << 10) |
                                                     ((unsigned)cs.c[2] << 20))
                                                  : (0x80000000u | (unsigned)lane);
+                        const int omax = P[q].x < MERGE8_RES ? 4 : 2;
+                        const unsigned wmask = 2u * omax - 1u;
 #pragma unroll
-                        for (int o = 1; o <= 2; o <<= 1) {
+                        for (int o = 1; o <= 4; o <<= 1) {
+                            if (o > omax) break;
                             const unsigned ko = __shfl_down_sync(0xffffffffu, key, o);
                             const bool mg = lane + o < 32 && ko == key;
 #pragma unroll
@@ -485,7 +527,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const unsigned kp = __shfl_up_sync(0xffffffffu, key, 1);
                         const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || kp != key);
                         const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
-                        issue = issue && ((lane - run0) & 3) == 0;
+                        issue = issue && ((lane - run0) & wmask) == 0;
                     }
                     if (issue) {
 #pragma unroll
@@ -520,9 +562,15 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
                         const unsigned ea = e[q][2 * p], eb = e[q][2 * p + 1];
+#ifdef ROMAP_LDG256
+                        const bool same = (ea >> 3) == (eb >> 3);
+                        const uint32_t h0 = sel8(qw[q][p], ea & 7);
+                        const uint32_t h1 = same ? sel8(qw[q][p], eb & 7) : xv[q][p];
+#else
                         const bool same = (ea >> 2) == (eb >> 2);
                         const uint32_t h0 = sel4(qv[q][p], ea & 3);
                         const uint32_t h1 = same ? sel4(qv[q][p], eb & 3) : xv[q][p];
+#endif
                         const __half2 a = *reinterpret_cast<const __half2*>(&h0);
                         const __half2 c = *reinterpret_cast<const __half2*>(&h1);
                         vx[p] = __hfma2(fx, __hsub2(c, a), a);
@@ -655,6 +703,15 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         FP_MARK(m_t1);
         tc::mbar_wait(&misc->x0_full[b], (j >> 1) & 1);
         FP_MARK(m_t2);
+#ifdef ROMAP_EXP_NOM
+        if (leader) {                                  // experiment: M hands the tile straight back
+            if (j >= 2) tc::mbar_wait(&misc->df_empty[b], ((j - 2) >> 1) & 1);
+            tc::fence_after();
+            tc::commit(&misc->tile_done[b]);
+        }
+        dw_fresh = false;
+        continue;
+#endif
         m_sync_for_mma();
         const uint32_t sX0 = tc::smem_u32(smem + OFF_X0 + b * X0_BYTES);
 

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libromap.so")
+LIB_PATH = os.environ.get("ROMAP_LIB") or os.path.join(_HERE, "libromap.so")   # ROMAP_LIB: experiment builds
 
 OK = 0
 E_INVALID, E_NOT_FOUND, E_OOM, E_CUDA, E_NONFINITE, E_CONFIG_MISMATCH, E_STATE = -1, -2, -3, -4, -5, -6, -7
