@@ -266,11 +266,12 @@ def run_ours(args):
             precision = 0
     kw = cfg1_kwargs(precision)
     scene = load_scene()
+    from paper_2304_05735_b200.shard import partition, reduce_throughput
     objs = []
     ob = scene.objects[0]
-    h2d_kf = []
-    for i in range(args.objects_per_gpu):
-        gid = rank * args.objects_per_gpu + i
+    n_total = args.objects or args.objects_per_gpu * ws
+    mine = partition([kw["rays_per_iter"] * kw["samples_per_ray"]] * n_total, ws)[rank]   # LPT by cost (8(e))
+    for gid in mine:
         h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id, obj_id=gid)
         for fr in scene.frames[:args.keyframes]:
             ctx.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
@@ -346,16 +347,9 @@ def run_ours(args):
     if pg:
         pg.barrier()
 
-    # reductions over ranks: max time, sum of samples (one NCCL all_reduce each)
-    t_dev = torch.tensor([step_ms * args.steps, e2e_s], dtype=torch.float64, device="cuda")
-    n_dev = torch.tensor([float(samples), float(e2e_samples)], dtype=torch.float64, device="cuda")
-    if pg:
-        pg.all_reduce(t_dev, op=pg.ReduceOp.MAX)
-        pg.all_reduce(n_dev, op=pg.ReduceOp.SUM)
-    t_max_ms, e2e_max_s = t_dev.tolist()
-    tot_samples, tot_e2e = n_dev.tolist()
-    value = tot_samples / (t_max_ms * 1e-3)
-    e2e_value = tot_e2e / e2e_max_s
+    # reductions over ranks: max time, sum of samples (NCCL all_reduce, shard.reduce_throughput)
+    t_max_ms, tot_samples, value = reduce_throughput(step_ms * args.steps, samples, pg, device="cuda")
+    e2e_max_ms, tot_e2e, e2e_value = reduce_throughput(e2e_s * 1e3, e2e_samples, pg, device="cuda")
 
     if rank == 0:
         rf = roofline(prof, kw, precision, samples / args.steps, len(objs))
@@ -364,11 +358,13 @@ def run_ours(args):
         line = {
             "metric": "NeRF train ray-samples/s", "value": value, "unit": "ray-samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.objects else "weak", "vs_baseline": None,
             "dtype": "f16-mma/f32" if precision == 1 else "f32",
             "data": "synthetic (seeded box-union-torus SDF object on a textured floor, 20 keyframes 640x480, 1 cm pose jitter)",
-            "config": {"workload": "cfg1: 1 object per GPU, L=16 F=2 T=2^16 res 16->512, density 32->64->16 + SH4 colour "
-                                   "32->64->64->3, 4096 rays x 64 stratified samples, Adam",
+            "config": {"workload": (f"cfg1 family: {n_total} object(s) over {ws} GPU(s) (LPT by cost)" if args.objects
+                                    else f"cfg1: {len(objs)} object(s) per GPU") +
+                                   ", L=16 F=2 T=2^16 res 16->512, density 32->64->16 + SH4 colour "
+                                   "32->64->64->3, 4096 rays x 64 stratified samples per object, Adam",
                        "objects_per_gpu": len(objs), "rays_per_iter": kw["rays_per_iter"],
                        "samples_per_ray": kw["samples_per_ray"], "keyframes": args.keyframes,
                        "precision": "mixed" if precision == 1 else "fp32",
@@ -406,6 +402,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["auto", "mixed", "fp32"], default="auto")
     ap.add_argument("--objects-per-gpu", type=int, default=1)
+    ap.add_argument("--objects", type=int, default=0,
+                    help="total objects over all ranks, LPT-partitioned (0: objects-per-gpu x ranks)")
     ap.add_argument("--keyframes", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--e2e-iters", type=int, default=50)
