@@ -391,7 +391,7 @@ __device__ __forceinline__ void level_entries(const float u[3], const int4 P, un
 template <int L>
 __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
                                        const RayRec* __restrict__ rays, const float4* __restrict__ srec, int tile0,
-                                       int n, uint8_t* smem, Misc* misc, uint32_t tm) {
+                                       int tstride, int n, uint8_t* smem, Misc* misc, uint32_t tm) {
     constexpr int LF = 2 * L;
     const int t = threadIdx.x, r = t & (TILE - 1), lane = t & 31, q4 = (t >> 5) & 3, WG = t >> 7;
     const int N = cfg.N;
@@ -399,6 +399,8 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     const float inv_scale = 1.0f / cfg.loss_scale;
     const uint32_t df_lane = tc::taddr(tm, q4 * 32, TM_DF);
 
+    // tile j of this CTA = tile0 + j * tstride (strided over the grid: all CTAs
+    // work on neighbouring tiles, i.e. on the same object, at any time)
     float4 u_next = srec[(long long)tile0 * TILE + r];
     int slot_next = rays[(int)(((long long)tile0 * TILE) / N)].slot;
     int slot_tab = -1;
@@ -418,8 +420,9 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
         const float ug[3] = {u_next.x, u_next.y, u_next.z};
         const int slot_g = slot_next;
         if (it + 1 < n) {
-            u_next = srec[(long long)(tile0 + it + 1) * TILE + r];
-            slot_next = rays[(int)(((long long)(tile0 + it + 1) * TILE) / N)].slot;
+            const long long tn = (long long)tile0 + (long long)(it + 1) * tstride;
+            u_next = srec[tn * TILE + r];
+            slot_next = rays[(int)((tn * TILE) / N)].slot;
         }
         if (dg && slot_g != slot_tab) {
             tab = reinterpret_cast<const uint32_t*>(objs[slot_g].p16);
@@ -635,7 +638,8 @@ __device__ __forceinline__ MIn m_load(const RayRec* __restrict__ rays, const flo
 template <int L>
 __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
                                        const RayRec* __restrict__ rays, const float4* __restrict__ srec,
-                                       const float* __restrict__ sdelta, int tile0, int n, uint8_t* smem, Misc* misc,
+                                       const float* __restrict__ sdelta, int tile0, int tstride, int n, uint8_t* smem,
+                                       Misc* misc,
                                        uint32_t tm, double* __restrict__ loss_acc, int* __restrict__ nonfinite,
                                        float* __restrict__ dbg) {
     constexpr int LF = 2 * L;
@@ -675,11 +679,12 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     MIn nx = m_load(rays, srec, sdelta, (long long)tile0 * TILE + m, N);
     for (int j = 0; j < n; ++j) {
         FP_MARK(m_t0);
-        const int tile = tile0 + j, b = j & 1;
+        const long long tile = (long long)tile0 + (long long)j * tstride;
+        const int b = j & 1;
         const long long s = (long long)tile * TILE + m;
         const int i = (int)(s % N);
         const MIn rr = nx;
-        if (j + 1 < n) nx = m_load(rays, srec, sdelta, s + TILE, N);
+        if (j + 1 < n) nx = m_load(rays, srec, sdelta, s + (long long)tstride * TILE, N);
         const float delta = rr.delta;
         const bool active = (rr.flags & RF_ACTIVE) != 0;
         if (rr.slot != cur) {                      // uniform: a tile holds rays of one object
@@ -986,13 +991,13 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     __syncthreads();
     tc::fence_after();
     const uint32_t tm = misc->tmem;
-    const int tile0 = blockIdx.x * tiles_per_cta;
-    const int n = min(tiles_per_cta, n_tiles - tile0);
+    const int tile0 = blockIdx.x, tstride = gridDim.x;
+    const int n = tile0 < n_tiles ? (n_tiles - 1 - tile0) / tstride + 1 : 0;
     if (n > 0) {
         if (warp < NG / 32)
-            g_loop<L>(cfg, objs, rays, srec, tile0, n, smem, misc, tm);
+            g_loop<L>(cfg, objs, rays, srec, tile0, tstride, n, smem, misc, tm);
         else
-            m_loop<L>(cfg, objs, rays, srec, sdelta, tile0, n, smem, misc, tm, loss_acc, nonfinite, dbg);
+            m_loop<L>(cfg, objs, rays, srec, sdelta, tile0, tstride, n, smem, misc, tm, loss_acc, nonfinite, dbg);
     }
     tc::fence_before();
     __syncthreads();
@@ -1013,8 +1018,7 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
     }
     int grid = lc.num_sms;
     if (grid > n_tiles) grid = n_tiles;
-    const int per = (n_tiles + grid - 1) / grid;
-    grid = (n_tiles + per - 1) / per;
+    const int per = 0;   // unused: tiles are strided over the grid
     if (cfg.L == 16)
         k_fused_mixed<16><<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc,
                                                             nonfinite, dbg);
