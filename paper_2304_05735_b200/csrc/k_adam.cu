@@ -41,20 +41,19 @@ constexpr int ADAM_G = 4;   // float4 groups per thread (all loads issued before
 // m, v of all ADAM_G groups loaded together); the last block of the object to
 // finish advances its Adam step counter (step_d[0]; step_d[1] counts finished
 // blocks), so no separate launch is needed for the step increment.
-__global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restrict__ objs, int* __restrict__ nonfinite,
-                                              int write_half) {
+// step_d layout: [0] Adam step (i64), [1] finished-block counter (u64), [2] the
+// bias corrections 1 / (1 - beta^t) of the NEXT step t = step + 1 as two fp32
+// (computed in double, rounded once: by the host at creation / set_params, then
+// by the last block of every launch for the following step)
+__device__ __forceinline__ float2 bias_corrections(double b1, double b2, long long t) {
+    return make_float2((float)(1.0 / (1.0 - pow(b1, (double)t))), (float)(1.0 / (1.0 - pow(b2, (double)t))));
+}
+
+__global__ void __launch_bounds__(256, 3) k_adam(CfgDev cfg, const ObjDev* __restrict__ objs, int* __restrict__ nonfinite,
+                                                 int write_half) {
     const ObjDev& ob = objs[blockIdx.y];
-    __shared__ float sc[2];
-    __shared__ long long st;
-    if (threadIdx.x == 0) {
-        const long long t = *ob.step + 1;
-        st = t;
-        // bias corrections in double, rounded once
-        sc[0] = (float)(1.0 / (1.0 - pow((double)cfg.b1, (double)t)));
-        sc[1] = (float)(1.0 / (1.0 - pow((double)cfg.b2, (double)t)));
-    }
-    __syncthreads();
-    const float ibc1 = sc[0], ibc2 = sc[1];
+    const float2 bc = *reinterpret_cast<const float2*>(ob.step + 2);
+    const float ibc1 = bc.x, ibc2 = bc.y;
     const float b1 = cfg.b1, b2 = cfg.b2, lr = cfg.lr, eps = cfg.eps;
     const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
     const int n_table = cfg.n_table;
@@ -108,12 +107,16 @@ __global__ void __launch_bounds__(256) k_adam(CfgDev cfg, const ObjDev* __restri
         if (write_half) ob.p16[i] = __float2half_rn(p);
     }
     if (bad) atomicOr(nonfinite, 2);
-    // every block read the step counter before its first __syncthreads: count it
+    // every thread of this block has read the bias corrections: count the block;
+    // the last one advances the step and prepares the next step's corrections
+    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         unsigned long long* done = reinterpret_cast<unsigned long long*>(ob.step + 1);
         if (atomicAdd(done, 1ull) == (unsigned long long)(gridDim.x - 1)) {
-            *ob.step = st;
+            const long long t = *ob.step + 1;
+            *ob.step = t;
+            *reinterpret_cast<float2*>(ob.step + 2) = bias_corrections(cfg.b1, cfg.b2, t + 1);
             *done = 0ull;
         }
     }

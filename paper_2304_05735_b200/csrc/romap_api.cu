@@ -307,6 +307,16 @@ static ObjDev make_objdev(const Object* ob) {
     return d;
 }
 
+// bias corrections 1 / (1 - beta^t) of the next Adam step t = step + 1 (double,
+// rounded once), stored after the step counter for k_adam (synchronous copy)
+static cudaError_t upload_bias_corrections(romap_ctx* ctx, Object* ob) {
+    const double t = (double)(ob->step + 1);
+    float bc[2] = {(float)(1.0 / (1.0 - pow((double)ob->cdev.b1, t))), (float)(1.0 / (1.0 - pow((double)ob->cdev.b2, t)))};
+    cudaError_t e = cudaMemcpyAsync(ob->step_d + 2, bc, sizeof bc, cudaMemcpyHostToDevice, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    return e;
+}
+
 static Object* find(romap_ctx* ctx, int id) {
     auto it = ctx->objs.find(id);
     return it == ctx->objs.end() ? nullptr : it->second;
@@ -413,7 +423,7 @@ static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const roma
     ob->m = (float*)dalloc(ctx, n * 4);
     ob->v = (float*)dalloc(ctx, n * 4);
     ob->p16 = (__half*)dalloc(ctx, n * 2 + 16);
-    ob->step_d = (long long*)dalloc(ctx, 16);   // [Adam step, finished-block counter of k_adam]
+    ob->step_d = (long long*)dalloc(ctx, 32);   // [Adam step, k_adam block counter, next bias corrections]
     if (!ob->p32 || !ob->g32 || !ob->m || !ob->v || !ob->p16 || !ob->step_d) {
         free_object(ctx, ob);
         return fail(ROMAP_E_OOM, "parameter allocation failed");
@@ -436,7 +446,8 @@ static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const roma
     if (e == cudaSuccess) e = cudaMemsetAsync(ob->g32, 0, n * 4, ctx->st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ob->m, 0, n * 4, ctx->st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ob->v, 0, n * 4, ctx->st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ob->step_d, 0, 16, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ob->step_d, 0, 32, ctx->st);
+    if (e == cudaSuccess) e = upload_bias_corrections(ctx, ob);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
     if (e != cudaSuccess) {
         ctx->poisoned = true;
@@ -1018,6 +1029,7 @@ romap_status romap_set_params(romap_ctx* ctx, int32_t obj, int32_t block, const 
     }
     if (block == ROMAP_BLOCK_STEP) {
         ob->step = *(const long long*)buf;
+        CK(upload_bias_corrections(ctx, ob));
     }
     if (block == ROMAP_BLOCK_GRAD_TABLE || block == ROMAP_BLOCK_GRAD_MLP) ob->grads_dirty = false;
     CK(cudaStreamSynchronize(ctx->st));
