@@ -177,6 +177,35 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
     return out
 
 
+# ----------------------------------------------------------------------------- inference (8(a) a10, a11)
+def measure_inference(ctx, h, ob, frame, torch):
+    """cfg4-style inference on one trained object: density on the 128^3 vertex
+    lattice spanning the box (marching-cubes input, R21) with device buffers, and
+    one 640x480 render (128 midpoints per ray, host outputs)."""
+    a = [float(x) for x in ob.a]
+    axes = [torch.linspace(-a[k], a[k], 128, device="cuda") for k in range(3)]
+    P = torch.stack(torch.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3).float().contiguous()
+    ctx.query_density(h, P)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        ctx.query_density(h, P)
+    e1.record()
+    torch.cuda.synchronize()
+    q_ms = e0.elapsed_time(e1) / reps
+    ctx.render(h, frame.T_wc, frame.K, 640, 480, 128)
+    t0 = time.perf_counter()
+    ctx.render(h, frame.T_wc, frame.K, 640, 480, 128)
+    r_s = time.perf_counter() - t0
+    return {"query_density": {"points_per_s": P.shape[0] / (q_ms * 1e-3), "ms_per_lattice": q_ms,
+                              "points": int(P.shape[0]), "what": "128^3 vertex lattice of the trained object, "
+                              "device buffers, CUDA events (mixed path: fp16 tables + tcgen05 first layer)"},
+            "render": {"rays_per_s": 640 * 480 / r_s, "ms_per_frame": r_s * 1e3, "samples_per_ray": 128,
+                       "what": "one 640x480 frame, host outputs, wall clock (fp32 SIMT forward)"}}
+
+
 # ----------------------------------------------------------------------------- CPU oracle
 def oracle_run(scene, kw, rays, iters, obj_id=0):
     import numpy as np
@@ -351,6 +380,7 @@ def run_ours(args):
     t_max_ms, tot_samples, value = reduce_throughput(step_ms * args.steps, samples, pg, device="cuda")
     e2e_max_ms, tot_e2e, e2e_value = reduce_throughput(e2e_s * 1e3, e2e_samples, pg, device="cuda")
 
+    infer = measure_inference(ctx, objs[0], ob, scene.frames[0], torch) if rank == 0 else None
     if rank == 0:
         rf = roofline(prof, kw, precision, samples / args.steps, len(objs))
         cpu = None if args.no_cpu_baseline else cpu_baseline(scene, kw)
@@ -386,6 +416,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(len(objs) * 40 + 4),
                     "step": f"add_observation(1 keyframe, host) + train_step({args.e2e_iters} iterations) + stats D2H"},
             "clocks": clocks,
+            "inference": infer,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

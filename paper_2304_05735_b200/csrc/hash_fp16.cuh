@@ -1,0 +1,100 @@
+// hash_fp16.cuh -- multiresolution hash-grid helpers of the mixed path (fp16
+// tables, one 4-byte half2 word per entry), shared by the fused training kernel
+// and the mixed inference kernels.  Grid definition: DESIGN.md R5.
+#pragma once
+#include "romap_internal.cuh"
+
+// 32-byte gather (LDG.E.256) of 8 table words, zeros when !on
+__device__ __forceinline__ void ldg_v8(const uint32_t* p, bool on, uint32_t (&w)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = 0u;
+    if (on)
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                     : "l"(p));
+}
+// word k (0..7) of 8 by a 3-level select tree
+__device__ __forceinline__ uint32_t sel8(const uint32_t (&w)[8], unsigned k) {
+    const bool b0 = k & 1u, b1 = k & 2u, b2 = k & 4u;
+    const uint32_t a0 = b0 ? w[1] : w[0], a1 = b0 ? w[3] : w[2], a2 = b0 ? w[5] : w[4], a3 = b0 ? w[7] : w[6];
+    const uint32_t c0 = b1 ? a1 : a0, c1 = b1 ? a3 : a2;
+    return b2 ? c1 : c0;
+}
+
+// cell and the 8 corner entries of one level (R5), as absolute entry indices
+// (level offset `off` added): P = {res, y multiplier, z multiplier, dense};
+// dense: x + (N+1) y + (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^
+// z * 805459861) & (T - 1).  Corner b: bit k -> +1 on axis k.
+__device__ __forceinline__ void level_entries(const float u[3], const int4 P, unsigned off, unsigned hmask, Cell& cl,
+                                              unsigned (&e)[8]) {
+    cl = grid_cell(u, P.x);
+    const unsigned my = (unsigned)P.y, mz = (unsigned)P.z;
+    const unsigned x0 = (unsigned)cl.c[0], x1 = x0 + 1u;
+    const unsigned ty0 = (unsigned)cl.c[1] * my, ty1 = ty0 + my;
+    const unsigned tz0 = (unsigned)cl.c[2] * mz, tz1 = tz0 + mz;
+    if (P.w) {
+        const unsigned yz[4] = {ty0 + tz0 + off, ty1 + tz0 + off, ty0 + tz1 + off, ty1 + tz1 + off};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            e[2 * k] = x0 + yz[k];
+            e[2 * k + 1] = x1 + yz[k];
+        }
+    } else {
+        const unsigned yz[4] = {ty0 ^ tz0, ty1 ^ tz0, ty0 ^ tz1, ty1 ^ tz1};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            e[2 * k] = ((x0 ^ yz[k]) & hmask) + off;
+            e[2 * k + 1] = ((x1 ^ yz[k]) & hmask) + off;
+        }
+    }
+}
+
+// level parameters as the kernels keep them in shared memory:
+// {res, y multiplier, z multiplier, dense} (R5) and the entry offset
+__device__ __forceinline__ int4 level_params(const CfgDev& cfg, int l) {
+    const int res = cfg.res[l];
+    const bool dense = cfg.dense[l] != 0;
+    const unsigned n1 = (unsigned)res + 1u;
+    return make_int4(res, (int)(dense ? n1 : 2654435761u), (int)(dense ? n1 * n1 : 805459861u), dense ? 1 : 0);
+}
+
+// encode two levels (P0/P1 at offsets off0/off1) of one point into two half2
+// features: x-neighbour corner pairs as one LDG.128 (+ a 4-byte load when the
+// pair straddles a 16-byte chunk), packed-fp16 trilinear lerps (x, y, z); zeros
+// when !on
+__device__ __forceinline__ void encode_pair_fp16(const uint32_t* __restrict__ tab, const float u[3], const int4 P[2],
+                                                 const unsigned off[2], unsigned hmask, bool on, __half2 (&fq)[2]) {
+    uint4 qv[2][4];
+    uint32_t xv[2][4];
+    unsigned e[2][8];
+    Cell cl[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        level_entries(u, P[q], off[q], hmask, cl[q], e[q]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
+            qv[q][p] = on ? ldg_v4(tab + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+            xv[q][p] = (on && !same) ? ldg_u32(tab + e[q][2 * p + 1]) : 0u;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const __half2 fx = __float2half2_rn(cl[q].f[0]), fy = __float2half2_rn(cl[q].f[1]),
+                      fz = __float2half2_rn(cl[q].f[2]);
+        __half2 vx[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const unsigned ea = e[q][2 * p], eb = e[q][2 * p + 1];
+            const bool same = (ea >> 2) == (eb >> 2);
+            const uint32_t h0 = sel4(qv[q][p], ea & 3);
+            const uint32_t h1 = same ? sel4(qv[q][p], eb & 3) : xv[q][p];
+            const __half2 a = *reinterpret_cast<const __half2*>(&h0);
+            const __half2 c = *reinterpret_cast<const __half2*>(&h1);
+            vx[p] = __hfma2(fx, __hsub2(c, a), a);
+        }
+        const __half2 vy0 = __hfma2(fy, __hsub2(vx[1], vx[0]), vx[0]);
+        const __half2 vy1 = __hfma2(fy, __hsub2(vx[3], vx[2]), vx[2]);
+        fq[q] = __hfma2(fz, __hsub2(vy1, vy0), vy0);
+    }
+}

@@ -31,6 +31,7 @@
 // of two, exact) and divided out before the fp32 atomics.
 #include "romap_internal.cuh"
 #include "tc_sm100.cuh"
+#include "hash_fp16.cuh"
 
 bool fused_mixed_available() { return true; }
 
@@ -335,51 +336,6 @@ __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint
             for (int k = 0; k < 4; ++k)
                 q[k] = __hmul2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), __hgt2(a[k], z));
             *reinterpret_cast<uint4*>(out + off) = *reinterpret_cast<uint4*>(q);
-        }
-    }
-}
-
-// 32-byte gather (LDG.E.256) of 8 table words, zeros when !on
-__device__ __forceinline__ void ldg_v8(const uint32_t* p, bool on, uint32_t (&w)[8]) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = 0u;
-    if (on)
-        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-                     : "l"(p));
-}
-// word k (0..7) of 8 by a 3-level select tree
-__device__ __forceinline__ uint32_t sel8(const uint32_t (&w)[8], unsigned k) {
-    const bool b0 = k & 1u, b1 = k & 2u, b2 = k & 4u;
-    const uint32_t a0 = b0 ? w[1] : w[0], a1 = b0 ? w[3] : w[2], a2 = b0 ? w[5] : w[4], a3 = b0 ? w[7] : w[6];
-    const uint32_t c0 = b1 ? a1 : a0, c1 = b1 ? a3 : a2;
-    return b2 ? c1 : c0;
-}
-
-// cell and the 8 corner entries of one level (R5), as absolute entry indices
-// (level offset `off` added): P = {res, y multiplier, z multiplier, dense};
-// dense: x + (N+1) y + (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^
-// z * 805459861) & (T - 1).  Corner b: bit k -> +1 on axis k.
-__device__ __forceinline__ void level_entries(const float u[3], const int4 P, unsigned off, unsigned hmask, Cell& cl,
-                                              unsigned (&e)[8]) {
-    cl = grid_cell(u, P.x);
-    const unsigned my = (unsigned)P.y, mz = (unsigned)P.z;
-    const unsigned x0 = (unsigned)cl.c[0], x1 = x0 + 1u;
-    const unsigned ty0 = (unsigned)cl.c[1] * my, ty1 = ty0 + my;
-    const unsigned tz0 = (unsigned)cl.c[2] * mz, tz1 = tz0 + mz;
-    if (P.w) {
-        const unsigned yz[4] = {ty0 + tz0 + off, ty1 + tz0 + off, ty0 + tz1 + off, ty1 + tz1 + off};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            e[2 * k] = x0 + yz[k];
-            e[2 * k + 1] = x1 + yz[k];
-        }
-    } else {
-        const unsigned yz[4] = {ty0 ^ tz0, ty1 ^ tz0, ty0 ^ tz1, ty1 ^ tz1};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            e[2 * k] = ((x0 ^ yz[k]) & hmask) + off;
-            e[2 * k + 1] = ((x1 ^ yz[k]) & hmask) + off;
         }
     }
 }
@@ -981,10 +937,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     }
     if (t < 4) misc->loss[t] = 0.f;
     if (t < L) {
-        const int res = cfg.res[t];
-        const bool dense = cfg.dense[t] != 0;
-        const unsigned n1 = (unsigned)res + 1u;
-        misc->lv[t] = make_int4(res, (int)(dense ? n1 : 2654435761u), (int)(dense ? n1 * n1 : 805459861u), dense ? 1 : 0);
+        misc->lv[t] = level_params(cfg, t);
         misc->lvoff[t] = cfg.off[t];
     }
     tc::fence_before();

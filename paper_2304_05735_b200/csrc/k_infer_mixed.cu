@@ -1,0 +1,144 @@
+// k_infer_mixed.cu -- mixed-precision inference of SURVEY.md 8(a) a10 (density
+// query for marching cubes; BASELINE cfg4 "fp16 MLP") for
+// objects created with precision = 1: the same fp16 tables / weights and the
+// same arithmetic as the forward half of the training kernel.
+//
+// k_query_mixed: persistent CTAs of 128 threads, tiles of 128 points.  Thread t
+// encodes point t of the tile (all L levels, fp16 gathers + packed lerps) into
+// the fp16 operand X0 (shared memory), one thread issues the first density
+// layer H = X0 . W1^T on the tensor cores (tcgen05.mma, D in TMEM), and every
+// thread finishes its row: h = fp16(relu(H)), raw0 = sum_j h_j W2[0][j] (only
+// the density output is needed), sigma = act(raw0), 0 outside the box (R21).
+#include "romap_internal.cuh"
+#include "tc_sm100.cuh"
+#include "hash_fp16.cuh"
+
+namespace {
+
+constexpr int QT = 128;
+constexpr int Q_OFF_W1 = 0;                   // 64 x LF fp16 (interleaved)
+constexpr int Q_OFF_X0 = 64 * 32 * 2;         // 128 x LF fp16 (interleaved)
+constexpr int Q_OFF_MISC = Q_OFF_X0 + QT * 32 * 2;
+
+struct QMisc {
+    uint64_t mbar;
+    uint32_t tmem;
+    int pad;
+    int4 lv[ROMAP_MAX_LEVELS];
+    int lvoff[ROMAP_MAX_LEVELS];
+    float w2[64];                              // W2 row 0 (fp16 weight as fp32)
+};
+constexpr int Q_SMEM = Q_OFF_MISC + (int)((sizeof(QMisc) + 127) / 128 * 128);
+
+}  // namespace
+
+template <int L>
+__global__ void __launch_bounds__(QT) k_query_mixed(CfgDev cfg, const ObjDev* __restrict__ obj,
+                                                    const float* __restrict__ xyz, long long n,
+                                                    float* __restrict__ out) {
+    constexpr int LF = 2 * L;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    QMisc* misc = reinterpret_cast<QMisc*>(smem + Q_OFF_MISC);
+    const int t = threadIdx.x, warp = t >> 5;
+    const ObjDev& ob = *obj;
+    if (warp == 0) tc::tmem_alloc(&misc->tmem, 64);
+    if (t == 32) {
+        tc::mbar_init(&misc->mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (t < L) {
+        misc->lv[t] = level_params(cfg, t);
+        misc->lvoff[t] = cfg.off[t];
+    }
+    const __half* mlp16 = ob.p16 + cfg.n_table;
+    if (t < 64) misc->w2[t] = __half2float(mlp16[cfg.w_off[1] + t]);
+    for (int q = t; q < 64 * (LF / 8); q += QT) {
+        const int r = q / (LF / 8), cb = q % (LF / 8);
+        const __half2* s2 = reinterpret_cast<const __half2*>(mlp16 + cfg.w_off[0] + r * LF + cb * 8);
+        __half2 h[4] = {s2[0], s2[1], s2[2], s2[3]};
+        *reinterpret_cast<uint4*>(smem + Q_OFF_W1 + tc::il_offset(r, cb * 8, LF)) = *reinterpret_cast<uint4*>(h);
+    }
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tm = misc->tmem;
+    const uint32_t wk = tc::taddr(tm, warp * 32, 0);
+    const uint32_t sW1 = tc::smem_u32(smem + Q_OFF_W1), sX0 = tc::smem_u32(smem + Q_OFF_X0);
+    uint8_t* X0 = smem + Q_OFF_X0;
+    const uint32_t* tab = reinterpret_cast<const uint32_t*>(ob.p16);
+    const unsigned hmask = (unsigned)cfg.T - 1u;
+    uint32_t phase = 0;
+    for (long long tile = blockIdx.x; tile * QT < n; tile += gridDim.x) {
+        const long long p = tile * QT + t;
+        const bool valid = p < n;
+        float u[3];
+        bool inside = valid;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float x = valid ? xyz[3 * p + k] : 0.f;
+            inside &= fabsf(x) <= ob.a[k];
+            const float v = __fdiv_rn(__fadd_rn(x, ob.a[k]), __fadd_rn(ob.a[k], ob.a[k]));   // R6
+            u[k] = fminf(fmaxf(v, 0.f), 1.f);
+        }
+#pragma unroll 1
+        for (int l = 0; l < L; l += 2) {
+            const int4 P[2] = {misc->lv[l], misc->lv[l + 1]};
+            const unsigned off[2] = {(unsigned)misc->lvoff[l], (unsigned)misc->lvoff[l + 1]};
+            __half2 fq[2];
+            encode_pair_fp16(tab, u, P, off, hmask, inside, fq);
+            *reinterpret_cast<uint2*>(X0 + tc::il_offset(t, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (t == 0) {
+#pragma unroll
+            for (int ks = 0; ks < LF / 16; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sX0, LF, ks), tc::desc_kmajor(sW1, LF, ks),
+                            tc::idesc_f16(128, 64, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        tc::mbar_wait(&misc->mbar, phase);
+        phase ^= 1;
+        tc::fence_after();
+        float raw0 = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float v[32];
+            tc::tmem_ld32_sync(wk + 32 * h, v);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                // the training forward stores h = fp16(relu(H)) as the next operand
+                const float hk = __half2float(__float2half_rn(fmaxf(v[k], 0.f)));
+                raw0 += hk * misc->w2[32 * h + k];
+            }
+        }
+        if (valid) out[p] = inside ? density_act(raw0, cfg.density_act) : 0.f;
+        // X0 and the accumulator are rewritten by the next tile
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (warp == 0) tc::tmem_dealloc(tm, 64);
+}
+
+void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz,
+                                long long n, float* sigma) {
+    if (n == 0) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_query_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
+        cudaFuncSetAttribute(k_query_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
+        attr = true;
+    }
+    const long long tiles = (n + QT - 1) / QT;
+    // 8 CTAs per SM (64 TMEM columns each = the whole TMEM), persistent over tiles
+    long long grid = (long long)lc.num_sms * 8;
+    if (grid > tiles) grid = tiles;
+    if (cfg.L == 16)
+        k_query_mixed<16><<<(unsigned)grid, QT, Q_SMEM, lc.st>>>(cfg, obj, xyz, n, sigma);
+    else
+        k_query_mixed<8><<<(unsigned)grid, QT, Q_SMEM, lc.st>>>(cfg, obj, xyz, n, sigma);
+}

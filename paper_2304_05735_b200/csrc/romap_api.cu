@@ -22,6 +22,8 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
                         const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
                         float* dbg_ray_grads);
 bool fused_mixed_available();
+void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz,
+                                long long n, float* sigma);
 
 static thread_local std::string g_err;
 
@@ -945,8 +947,15 @@ romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, 
     ObjDev od = make_objdev(ob);
     CK(cudaMemcpyAsync(ctx->single_d, &od, sizeof od, cudaMemcpyHostToDevice, ctx->st));
     LaunchCtx lc{ctx->st, ctx->num_sms};
+    // precision 1 objects: fp16 tables / MLP on the tensor cores (k_infer_mixed.cu)
+    auto launch = [&](const float* x, long long m, float* o) {
+        if (ob->cfg.precision == 1)
+            launch_query_density_mixed(lc, ob->cdev, ctx->single_d, x, m, o);
+        else
+            launch_query_density(lc, ob->cdev, ctx->single_d, x, m, o);
+    };
     if (flags & ROMAP_DEVICE_PTRS) {
-        launch_query_density(lc, ob->cdev, ctx->single_d, xyz, n, sigma);
+        launch(xyz, n, sigma);
         CK(cudaGetLastError());
         return ROMAP_OK;
     }
@@ -955,7 +964,7 @@ romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, 
     for (long long p0 = 0; p0 < n; p0 += chunk) {
         long long m = n - p0 < chunk ? n - p0 : chunk;
         CK(cudaMemcpyAsync(ctx->io_d, xyz + 3 * p0, m * 12, cudaMemcpyHostToDevice, ctx->st));
-        launch_query_density(lc, ob->cdev, ctx->single_d, ctx->io_d, m, ctx->io_d + 3 * chunk);
+        launch(ctx->io_d, m, ctx->io_d + 3 * chunk);
         CK(cudaMemcpyAsync(sigma + p0, ctx->io_d + 3 * chunk, m * 4, cudaMemcpyDeviceToHost, ctx->st));
     }
     CK(cudaGetLastError());

@@ -104,3 +104,39 @@ def test_mixed_multi_object_and_training(ctx):
 def test_mixed_rejects_bad_levels(ctx):
     with pytest.raises(R.RomapError):
         ctx.create_object([0, 0, 0], 0.0, [1, 1, 1], R.model_config(precision=1, levels=6), 1)
+
+
+def _check_query(ctx, h, st, pts, rtol=2e-2):
+    s = ctx.query_density(h, pts)
+    so = O.query_density(st.cfg, st.box_a, st.params, pts)
+    # the inside / outside decision is bit-exact (same fp32 test as the oracle, R21)
+    assert np.array_equal(s == 0, so == 0)
+    inside = so != 0
+    # fp16 tables / weights / activations: sigma = exp(raw0) within 2e-2 relative
+    # (the mixed path's tolerance, BASELINE north_star; |d raw0| ~ 1e-3 here)
+    rel = np.abs(s[inside] / so[inside] - 1.0)
+    assert rel.max() < rtol, rel.max()
+    return rel
+
+
+def test_mixed_query_density_cfg0(ctx):
+    sc = scenes.sphere_scene(0)
+    h, st = make_pair(R, ctx, sc, CFG0M, avoid_kinks=False)
+    g = np.random.default_rng(11)
+    pts = g.uniform(-0.6, 0.6, (20000, 3)).astype(np.float32)
+    pts[:6] = [[0.5, 0.5, 0.5], [-0.5, -0.5, -0.5], [0.50001, 0, 0], [0, 0, 0], [0.25, -0.25, 0.125], [0.6, 0, 0]]
+    _check_query(ctx, h, st, pts)
+    assert ctx.query_density(h, np.zeros((0, 3), np.float32)).shape == (0,)
+    ctx.destroy_object(h)
+
+
+def test_mixed_query_density_cfg1_lattice(ctx):
+    # marching-cubes input: a vertex lattice spanning [-a, a] (R21),
+    # 23 points per axis (ragged last tile), cfg1 grid with dense + hashed levels
+    sc = scenes.object_scene(1, n_views=2, W=160, H=120, f=131.25)
+    h, st = make_pair(R, ctx, sc, CFG1M, avoid_kinks=False)
+    a = np.asarray(st.box_a, np.float64)
+    axes = [np.linspace(-a[k], a[k], 23) for k in range(3)]
+    P = np.stack(np.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3).astype(np.float32)
+    _check_query(ctx, h, st, P)
+    ctx.destroy_object(h)
