@@ -114,13 +114,32 @@ __global__ void __launch_bounds__(128) k_raygen_samples(CfgDev cfg, const ObjDev
     const long long S = (long long)total_slots * N;
     const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int g = (int)(s / N);
-    if (g >= total_slots) return;
+    const bool in = g < total_slots;          // (always true for the mixed path: S % 128 == 0)
     const int i = (int)(s - (long long)g * N);
+    // one lane per ray segment of the warp builds the record, the others receive
+    // the fields the samples need by shuffle (rays never straddle a warp segment:
+    // segments of min(N, 32) lanes are aligned)
+    const int lane = threadIdx.x & 31, seg = N < 32 ? N : 32, src = lane & ~(seg - 1);
     RayRec rr;
-    bool active;
-    int lo = make_ray_rec(cfg, objs, n_objs, g, k, rr, active);
-    if (i == 0) rays[(long long)k * total_slots + g] = rr;
+    bool active = false;
+    int lo = 0;
+    if (lane == src && in) {
+        lo = make_ray_rec(cfg, objs, n_objs, g, k, rr, active);
+        if (i == 0) rays[(long long)k * total_slots + g] = rr;
+    }
+    __syncwarp();
+    const unsigned full = 0xffffffffu;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        rr.o[c] = __shfl_sync(full, rr.o[c], src);
+        rr.d[c] = __shfl_sync(full, rr.d[c], src);
+    }
+    rr.tn = __shfl_sync(full, rr.tn, src);
+    rr.tf = __shfl_sync(full, rr.tf, src);
+    active = __shfl_sync(full, active ? 1 : 0, src) != 0;
+    lo = __shfl_sync(full, lo, src);
     count_hit(hit_count, lo, active && i == 0);
+    if (!in) return;
     float4 o = make_float4(-1.f, -1.f, -1.f, 0.f);
     float delta = 0.f;
     if (active) {
