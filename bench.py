@@ -203,7 +203,7 @@ def measure_inference(ctx, h, ob, frame, torch):
                               "points": int(P.shape[0]), "what": "128^3 vertex lattice of the trained object, "
                               "device buffers, CUDA events (mixed path: fp16 tables + tcgen05 first layer)"},
             "render": {"rays_per_s": 640 * 480 / r_s, "ms_per_frame": r_s * 1e3, "samples_per_ray": 128,
-                       "what": "one 640x480 frame, host outputs, wall clock (fp32 SIMT forward)"}}
+                       "what": "one 640x480 frame, host outputs, wall clock (mixed path: tensor-core forward of midpoint samples + compositing)"}}
 
 
 # ----------------------------------------------------------------------------- CPU oracle

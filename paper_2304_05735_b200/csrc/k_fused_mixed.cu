@@ -294,30 +294,6 @@ __device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* 
     tc::fence_after();
 }
 
-// store 16 consecutive fp32 values (columns c0..c0+15 of row r) as fp16
-__device__ __forceinline__ void st16(uint8_t* buf, int r, int c0, int C, const float* v) {
-    tc::st_chunk(buf, r, c0, C, v);
-    tc::st_chunk(buf, r, c0 + 8, C, v + 8);
-}
-
-// forward epilogue of a 64-wide layer (M thread, row r): TMEM -> fp16 ->
-// ReLU on packed halves (relu(round(v)) = round(relu(v))) -> smem
-__device__ __forceinline__ void epi_relu64(uint32_t wk, uint8_t* buf, int r) {
-    const __half2 z = __float2half2_rn(0.f);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        float v[32];
-        tc::tmem_ld32_sync(wk + 32 * h, v);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            __half2 q[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) q[k] = __hmax2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), z);
-            *reinterpret_cast<uint4*>(buf + tc::il_offset(r, 32 * h + 8 * c, 64)) = *reinterpret_cast<uint4*>(q);
-        }
-    }
-}
-
 // backward epilogue: dX (TMEM) masked by the ReLU derivative of the forward
 // activation `act` (its fp16 ReLU output in smem: relu' = act > 0) -> fp16 -> smem
 __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint8_t* act, int r) {
@@ -659,7 +635,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         {
             float sh[16];
             sh4(rr.d, sh);
-            st16(CIN, m, 16, 32, sh);
+            tc::st16(CIN, m, 16, 32, sh);
         }
         FP_MARK(m_t1);
         tc::mbar_wait(&misc->x0_full[b], (j >> 1) & 1);
@@ -686,7 +662,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi_relu64(wk, H1, m);
+        tc::epi_relu64(wk, H1, m);
         m_sync_for_mma();
         // L2: WK[128 x 16] = H1 . W2^T
         if (leader) {
@@ -703,7 +679,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::tmem_ld16_sync(wk, v);
             r0 = v[0];
             sigma = density_act(r0, cfg.density_act);
-            st16(CIN, m, 0, 32, v);
+            tc::st16(CIN, m, 0, 32, v);
         }
         m_sync_for_mma();
         // L3: WK = CIN . W3^T
@@ -715,7 +691,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi_relu64(wk, G1, m);
+        tc::epi_relu64(wk, G1, m);
         m_sync_for_mma();
         // L4: WK = G1 . W4^T
         if (leader) {
@@ -726,7 +702,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi_relu64(wk, G2, m);
+        tc::epi_relu64(wk, G2, m);
         m_sync_for_mma();
         // L5: WK[128 x 16] = G2 . W5^T (rows 3..15 of W5 are zero)
         if (leader) {
@@ -813,7 +789,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             for (int k = 0; k < 16; ++k) v[k] = 0.f;
 #pragma unroll
             for (int k = 0; k < 3; ++k) v[k] = dcol[k] * c[k] * (1.f - c[k]) * scale;
-            st16(DC, m, 0, 16, v);
+            tc::st16(DC, m, 0, 16, v);
         }
         const float dr0_extra = dsig * density_act_grad(r0, sigma, cfg.density_act) * scale;
         m_sync_for_mma();
@@ -865,7 +841,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             if (!active)
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
-            st16(DR, m, 0, 16, v);
+            tc::st16(DR, m, 0, 16, v);
         }
         m_sync_for_mma();
         // B2: WK[128 x 64] = DR[128 x 16] . W2[16 x 64];  dW2^T[64 x 16] += H1^T . DR

@@ -142,3 +142,219 @@ void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const Ob
     else
         k_query_mixed<8><<<(unsigned)grid, QT, Q_SMEM, lc.st>>>(cfg, obj, xyz, n, sigma);
 }
+
+// ---------------------------------------------------------------------------
+// a11 render, mixed path: the forward half of the training step on the tensor
+// cores for midpoint samples (R12), one sample per thread, tiles of 128 samples
+// (whole rays of the object).  Writes sigma, rgb, dist, delta per sample in the
+// layout k_composite consumes (inactive rays: sigma = 0, rgb = 0), so the
+// compositing (front to back over black, R20) is shared with the fp32 path.
+namespace {
+constexpr int F_OFF_W1 = 0;                     // 64 x LF
+constexpr int F_OFF_W2 = F_OFF_W1 + 64 * 32 * 2;
+constexpr int F_OFF_W3 = F_OFF_W2 + 16 * 64 * 2;
+constexpr int F_OFF_W4 = F_OFF_W3 + 64 * 32 * 2;
+constexpr int F_OFF_W5 = F_OFF_W4 + 64 * 64 * 2;
+constexpr int F_OFF_X0 = F_OFF_W5 + 16 * 64 * 2;
+constexpr int F_OFF_H1 = F_OFF_X0 + QT * 32 * 2;
+constexpr int F_OFF_CIN = F_OFF_H1 + QT * 64 * 2;
+constexpr int F_OFF_G1 = F_OFF_CIN + QT * 32 * 2;
+constexpr int F_OFF_G2 = F_OFF_G1 + QT * 64 * 2;
+constexpr int F_OFF_MISC = F_OFF_G2 + QT * 64 * 2;
+constexpr int F_SMEM = F_OFF_MISC + (int)((sizeof(QMisc) + 127) / 128 * 128);
+
+__device__ __forceinline__ void f_sync_for_mma() {
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+}
+}  // namespace
+
+template <int L>
+__global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __restrict__ obj,
+                                                  const RayRec* __restrict__ rays, int n_rays,
+                                                  float* __restrict__ sigma_o, float* __restrict__ rgb_o,
+                                                  float* __restrict__ dist_o, float* __restrict__ delta_o) {
+    constexpr int LF = 2 * L;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    QMisc* misc = reinterpret_cast<QMisc*>(smem + F_OFF_MISC);
+    const int t = threadIdx.x, warp = t >> 5;
+    const ObjDev& ob = *obj;
+    const int N = cfg.N;
+    if (warp == 0) tc::tmem_alloc(&misc->tmem, 64);
+    if (t == 32) {
+        tc::mbar_init(&misc->mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (t < L) {
+        misc->lv[t] = level_params(cfg, t);
+        misc->lvoff[t] = cfg.off[t];
+    }
+    {   // fp16 weights -> interleaved operand layout (W5: rows 3..15 zero)
+        const __half* mlp16 = ob.p16 + cfg.n_table;
+        struct Lw { int off, rows, cols, srows, smem; };
+        const Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, F_OFF_W1}, {cfg.w_off[1], 16, 64, 16, F_OFF_W2},
+                          {cfg.w_off[2], 64, 32, 64, F_OFF_W3}, {cfg.w_off[3], 64, 64, 64, F_OFF_W4},
+                          {cfg.w_off[4], 3, 64, 16, F_OFF_W5}};
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const int chunks = ls[k].srows * (ls[k].cols / 8);
+            for (int q = t; q < chunks; q += QT) {
+                const int r = q / (ls[k].cols / 8), cb = q % (ls[k].cols / 8);
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (r < ls[k].rows) {
+                    const __half2* s2 =
+                        reinterpret_cast<const __half2*>(mlp16 + ls[k].off + r * ls[k].cols + cb * 8);
+                    __half2 h[4] = {s2[0], s2[1], s2[2], s2[3]};
+                    v = *reinterpret_cast<uint4*>(h);
+                }
+                *reinterpret_cast<uint4*>(smem + ls[k].smem + tc::il_offset(r, cb * 8, ls[k].cols)) = v;
+            }
+        }
+    }
+    f_sync_for_mma();
+    const uint32_t tm = misc->tmem;
+    const uint32_t wk = tc::taddr(tm, warp * 32, 0);
+    const uint32_t sW1 = tc::smem_u32(smem + F_OFF_W1), sW2 = tc::smem_u32(smem + F_OFF_W2),
+                   sW3 = tc::smem_u32(smem + F_OFF_W3), sW4 = tc::smem_u32(smem + F_OFF_W4),
+                   sW5 = tc::smem_u32(smem + F_OFF_W5), sX0 = tc::smem_u32(smem + F_OFF_X0),
+                   sH1 = tc::smem_u32(smem + F_OFF_H1), sCIN = tc::smem_u32(smem + F_OFF_CIN),
+                   sG1 = tc::smem_u32(smem + F_OFF_G1), sG2 = tc::smem_u32(smem + F_OFF_G2);
+    uint8_t* X0 = smem + F_OFF_X0;
+    uint8_t* H1 = smem + F_OFF_H1;
+    uint8_t* CIN = smem + F_OFF_CIN;
+    uint8_t* G1 = smem + F_OFF_G1;
+    uint8_t* G2 = smem + F_OFF_G2;
+    const uint32_t* tab = reinterpret_cast<const uint32_t*>(ob.p16);
+    const unsigned hmask = (unsigned)cfg.T - 1u;
+    uint32_t phase = 0;
+    auto mma_wait = [&]() {
+        tc::mbar_wait(&misc->mbar, phase);
+        phase ^= 1;
+        tc::fence_after();
+    };
+    const long long S = (long long)n_rays * N;
+    for (long long tile = blockIdx.x; tile * QT < S; tile += gridDim.x) {
+        const long long s = tile * QT + t;
+        const bool valid = s < S;
+        const long long ray = valid ? s / N : 0;
+        const int i = valid ? (int)(s - ray * N) : 0;
+        const RayRec rr = rays[ray];
+        const bool active = valid && (rr.flags & RF_ACTIVE);
+        // R12 inference samples: midpoints, delta = Delta (bit-exact with k_fwd_fp32)
+        float dist = 0.f, delta = 0.f, u[3] = {0.f, 0.f, 0.f};
+        if (active) {
+            const float Dl = __fdiv_rn(__fsub_rn(rr.tf, rr.tn), (float)N);
+            dist = sample_dist(rr.tn, Dl, i, 0.5f);
+            delta = Dl;
+            sample_u(rr.o, rr.d, ob.a, dist, u);
+        }
+#pragma unroll 1
+        for (int l = 0; l < L; l += 2) {
+            const int4 P[2] = {misc->lv[l], misc->lv[l + 1]};
+            const unsigned off[2] = {(unsigned)misc->lvoff[l], (unsigned)misc->lvoff[l + 1]};
+            __half2 fq[2];
+            encode_pair_fp16(tab, u, P, off, hmask, active, fq);
+            *reinterpret_cast<uint2*>(X0 + tc::il_offset(t, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
+        }
+        {
+            float sh[16];
+            sh4(rr.d, sh);
+            tc::st16(CIN, t, 16, 32, sh);
+        }
+        f_sync_for_mma();
+        if (t == 0) {
+#pragma unroll
+            for (int ks = 0; ks < LF / 16; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sX0, LF, ks), tc::desc_kmajor(sW1, LF, ks),
+                            tc::idesc_f16(128, 64, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        mma_wait();
+        tc::epi_relu64(wk, H1, t);
+        f_sync_for_mma();
+        if (t == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sH1, 64, ks), tc::desc_kmajor(sW2, 64, ks),
+                            tc::idesc_f16(128, 16, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        mma_wait();
+        float sigma;
+        {
+            float v[16];
+            tc::tmem_ld16_sync(wk, v);
+            sigma = density_act(v[0], cfg.density_act);
+            tc::st16(CIN, t, 0, 32, v);
+        }
+        f_sync_for_mma();
+        if (t == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sCIN, 32, ks), tc::desc_kmajor(sW3, 32, ks),
+                            tc::idesc_f16(128, 64, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        mma_wait();
+        tc::epi_relu64(wk, G1, t);
+        f_sync_for_mma();
+        if (t == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sG1, 64, ks), tc::desc_kmajor(sW4, 64, ks),
+                            tc::idesc_f16(128, 64, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        mma_wait();
+        tc::epi_relu64(wk, G2, t);
+        f_sync_for_mma();
+        if (t == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sG2, 64, ks), tc::desc_kmajor(sW5, 64, ks),
+                            tc::idesc_f16(128, 16, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        mma_wait();
+        float c[3];
+        {
+            float v[16];
+            tc::tmem_ld16_sync(wk, v);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[k]));
+        }
+        if (valid) {
+            sigma_o[s] = active ? sigma : 0.f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) rgb_o[3 * s + k] = active ? c[k] : 0.f;
+            dist_o[s] = dist;
+            delta_o[s] = delta;
+        }
+        // the next tile rewrites X0 / CIN and the accumulator
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (warp == 0) tc::tmem_dealloc(tm, 64);
+}
+
+void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const RayRec* rays, int n_rays,
+                      float* sigma, float* rgb, float* dist, float* delta) {
+    const long long S = (long long)n_rays * cfg.N;
+    if (S == 0) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fwd_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+        cudaFuncSetAttribute(k_fwd_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+        attr = true;
+    }
+    const long long tiles = (S + QT - 1) / QT;
+    long long grid = (long long)lc.num_sms * 2;
+    if (grid > tiles) grid = tiles;
+    if (cfg.L == 16)
+        k_fwd_mixed<16><<<(unsigned)grid, QT, F_SMEM, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
+    else
+        k_fwd_mixed<8><<<(unsigned)grid, QT, F_SMEM, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
+}

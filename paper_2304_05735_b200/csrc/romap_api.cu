@@ -22,6 +22,8 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
                         const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
                         float* dbg_ray_grads);
 bool fused_mixed_available();
+void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const RayRec* rays, int n_rays,
+                      float* sigma, float* rgb, float* dist, float* delta);
 void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz,
                                 long long n, float* sigma);
 
@@ -866,7 +868,10 @@ static romap_status render_one(romap_ctx* ctx, Object* ob, const float T_wc[12],
     for (long long r0 = 0; r0 < HW; r0 += chunk) {
         int nr = (int)(HW - r0 < chunk ? HW - r0 : chunk);
         // rays of this chunk all belong to slot 0 (ctx->single_d)
-        launch_fwd_fp32(lc, cfg, ctx->single_d, ctx->rays + r0, nr, false, true, sg, cl, ds, dl, nullptr, 0);
+        if (ob->cfg.precision == 1)   // mixed objects: fp16 tables / MLP on the tensor cores (k_infer_mixed.cu)
+            launch_fwd_mixed(lc, cfg, ctx->single_d, ctx->rays + r0, nr, sg, cl, ds, dl);
+        else
+            launch_fwd_fp32(lc, cfg, ctx->single_d, ctx->rays + r0, nr, false, true, sg, cl, ds, dl, nullptr, 0);
         launch_composite(lc, N, ctx->rays + r0, nr, sg, cl, ds, dl, o_rgb ? o_rgb + 3 * r0 : nullptr,
                          o_dep ? o_dep + r0 : nullptr, o_opa ? o_opa + r0 : nullptr);
     }

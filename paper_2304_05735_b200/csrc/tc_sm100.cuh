@@ -175,4 +175,29 @@ __device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, int C, cons
     *reinterpret_cast<uint4*>(buf + il_offset(r, c, C)) = *reinterpret_cast<uint4*>(h);
 }
 
+
+// store 16 consecutive fp32 values (columns c0..c0+15 of row r) as fp16
+__device__ __forceinline__ void st16(uint8_t* buf, int r, int c0, int C, const float* v) {
+    st_chunk(buf, r, c0, C, v);
+    st_chunk(buf, r, c0 + 8, C, v + 8);
+}
+
+// forward epilogue of a 64-wide layer (M thread, row r): TMEM -> fp16 ->
+// ReLU on packed halves (relu(round(v)) = round(relu(v))) -> smem
+__device__ __forceinline__ void epi_relu64(uint32_t wk, uint8_t* buf, int r) {
+    const __half2 z = __float2half2_rn(0.f);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        float v[32];
+        tmem_ld32_sync(wk + 32 * h, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            __half2 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = __hmax2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), z);
+            *reinterpret_cast<uint4*>(buf + il_offset(r, 32 * h + 8 * c, 64)) = *reinterpret_cast<uint4*>(q);
+        }
+    }
+}
+
 }  // namespace tc

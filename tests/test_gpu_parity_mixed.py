@@ -140,3 +140,18 @@ def test_mixed_query_density_cfg1_lattice(ctx):
     P = np.stack(np.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3).astype(np.float32)
     _check_query(ctx, h, st, P)
     ctx.destroy_object(h)
+
+
+def test_mixed_render_cfg0(ctx):
+    # a11 on the mixed path (tensor-core forward of midpoint samples, shared
+    # compositing): colour / opacity within the fp16 tolerance of the oracle (fp64)
+    sc = scenes.sphere_scene(0)
+    h, st = make_pair(R, ctx, sc, CFG0M, avoid_kinks=False)
+    fr = sc.frames[0]
+    rgb, dep, opa = ctx.render(h, fr.T_wc, fr.K, 64, 64, 32)
+    orgb, odep, oopa = O.render(st.cfg, st.box_t, st.box_yaw, st.box_a, st.params, fr.T_wc, fr.K, 64, 64, 32)
+    assert np.array_equal(opa == 0, oopa == 0)          # same hit rays (bit-exact geometry)
+    assert np.abs(rgb - orgb).max() < 2e-2
+    assert np.abs(opa - oopa).max() < 2e-2
+    assert (oopa > 0.1).sum() > 100
+    ctx.destroy_object(h)
