@@ -25,7 +25,9 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
                     trilinear weights = 1, dense-level bijection, continuity
                     (SPEC.md:278), brute-force XOR-hash on python ints
   sh4               quadrature orthonormality + addition theorem
-  mlp_forward       zero model (SPEC.md:253 adapted to R4), selection weights
+  mlp_forward       zero model (SPEC.md:253 adapted to R4), selection weights;
+                    network 1 (R24): shapes for 1..3 hidden layers, zero model,
+                    selection weights, whole-step central differences
   volume_render     sigma=0, opaque first sample, ln2 case,
                     constant-density closed form 1-exp(-sigma L) (north_star)
   losses            (0.3,0,0.4)->0.5, decomposition identity,
@@ -79,6 +81,8 @@ class ModelConfig:
     lambda_density: float = 0.01  # PAPER.md:222 lambda_2
     obj_bg: int = 0               # R14: 0 random bg for all supervised rays, 1 black for R_o
     seed: int = 0
+    network: int = 0              # R24: 0 BASELINE density + SH colour nets, 1 the paper's position-only MLP
+    hidden_layers: int = 1        # network 1: hidden layers of width `width` (Table 4: 1..3)
 
 
 @dataclass
@@ -119,8 +123,12 @@ def table_entries(cfg: ModelConfig) -> int:
 
 def mlp_shapes(cfg: ModelConfig) -> list[tuple[int, int]]:
     """(out, in) of each bias-free layer (R1, R4): density LF->W->16; colour
-    [16 raw || dir_enc]->W->...->W->3 (color_hidden hidden layers)."""
+    [16 raw || dir_enc]->W->...->W->3 (color_hidden hidden layers).
+    network 1 (R24, "multi-resolution hash encoding and a
+    single-layer MLP", positions only -> sigma and c): LF->W (->W ...)->4."""
     lf = cfg.levels * cfg.feats
+    if cfg.network == 1:
+        return [(cfg.width, lf)] + [(cfg.width, cfg.width)] * (cfg.hidden_layers - 1) + [(4, cfg.width)]
     shapes = [(cfg.width, lf), (cfg.density_out, cfg.width), (cfg.width, cfg.density_out + cfg.dir_enc)]
     shapes += [(cfg.width, cfg.width)] * (cfg.color_hidden - 1)
     shapes.append((3, cfg.width))
@@ -444,9 +452,25 @@ def relu(x):
     return np.maximum(x, 0.0)
 
 
+def mlp_forward_paper(feat, W, cfg: ModelConfig):
+    """network 1 (R24): h_1 = ReLU(W_1 feat), h_k = ReLU(W_k h_{k-1}), raw = W_out h_L;
+    sigma = act(raw_0) (R3), c = sigmoid(raw_1..3).  No view direction
+    (PAPER.md:155).  fp64."""
+    hs = [relu(feat @ W[0].T)]
+    for k in range(1, cfg.hidden_layers):
+        hs.append(relu(hs[-1] @ W[k].T))
+    raw = hs[-1] @ W[-1].T
+    sigma = density_activation(raw[:, 0], cfg.density_act)
+    c = 1.0 / (1.0 + np.exp(-raw[:, 1:4]))
+    return {"feat": feat, "h": hs, "raw": raw, "r": raw, "sigma": sigma, "rgb": c}
+
+
 def mlp_forward(feat, sh, W, cfg: ModelConfig):
     """h = ReLU(W1 feat); r = W2 h; sigma = act(r0); g = ReLU(W3 [r||sh]);
-    g_k = ReLU(W g_{k-1}) ...; c = sigmoid(W_last g).  fp64.  sh may be (S,0)."""
+    g_k = ReLU(W g_{k-1}) ...; c = sigmoid(W_last g).  fp64.  sh may be (S,0).
+    network 1: mlp_forward_paper (sh unused)."""
+    if cfg.network == 1:
+        return mlp_forward_paper(feat, W, cfg)
     h1 = relu(feat @ W[0].T)
     r = h1 @ W[1].T
     sigma = density_activation(r[:, 0], cfg.density_act)
@@ -460,7 +484,9 @@ def mlp_forward(feat, sh, W, cfg: ModelConfig):
 
 
 def mlp_forward_density(feat, W, cfg: ModelConfig):
-    """Density net only (query_density, R21)."""
+    """Density net only (query_density, R21); network 1: the whole MLP's sigma."""
+    if cfg.network == 1:
+        return mlp_forward_paper(feat, W, cfg)["sigma"]
     h1 = relu(feat @ W[0].T)
     r = h1 @ W[1].T
     return density_activation(r[:, 0], cfg.density_act)
@@ -468,6 +494,8 @@ def mlp_forward_density(feat, W, cfg: ModelConfig):
 
 def mlp_backward(fw, dsigma, drgb, W, cfg: ModelConfig):
     """Reverse mode through mlp_forward by hand (ReLU masks h>0, dW = delta^T x)."""
+    if cfg.network == 1:
+        return mlp_backward_paper(fw, dsigma, drgb, W, cfg)
     c = fw["rgb"]
     dcraw = drgb * c * (1.0 - c)
     dW = [None] * len(W)
@@ -485,6 +513,25 @@ def mlp_backward(fw, dsigma, drgb, W, cfg: ModelConfig):
     dh1 = (dr @ W[1]) * (fw["h1"] > 0)
     dW[0] = dh1.T @ fw["feat"]
     dfeat = dh1 @ W[0]
+    return dW, dfeat
+
+
+def mlp_backward_paper(fw, dsigma, drgb, W, cfg: ModelConfig):
+    """Reverse mode through mlp_forward_paper: draw_0 = dsigma act'(raw_0),
+    draw_1..3 = drgb c (1 - c); dW_out = draw^T h_L; dh = (draw W_out) [h > 0] ..."""
+    c = fw["rgb"]
+    hs = fw["h"]
+    draw = np.zeros_like(fw["raw"])
+    draw[:, 0] = dsigma * density_activation_grad(fw["raw"][:, 0], fw["sigma"], cfg.density_act)
+    draw[:, 1:4] = drgb * c * (1.0 - c)
+    dW = [None] * len(W)
+    dW[-1] = draw.T @ hs[-1]
+    dh = (draw @ W[-1]) * (hs[-1] > 0)
+    for k in range(cfg.hidden_layers - 1, 0, -1):
+        dW[k] = dh.T @ hs[k - 1]
+        dh = (dh @ W[k]) * (hs[k - 1] > 0)
+    dW[0] = dh.T @ fw["feat"]
+    dfeat = dh @ W[0]
     return dW, dfeat
 
 
@@ -655,7 +702,7 @@ def loss_and_grads(st: ObjectState, t: int, params=None, rays=None):
     Ra = ia.size
     u = rs["u"][ia].reshape(-1, 3)
     feat, idx, w = hash_encode(u, P["table"], cfg)
-    sh = sh4(np.repeat(rs["d"][ia], N, axis=0)) if cfg.dir_enc == 16 else np.zeros((Ra * N, 0))
+    sh = sh4(np.repeat(rs["d"][ia], N, axis=0)) if (cfg.network == 0 and cfg.dir_enc == 16) else np.zeros((Ra * N, 0))
     fw = mlp_forward(feat, sh, P["W"], cfg)
     sigma = fw["sigma"].reshape(Ra, N)
     rgb = fw["rgb"].reshape(Ra, N, 3)
@@ -700,7 +747,7 @@ def train_iteration(st: ObjectState):
 # --------------------------------------------------------------------------
 def field_eval(cfg, params, u_flat, d_rep):
     feat, _, _ = hash_encode(u_flat, params["table"], cfg)
-    sh = sh4(d_rep) if cfg.dir_enc == 16 else np.zeros((u_flat.shape[0], 0))
+    sh = sh4(d_rep) if (cfg.network == 0 and cfg.dir_enc == 16) else np.zeros((u_flat.shape[0], 0))
     fw = mlp_forward(feat, sh, params["W"], cfg)
     return fw["sigma"], fw["rgb"]
 

@@ -596,3 +596,70 @@ def test_render_scene_two_boxes_closed_form():
         sg = math.exp(0.5 if oid == 0 else 0.2)
         Ltot += np.where(hit, sg * (tf - tn).astype(np.float64), 0.0)
     assert np.allclose(opa.reshape(-1), 1 - np.exp(-Ltot), atol=1e-6)
+
+
+# ---------------------------------------------------------------- network 1 (R24, the paper's MLP)
+def test_paper_network_shapes_and_zero_model():
+    # hash encoding + single hidden layer of 64; Table 4: 1..3 layers
+    for hl in (1, 2, 3):
+        cfg = O.ModelConfig(levels=16, network=1, hidden_layers=hl, dir_enc=0)
+        sh = O.mlp_shapes(cfg)
+        assert sh[0] == (64, 32) and sh[-1] == (4, 64) and len(sh) == hl + 1
+        assert all(s == (64, 64) for s in sh[1:-1])
+    cfg = O.ModelConfig(network=1, hidden_layers=2, dir_enc=0)
+    W = [np.zeros(s) for s in O.mlp_shapes(cfg)]
+    fw = O.mlp_forward(np.random.default_rng(0).normal(size=(7, 16)), np.zeros((7, 0)), W, cfg)
+    assert np.allclose(fw["sigma"], 1.0) and np.allclose(fw["rgb"], 0.5)     # raw = 0 (R3, R4)
+
+
+def test_paper_network_selection_weights():
+    # W1 copies features 0..3 into hidden units 0..3, W2 = identity on them, W_out maps
+    # hidden unit k -> raw k: sigma = exp(relu(f0)), c_k = sigmoid(relu(f_k)) (positions only)
+    cfg = O.ModelConfig(network=1, hidden_layers=2, dir_enc=0)
+    W = [np.zeros(s) for s in O.mlp_shapes(cfg)]
+    for k in range(4):
+        W[0][k, k] = 1
+        W[1][k, k] = 1
+        W[2][k, k] = 1
+    f = np.random.default_rng(1).normal(size=(9, 16))
+    fw = O.mlp_forward(f, np.zeros((9, 0)), W, cfg)
+    r = np.maximum(f[:, :4], 0)
+    assert np.allclose(fw["sigma"], np.exp(r[:, 0]))
+    assert np.allclose(fw["rgb"], 1 / (1 + np.exp(-r[:, 1:4])))
+    # the view direction plays no role
+    st_cfg = O.ModelConfig(network=1, dir_enc=0)
+    assert O.mlp_shapes(st_cfg)[0][1] == st_cfg.levels * st_cfg.feats
+
+
+@pytest.mark.parametrize("hl", [1, 2, 3])
+def test_paper_network_step_gradient_central_differences(hl):
+    # O12 for network 1: whole-step analytic gradients vs fp64 central differences
+    cfg = O.ModelConfig(levels=2, log2_T=6, base_res=2, finest_res=4.0, res_cap=0, width=5, dir_enc=0, network=1,
+                        hidden_layers=hl, rays_per_iter=24, samples_per_ray=6, seed=hl)
+    st = _small_state(cfg, seed=hl, occluders=(hl == 2), depth=True)
+    g = np.random.default_rng(200 + hl)
+    st.params["W"] = [g.normal(0, 0.8, w.shape) for w in st.params["W"]]
+    rays = O.forward_rays(st, 1)
+    L0, grads, _ = O.loss_and_grads(st, 1, rays=rays)
+
+    def loss_at(P):
+        return O.loss_and_grads(st, 1, params=P, rays=rays)[0]["l_total"]
+    h = 1e-6
+    cand = [("table", i, j) for i in np.nonzero(np.abs(grads["table"]).sum(1) > 0)[0] for j in range(2)]
+    cand = [cand[i] for i in g.permutation(len(cand))[:10]]
+    for li, w in enumerate(st.params["W"]):
+        for _ in range(4):
+            cand.append(("W", li, tuple(int(g.integers(0, s)) for s in w.shape)))
+    for kind, a, b in cand:
+        Pp = {"table": st.params["table"].copy(), "W": [w.copy() for w in st.params["W"]]}
+        Pm = {"table": st.params["table"].copy(), "W": [w.copy() for w in st.params["W"]]}
+        if kind == "table":
+            Pp["table"][a, b] += h
+            Pm["table"][a, b] -= h
+            an = grads["table"][a, b]
+        else:
+            Pp["W"][a][b] += h
+            Pm["W"][a][b] -= h
+            an = grads["W"][a][b]
+        fd = (loss_at(Pp) - loss_at(Pm)) / (2 * h)
+        assert abs(fd - an) <= 1e-5 * max(1.0, abs(an)) + 1e-7, (kind, a, b, fd, an)
