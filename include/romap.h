@@ -77,9 +77,14 @@ typedef struct {
 } romap_depth_sample;
 
 /* Model / training configuration (BASELINE.json configs; PAPER.md:222 constants).
- * Supported on the GPU in this version: feats == 2, 1 <= levels <= 16,
- * width == 64, density_out == 16, color_hidden == 2, dir_enc == 16 (SH degree 4),
- * samples_per_ray a power of two in [1, 128], precision 0 (fp32) or 1 (mixed). */
+ * Supported on the GPU in this version: feats == 2, 1 <= levels <= 16, width == 64,
+ * samples_per_ray a power of two in [1, 128], precision 0 (fp32) or 1 (mixed), and
+ *   network 0 (BASELINE): density_out == 16, color_hidden == 2, dir_enc == 16
+ *              (SH degree 4), density net LF->64->16 + colour net [16||SH]->64->64->3;
+ *   network 1 (the paper's MLP, R24): LF -> 64
+ *              (hidden_layers x, 1..3) -> 4 (sigma, rgb), positions only; mixed
+ *              path only (precision 1), levels 8 or 16; density_out, color_hidden,
+ *              dir_enc are ignored. */
 typedef struct {
     int32_t levels;          /* L hash levels                                    */
     int32_t feats;           /* F features per level                             */
@@ -100,6 +105,8 @@ typedef struct {
     float loss_scale;        /* mixed path static loss scale (power of two)      */
     int32_t obj_bg;          /* 0: random bg colour composited for R_o too (R14) */
     uint64_t seed;           /* counter-RNG seed (R13)                           */
+    int32_t network;         /* 0 BASELINE density + SH colour nets, 1 paper (R24) */
+    int32_t hidden_layers;   /* network 1: hidden layers (Table 4: 1..3)         */
 } romap_model_config;
 
 /* Per-object statistics of one train_step call.  Loss terms are those of the

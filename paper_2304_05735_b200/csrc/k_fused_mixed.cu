@@ -78,8 +78,9 @@ constexpr int OFF_W2 = OFF_W1 + 64 * 32 * 2;   // 16 x 64
 constexpr int OFF_W3 = OFF_W2 + 16 * 64 * 2;   // 64 x 32
 constexpr int OFF_W4 = OFF_W3 + 64 * 32 * 2;   // 64 x 64
 constexpr int OFF_W5 = OFF_W4 + 64 * 64 * 2;   // 16 x 64 (rows 3..15 zero)
+constexpr int OFF_WH2 = OFF_W5 + 16 * 64 * 2;  // network 1: second 64 x 64 hidden layer
 constexpr int X0_BYTES = TILE * 32 * 2;
-constexpr int OFF_X0 = OFF_W5 + 16 * 64 * 2;   // 2 slots x 128 x LF
+constexpr int OFF_X0 = OFF_WH2 + 64 * 64 * 2;  // 2 slots x 128 x LF
 constexpr int OFF_H1 = OFF_X0 + 2 * X0_BYTES;  // 128 x 64
 constexpr int OFF_CIN = OFF_H1 + TILE * 64 * 2;
 constexpr int OFF_G1 = OFF_CIN + TILE * 32 * 2;
@@ -98,7 +99,11 @@ constexpr int TM_DW3 = 160;   // dW3   [64 x 32]
 constexpr int TM_DW4 = 192;   // dW4   [64 x 64]
 constexpr int TM_DW2 = 256;   // dW2^T [64 x 16]
 constexpr int TM_DW5 = 272;   // dW5^T [64 x 16]
+constexpr int TM_DWH2 = 320;  // network 1: dW of the second 64 x 64 hidden layer
 constexpr int TM_COLS = 512;
+// network 1 (R24) slots: W1 -> OFF_W1 / TM_DW1; hidden k = 1, 2 (64 x 64) ->
+// OFF_W4 / TM_DW4 and OFF_WH2 / TM_DWH2; W_out (4 x 64, rows 4..15 zero) ->
+// OFF_W2 / TM_DW2 (dW_out^T); activations h_1, h_2, h_3 -> H1, G1, G2
 
 struct Misc {
     uint64_t mbar_mma;        // M: completion of its own MMA groups
@@ -226,12 +231,21 @@ __device__ __forceinline__ void m_suffix2(float x0, float x1, int N, float* xw, 
 // copy one object's fp16 weights into the interleaved smem layout (M threads)
 __device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, const CfgDev& cfg, int LF) {
     struct Lw { int off, rows, cols, srows, smem; };
-    const Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, OFF_W1}, {cfg.w_off[1], 16, 64, 16, OFF_W2},
-                      {cfg.w_off[2], 64, 32, 64, OFF_W3}, {cfg.w_off[3], 64, 64, 64, OFF_W4},
-                      {cfg.w_off[4], 3, 64, 16, OFF_W5}};
+    Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, OFF_W1}, {cfg.w_off[1], 16, 64, 16, OFF_W2},
+                {cfg.w_off[2], 64, 32, 64, OFF_W3}, {cfg.w_off[3], 64, 64, 64, OFF_W4},
+                {cfg.w_off[4], 3, 64, 16, OFF_W5}};
+    int nl = 5;
+    if (cfg.net == 1) {
+        const int hl = cfg.hl;
+        ls[1] = {cfg.w_off[hl], 4, 64, 16, OFF_W2};
+        ls[2] = {cfg.w_off[1], 64, 64, 64, OFF_W4};
+        ls[3] = {cfg.w_off[2], 64, 64, 64, OFF_WH2};
+        nl = hl + 1;       // W1, W_out, then hl - 1 hidden layers
+    }
     const int m = threadIdx.x - NG;
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
+        if (k >= nl) break;
         const int chunks = ls[k].srows * (ls[k].cols / 8);
         for (int q = m; q < chunks; q += NM) {
             const int r = q / (ls[k].cols / 8), cb = q % (ls[k].cols / 8);
@@ -269,6 +283,18 @@ __device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* 
         };
 #pragma unroll
         for (int c0 = 0; c0 < LF; c0 += 16) rows4(TM_DW1 + c0, gm + cfg.w_off[0] + row * LF + c0);
+        if (cfg.net == 1) {
+            const int hl = cfg.hl;
+            for (int k = 1; k < hl; ++k)
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 16)
+                    rows4((k == 1 ? TM_DW4 : TM_DWH2) + c0, gm + cfg.w_off[k] + row * 64 + c0);
+            // dW_out^T [64 in x 16 (4) out]
+            tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, TM_DW2), v);
+            if (on)
+#pragma unroll
+                for (int o = 0; o < 4; ++o) red_add_f1(gm + cfg.w_off[hl] + o * 64 + row, v[o] * inv);
+        } else {
 #pragma unroll
         for (int c0 = 0; c0 < 32; c0 += 16) rows4(TM_DW3 + c0, gm + cfg.w_off[2] + row * 32 + c0);
 #pragma unroll
@@ -282,6 +308,7 @@ __device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* 
         if (on)
 #pragma unroll
             for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
+        }
     }
     tc::bar_sync(BAR_M, NM);
     if (m < 4) {
@@ -567,7 +594,7 @@ __device__ __forceinline__ MIn m_load(const RayRec* __restrict__ rays, const flo
 
 // ---------------------------------------------------------------------------
 // M: SH + MLP forward + render/loss + MLP backward of tile j
-template <int L>
+template <int L, int NET>
 __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
                                        const RayRec* __restrict__ rays, const float4* __restrict__ srec,
                                        const float* __restrict__ sdelta, int tile0, int tstride, int n, uint8_t* smem,
@@ -585,7 +612,8 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
                    sW5 = tc::smem_u32(smem + OFF_W5), sH1 = tc::smem_u32(smem + OFF_H1),
                    sCIN = tc::smem_u32(smem + OFF_CIN), sG1 = tc::smem_u32(smem + OFF_G1),
                    sG2 = tc::smem_u32(smem + OFF_G2), sDC = tc::smem_u32(smem + OFF_DC),
-                   sDR = tc::smem_u32(smem + OFF_DR), sDB = tc::smem_u32(smem + OFF_DB);
+                   sDR = tc::smem_u32(smem + OFF_DR), sDB = tc::smem_u32(smem + OFF_DB),
+                   sWH2 = tc::smem_u32(smem + OFF_WH2);
     uint8_t* H1 = smem + OFF_H1;
     uint8_t* CIN = smem + OFF_CIN;
     uint8_t* G1 = smem + OFF_G1;
@@ -652,6 +680,8 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         m_sync_for_mma();
         const uint32_t sX0 = tc::smem_u32(smem + OFF_X0 + b * X0_BYTES);
 
+        float sigma, r0, c[3];
+        if constexpr (NET == 0) {
         // ---- a4: MLP forward
         // L1: WK[128 x 64] = X0[128 x LF] . W1^T
         if (leader) {
@@ -673,7 +703,6 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        float sigma, r0;
         {
             float v[16];
             tc::tmem_ld16_sync(wk, v);
@@ -713,7 +742,6 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        float c[3];
         {
             float v[16];
             tc::tmem_ld16_sync(wk, v);
@@ -721,6 +749,50 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[k]));
         }
 
+        } else {
+        // ---- a4: MLP forward, network 1 (R24): h_1 = relu(X0 W1^T), h_k = relu(h_{k-1} W_k^T),
+        // raw = h_hl W_out^T (16 cols, rows 4..15 of W_out zero): sigma = act(raw_0), c = sigmoid(raw_1..3)
+        if (leader) {
+#pragma unroll
+            for (int ks = 0; ks < LF / 16; ++ks)
+                tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sX0, LF, ks), tc::desc_kmajor(sW1, LF, ks),
+                            tc::idesc_f16(128, 64, false, false), ks > 0);
+            tc::commit(&misc->mbar_mma);
+        }
+        mma_wait();
+        tc::epi_relu64(wk, H1, m);
+        m_sync_for_mma();
+        for (int k = 1; k < cfg.hl; ++k) {
+            const uint32_t sA = k == 1 ? sH1 : sG1, sW = k == 1 ? sW4 : sWH2;
+            if (leader) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sA, 64, ks), tc::desc_kmajor(sW, 64, ks),
+                                tc::idesc_f16(128, 64, false, false), ks > 0);
+                tc::commit(&misc->mbar_mma);
+            }
+            mma_wait();
+            tc::epi_relu64(wk, k == 1 ? G1 : G2, m);
+            m_sync_for_mma();
+        }
+        {
+            const uint32_t sHL = cfg.hl == 1 ? sH1 : (cfg.hl == 2 ? sG1 : sG2);
+            if (leader) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sHL, 64, ks), tc::desc_kmajor(sW2, 64, ks),
+                                tc::idesc_f16(128, 16, false, false), ks > 0);
+                tc::commit(&misc->mbar_mma);
+            }
+            mma_wait();
+            float v[16];
+            tc::tmem_ld16_sync(wk, v);
+            r0 = v[0];
+            sigma = density_act(r0, cfg.density_act);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[1 + k]));
+        }
+        }
         FP_MARK(m_t3);
         // ---- a5: volume rendering + loss + render backward
         const float dist = rr.dist;
@@ -782,6 +854,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         if (dbg) *reinterpret_cast<float4*>(dbg + 4 * s) = make_float4(dsig, dcol[0], dcol[1], dcol[2]);
         FP_MARK(m_t4);
 
+        if constexpr (NET == 0) {
         // ---- a6: MLP backward (scaled by loss_scale)
         {
             float v[16];
@@ -857,6 +930,54 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         mma_wait();
         epi_mask64(wk, DB, H1, m);
         m_sync_for_mma();
+        } else {
+        // ---- a6: MLP backward, network 1: DC = [dsigma act'(raw_0), dc c (1 - c)] x loss scale
+        {
+            float v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = 0.f;
+            v[0] = dsig * density_act_grad(r0, sigma, cfg.density_act) * scale;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) v[1 + k] = dcol[k] * c[k] * (1.f - c[k]) * scale;
+            tc::st16(DC, m, 0, 16, v);
+        }
+        m_sync_for_mma();
+        {
+            // B_out: WK[128 x 64] = DC[128 x 16] . W_out[16 x 64];  dW_out^T[64 x 16] += h_hl^T . DC
+            const uint32_t sHL = cfg.hl == 1 ? sH1 : (cfg.hl == 2 ? sG1 : sG2);
+            if (leader) {
+                tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDC, 16, 0), tc::desc_mnmajor(sW2, 64, 0),
+                            tc::idesc_f16(128, 64, false, true), 0);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma_f16(tm + TM_DW2, tc::desc_mnmajor(sHL, 64, ks), tc::desc_mnmajor(sDC, 16, ks),
+                                tc::idesc_f16(64, 16, true, true), (dw_fresh && ks == 0) ? 0 : 1);
+                tc::commit(&misc->mbar_mma);
+            }
+            mma_wait();
+            epi_mask64(wk, DB, cfg.hl == 1 ? H1 : (cfg.hl == 2 ? G1 : G2), m);
+            m_sync_for_mma();
+        }
+        for (int k = cfg.hl - 1; k >= 1; --k) {
+            // B_k: WK = DB(dh_{k+1}) . W_k;  dW_k[64 x 64] += DB^T . h_k
+            const uint32_t sW = k == 1 ? sW4 : sWH2, sHk = k == 1 ? sH1 : sG1;
+            const int tdw = k == 1 ? TM_DW4 : TM_DWH2;
+            if (leader) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW, 64, ks),
+                                tc::idesc_f16(128, 64, false, true), ks > 0);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma_f16(tm + tdw, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sHk, 64, ks),
+                                tc::idesc_f16(64, 64, true, true), (dw_fresh && ks == 0) ? 0 : 1);
+                tc::commit(&misc->mbar_mma);
+            }
+            mma_wait();
+            epi_mask64(wk, DB, k == 1 ? H1 : G1, m);
+            m_sync_for_mma();
+        }
+        }
         // B1: DF[b][128 x LF] = DB(dh1) . W1[64 x LF];  dW1[64 x LF] += DB^T . X0[b]
         // (DF[b] must have been read by G: scatter of tile j-2)
         if (leader) {
@@ -891,7 +1012,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
 
 }  // namespace
 
-template <int L>
+template <int L, int NET>
 __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev* __restrict__ objs,
                                                        const RayRec* __restrict__ rays,
                                                        const float4* __restrict__ srec,
@@ -926,7 +1047,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
         if (warp < NG / 32)
             g_loop<L>(cfg, objs, rays, srec, tile0, tstride, n, smem, misc, tm);
         else
-            m_loop<L>(cfg, objs, rays, srec, sdelta, tile0, tstride, n, smem, misc, tm, loss_acc, nonfinite, dbg);
+            m_loop<L, NET>(cfg, objs, rays, srec, sdelta, tile0, tstride, n, smem, misc, tm, loss_acc, nonfinite, dbg);
     }
     tc::fence_before();
     __syncthreads();
@@ -941,17 +1062,16 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
     if (n_tiles == 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_fused_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        cudaFuncSetAttribute(k_fused_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_fused_mixed<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_fused_mixed<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_fused_mixed<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_fused_mixed<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         attr = true;
     }
     int grid = lc.num_sms;
     if (grid > n_tiles) grid = n_tiles;
     const int per = 0;   // unused: tiles are strided over the grid
-    if (cfg.L == 16)
-        k_fused_mixed<16><<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc,
-                                                            nonfinite, dbg);
-    else
-        k_fused_mixed<8><<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc,
-                                                           nonfinite, dbg);
+    auto kern = cfg.net == 1 ? (cfg.L == 16 ? k_fused_mixed<16, 1> : k_fused_mixed<8, 1>)
+                             : (cfg.L == 16 ? k_fused_mixed<16, 0> : k_fused_mixed<8, 0>);
+    kern<<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc, nonfinite, dbg);
 }

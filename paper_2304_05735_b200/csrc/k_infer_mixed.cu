@@ -5,10 +5,11 @@
 //
 // k_query_mixed: persistent CTAs of 128 threads, tiles of 128 points.  Thread t
 // encodes point t of the tile (all L levels, fp16 gathers + packed lerps) into
-// the fp16 operand X0 (shared memory), one thread issues the first density
-// layer H = X0 . W1^T on the tensor cores (tcgen05.mma, D in TMEM), and every
-// thread finishes its row: h = fp16(relu(H)), raw0 = sum_j h_j W2[0][j] (only
-// the density output is needed), sigma = act(raw0), 0 outside the box (R21).
+// the fp16 operand X0 (shared memory), one thread issues the hidden layers
+// H = X0 . W1^T (network 1, R24: then h_k = relu(h_{k-1} W_k^T)) on the tensor
+// cores (tcgen05.mma, D in TMEM), and every thread finishes its row:
+// h = fp16(relu(H)), raw0 = sum_j h_j w_j with w the density output row (network
+// 0: W2 row 0; network 1: W_out row 0), sigma = act(raw0), 0 outside the box (R21).
 #include "romap_internal.cuh"
 #include "tc_sm100.cuh"
 #include "hash_fp16.cuh"
@@ -17,8 +18,10 @@ namespace {
 
 constexpr int QT = 128;
 constexpr int Q_OFF_W1 = 0;                   // 64 x LF fp16 (interleaved)
-constexpr int Q_OFF_X0 = 64 * 32 * 2;         // 128 x LF fp16 (interleaved)
-constexpr int Q_OFF_MISC = Q_OFF_X0 + QT * 32 * 2;
+constexpr int Q_OFF_WH = 64 * 32 * 2;         // network 1: hidden layers 2, 3 (64 x 64 each)
+constexpr int Q_OFF_X0 = Q_OFF_WH + 2 * 64 * 64 * 2;   // 128 x LF fp16 (interleaved)
+constexpr int Q_OFF_H = Q_OFF_X0 + QT * 32 * 2;         // 128 x 64 hidden activations
+constexpr int Q_OFF_MISC = Q_OFF_H + QT * 64 * 2;
 
 struct QMisc {
     uint64_t mbar;
@@ -26,7 +29,7 @@ struct QMisc {
     int pad;
     int4 lv[ROMAP_MAX_LEVELS];
     int lvoff[ROMAP_MAX_LEVELS];
-    float w2[64];                              // W2 row 0 (fp16 weight as fp32)
+    float w2[64];                              // density output row (network 0: W2 row 0, 1: W_out row 0)
 };
 constexpr int Q_SMEM = Q_OFF_MISC + (int)((sizeof(QMisc) + 127) / 128 * 128);
 
@@ -51,13 +54,23 @@ __global__ void __launch_bounds__(QT) k_query_mixed(CfgDev cfg, const ObjDev* __
         misc->lvoff[t] = cfg.off[t];
     }
     const __half* mlp16 = ob.p16 + cfg.n_table;
-    if (t < 64) misc->w2[t] = __half2float(mlp16[cfg.w_off[1] + t]);
+    const int n_hidden = cfg.net == 1 ? cfg.hl : 1;
+    const int out_layer = cfg.net == 1 ? cfg.hl : 1;
+    if (t < 64) misc->w2[t] = __half2float(mlp16[cfg.w_off[out_layer] + t]);
     for (int q = t; q < 64 * (LF / 8); q += QT) {
         const int r = q / (LF / 8), cb = q % (LF / 8);
         const __half2* s2 = reinterpret_cast<const __half2*>(mlp16 + cfg.w_off[0] + r * LF + cb * 8);
         __half2 h[4] = {s2[0], s2[1], s2[2], s2[3]};
         *reinterpret_cast<uint4*>(smem + Q_OFF_W1 + tc::il_offset(r, cb * 8, LF)) = *reinterpret_cast<uint4*>(h);
     }
+    for (int k = 1; k < n_hidden; ++k)
+        for (int q = t; q < 64 * 8; q += QT) {
+            const int r = q / 8, cb = q % 8;
+            const __half2* s2 = reinterpret_cast<const __half2*>(mlp16 + cfg.w_off[k] + r * 64 + cb * 8);
+            __half2 h[4] = {s2[0], s2[1], s2[2], s2[3]};
+            *reinterpret_cast<uint4*>(smem + Q_OFF_WH + (k - 1) * 8192 + tc::il_offset(r, cb * 8, 64)) =
+                *reinterpret_cast<uint4*>(h);
+        }
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
@@ -103,6 +116,24 @@ __global__ void __launch_bounds__(QT) k_query_mixed(CfgDev cfg, const ObjDev* __
         tc::mbar_wait(&misc->mbar, phase);
         phase ^= 1;
         tc::fence_after();
+        for (int k = 1; k < n_hidden; ++k) {       // network 1: further hidden layers
+            tc::epi_relu64(wk, smem + Q_OFF_H, t);
+            tc::fence_async_smem();
+            tc::fence_before();
+            __syncthreads();
+            tc::fence_after();
+            if (t == 0) {
+                const uint32_t sH = tc::smem_u32(smem + Q_OFF_H), sW = tc::smem_u32(smem + Q_OFF_WH + (k - 1) * 8192);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    tc::mma_f16(tm, tc::desc_kmajor(sH, 64, ks), tc::desc_kmajor(sW, 64, ks),
+                                tc::idesc_f16(128, 64, false, false), ks > 0);
+                tc::commit(&misc->mbar);
+            }
+            tc::mbar_wait(&misc->mbar, phase);
+            phase ^= 1;
+            tc::fence_after();
+        }
         float raw0 = 0.f;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -155,7 +186,8 @@ constexpr int F_OFF_W2 = F_OFF_W1 + 64 * 32 * 2;
 constexpr int F_OFF_W3 = F_OFF_W2 + 16 * 64 * 2;
 constexpr int F_OFF_W4 = F_OFF_W3 + 64 * 32 * 2;
 constexpr int F_OFF_W5 = F_OFF_W4 + 64 * 64 * 2;
-constexpr int F_OFF_X0 = F_OFF_W5 + 16 * 64 * 2;
+constexpr int F_OFF_WH2 = F_OFF_W5 + 16 * 64 * 2;   // network 1: third hidden layer (64 x 64)
+constexpr int F_OFF_X0 = F_OFF_WH2 + 64 * 64 * 2;
 constexpr int F_OFF_H1 = F_OFF_X0 + QT * 32 * 2;
 constexpr int F_OFF_CIN = F_OFF_H1 + QT * 64 * 2;
 constexpr int F_OFF_G1 = F_OFF_CIN + QT * 32 * 2;
@@ -194,11 +226,19 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
     {   // fp16 weights -> interleaved operand layout (W5: rows 3..15 zero)
         const __half* mlp16 = ob.p16 + cfg.n_table;
         struct Lw { int off, rows, cols, srows, smem; };
-        const Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, F_OFF_W1}, {cfg.w_off[1], 16, 64, 16, F_OFF_W2},
-                          {cfg.w_off[2], 64, 32, 64, F_OFF_W3}, {cfg.w_off[3], 64, 64, 64, F_OFF_W4},
-                          {cfg.w_off[4], 3, 64, 16, F_OFF_W5}};
+        Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, F_OFF_W1}, {cfg.w_off[1], 16, 64, 16, F_OFF_W2},
+                    {cfg.w_off[2], 64, 32, 64, F_OFF_W3}, {cfg.w_off[3], 64, 64, 64, F_OFF_W4},
+                    {cfg.w_off[4], 3, 64, 16, F_OFF_W5}};
+        int nl = 5;
+        if (cfg.net == 1) {       // R24: W1, W_out (W2 slot), hidden 2 (W4 slot), hidden 3 (WH2 slot)
+            ls[1] = {cfg.w_off[cfg.hl], 4, 64, 16, F_OFF_W2};
+            ls[2] = {cfg.w_off[1], 64, 64, 64, F_OFF_W4};
+            ls[3] = {cfg.w_off[2], 64, 64, 64, F_OFF_WH2};
+            nl = cfg.hl + 1;
+        }
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
+            if (k >= nl) break;
             const int chunks = ls[k].srows * (ls[k].cols / 8);
             for (int q = t; q < chunks; q += QT) {
                 const int r = q / (ls[k].cols / 8), cb = q % (ls[k].cols / 8);
@@ -220,7 +260,8 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
                    sW3 = tc::smem_u32(smem + F_OFF_W3), sW4 = tc::smem_u32(smem + F_OFF_W4),
                    sW5 = tc::smem_u32(smem + F_OFF_W5), sX0 = tc::smem_u32(smem + F_OFF_X0),
                    sH1 = tc::smem_u32(smem + F_OFF_H1), sCIN = tc::smem_u32(smem + F_OFF_CIN),
-                   sG1 = tc::smem_u32(smem + F_OFF_G1), sG2 = tc::smem_u32(smem + F_OFF_G2);
+                   sG1 = tc::smem_u32(smem + F_OFF_G1), sG2 = tc::smem_u32(smem + F_OFF_G2),
+                   sWH2 = tc::smem_u32(smem + F_OFF_WH2);
     uint8_t* X0 = smem + F_OFF_X0;
     uint8_t* H1 = smem + F_OFF_H1;
     uint8_t* CIN = smem + F_OFF_CIN;
@@ -272,6 +313,8 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
             tc::commit(&misc->mbar);
         }
         mma_wait();
+        float sigma, c[3];
+        if (cfg.net == 0) {
         tc::epi_relu64(wk, H1, t);
         f_sync_for_mma();
         if (t == 0) {
@@ -282,7 +325,6 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
             tc::commit(&misc->mbar);
         }
         mma_wait();
-        float sigma;
         {
             float v[16];
             tc::tmem_ld16_sync(wk, v);
@@ -318,12 +360,44 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
             tc::commit(&misc->mbar);
         }
         mma_wait();
-        float c[3];
         {
             float v[16];
             tc::tmem_ld16_sync(wk, v);
 #pragma unroll
             for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[k]));
+        }
+        } else {
+        tc::epi_relu64(wk, H1, t);
+        f_sync_for_mma();
+        for (int k = 1; k < cfg.hl; ++k) {          // R24 hidden layers 2, 3
+            if (t == 0) {
+                const uint32_t sA = k == 1 ? sH1 : sG1, sW = k == 1 ? sW4 : sWH2;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    tc::mma_f16(tm, tc::desc_kmajor(sA, 64, ks), tc::desc_kmajor(sW, 64, ks),
+                                tc::idesc_f16(128, 64, false, false), ks > 0);
+                tc::commit(&misc->mbar);
+            }
+            mma_wait();
+            tc::epi_relu64(wk, k == 1 ? G1 : G2, t);
+            f_sync_for_mma();
+        }
+        if (t == 0) {
+            const uint32_t sHL = cfg.hl == 1 ? sH1 : (cfg.hl == 2 ? sG1 : sG2);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                tc::mma_f16(tm, tc::desc_kmajor(sHL, 64, ks), tc::desc_kmajor(sW2, 64, ks),
+                            tc::idesc_f16(128, 16, false, false), ks > 0);
+            tc::commit(&misc->mbar);
+        }
+        mma_wait();
+        {
+            float v[16];
+            tc::tmem_ld16_sync(wk, v);
+            sigma = density_act(v[0], cfg.density_act);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) c[k] = 1.0f / (1.0f + expf(-v[1 + k]));
+        }
         }
         if (valid) {
             sigma_o[s] = active ? sigma : 0.f;

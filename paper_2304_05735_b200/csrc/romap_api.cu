@@ -212,6 +212,22 @@ static bool grow(romap_ctx* c, T*& ptr, size_t& cap, size_t need) {
     } while (0)
 
 // ---------------------------------------------------------------------------
+// (out, in) of the bias-free layers (R1, R4; network 1: R24); returns the count
+static int mlp_layer_shapes(const CfgDev& cd, int shapes[5][2]) {
+    if (cd.net == 1) {
+        int n = 0;
+        shapes[n][0] = ROMAP_WIDTH; shapes[n][1] = cd.LF; ++n;
+        for (int k = 1; k < cd.hl; ++k) { shapes[n][0] = ROMAP_WIDTH; shapes[n][1] = ROMAP_WIDTH; ++n; }
+        shapes[n][0] = 4; shapes[n][1] = ROMAP_WIDTH; ++n;
+        return n;
+    }
+    const int s[5][2] = {{ROMAP_WIDTH, cd.LF}, {ROMAP_DOUT, ROMAP_WIDTH}, {ROMAP_WIDTH, ROMAP_CIN},
+                         {ROMAP_WIDTH, ROMAP_WIDTH}, {3, ROMAP_WIDTH}};
+    for (int k = 0; k < 5; ++k) { shapes[k][0] = s[k][0]; shapes[k][1] = s[k][1]; }
+    return 5;
+}
+
+// ---------------------------------------------------------------------------
 // configuration (R5)
 static romap_status build_cfg(const romap_model_config* cfg, CfgDev& cd) {
     if (!cfg) return fail(ROMAP_E_INVALID, "null config");
@@ -219,8 +235,14 @@ static romap_status build_cfg(const romap_model_config* cfg, CfgDev& cd) {
     if (cfg->levels < 1 || cfg->levels > ROMAP_MAX_LEVELS) return fail(ROMAP_E_INVALID, "levels must be in [1,16]");
     if (cfg->log2_T < 4 || cfg->log2_T > 24) return fail(ROMAP_E_INVALID, "log2_T must be in [4,24]");
     if (cfg->base_res < 1 || !(cfg->finest_res >= cfg->base_res)) return fail(ROMAP_E_INVALID, "need finest_res >= base_res >= 1");
-    if (cfg->width != ROMAP_WIDTH || cfg->density_out != ROMAP_DOUT || cfg->color_hidden != 2 || cfg->dir_enc != ROMAP_SH)
-        return fail(ROMAP_E_INVALID, "network must be width 64, density_out 16, color_hidden 2, dir_enc 16");
+    if (cfg->network != 0 && cfg->network != 1) return fail(ROMAP_E_INVALID, "network must be 0 or 1");
+    if (cfg->width != ROMAP_WIDTH) return fail(ROMAP_E_INVALID, "width must be 64");
+    if (cfg->network == 0 && (cfg->density_out != ROMAP_DOUT || cfg->color_hidden != 2 || cfg->dir_enc != ROMAP_SH))
+        return fail(ROMAP_E_INVALID, "network 0 must be density_out 16, color_hidden 2, dir_enc 16");
+    if (cfg->network == 1 && (cfg->hidden_layers < 1 || cfg->hidden_layers > 3))
+        return fail(ROMAP_E_INVALID, "network 1 needs hidden_layers in [1,3]");
+    if (cfg->network == 1 && cfg->precision != 1)
+        return fail(ROMAP_E_INVALID, "network 1 runs on the mixed path only (precision 1)");
     if (cfg->precision != 0 && cfg->precision != 1) return fail(ROMAP_E_INVALID, "precision must be 0 or 1");
     if (cfg->precision == 1 && !fused_mixed_available()) return fail(ROMAP_E_INVALID, "mixed path not built");
     if (cfg->density_act != 0 && cfg->density_act != 1) return fail(ROMAP_E_INVALID, "density_act must be 0 or 1");
@@ -255,10 +277,15 @@ static romap_status build_cfg(const romap_model_config* cfg, CfgDev& cd) {
     }
     cd.n_entries = (int)off;
     cd.n_table = (int)(off * cd.F);
-    int w[5] = {ROMAP_WIDTH * cd.LF, ROMAP_DOUT * ROMAP_WIDTH, ROMAP_WIDTH * ROMAP_CIN, ROMAP_WIDTH * ROMAP_WIDTH,
-                3 * ROMAP_WIDTH};
+    cd.net = cfg->network;
+    cd.hl = cfg->network == 1 ? cfg->hidden_layers : 0;
+    int shapes[5][2];
+    cd.n_layers = mlp_layer_shapes(cd, shapes);
     int o = 0;
-    for (int k = 0; k < 5; ++k) { cd.w_off[k] = o; o += w[k]; }
+    for (int k = 0; k < 5; ++k) {
+        cd.w_off[k] = o;
+        if (k < cd.n_layers) o += shapes[k][0] * shapes[k][1];
+    }
     cd.n_mlp = o;
     cd.N = N;
     cd.density_act = cfg->density_act;
@@ -281,7 +308,7 @@ static bool same_model(const romap_model_config& a, const romap_model_config& b)
            a.precision == b.precision && a.density_act == b.density_act && a.samples_per_ray == b.samples_per_ray &&
            a.lr == b.lr && a.beta1 == b.beta1 && a.beta2 == b.beta2 && a.eps == b.eps &&
            a.lambda_depth == b.lambda_depth && a.lambda_density == b.lambda_density && a.loss_scale == b.loss_scale &&
-           a.obj_bg == b.obj_bg && a.seed == b.seed;
+           a.obj_bg == b.obj_bg && a.seed == b.seed && a.network == b.network && a.hidden_layers == b.hidden_layers;
 }
 
 // host RNG for initialisation (R19); independent of the training RNG streams
@@ -330,7 +357,7 @@ static Object* find(romap_ctx* ctx, int id) {
 extern "C" {
 
 const char* romap_last_error(void) { return g_err.c_str(); }
-const char* romap_version(void) { return "romap-b200 0.1 (sm_100a)"; }
+const char* romap_version(void) { return "romap-b200 0.2 (sm_100a)"; }
 
 romap_status romap_ctx_create(int32_t device, void* cuda_stream, romap_alloc_fn alloc, romap_free_fn free_fn,
                               void* user, romap_ctx** out) {
@@ -437,9 +464,9 @@ static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const roma
     std::vector<__half> h16(n);
     HostRng rng{cfg->seed ^ mix64(0x5eedULL + (unsigned long long)id)};
     for (int i = 0; i < cd.n_table; ++i) host[i] = (float)((rng.unit() * 2.0 - 1.0) * 1e-4);
-    int shapes[5][2] = {{ROMAP_WIDTH, cd.LF}, {ROMAP_DOUT, ROMAP_WIDTH}, {ROMAP_WIDTH, ROMAP_CIN},
-                        {ROMAP_WIDTH, ROMAP_WIDTH}, {3, ROMAP_WIDTH}};
-    for (int k = 0; k < 5; ++k) {
+    int shapes[5][2];
+    const int n_layers = mlp_layer_shapes(cd, shapes);
+    for (int k = 0; k < n_layers; ++k) {
         double lim = sqrt(6.0 / (shapes[k][0] + shapes[k][1]));
         for (int e = 0; e < shapes[k][0] * shapes[k][1]; ++e)
             host[cd.n_table + cd.w_off[k] + e] = (float)((rng.unit() * 2.0 - 1.0) * lim);

@@ -29,7 +29,10 @@ struct CfgDev {
     int n_entries;                // sum E_l
     int n_table;                  // n_entries * F
     int n_mlp;                    // MLP parameter count
-    int w_off[5];                 // W1..W5 offsets inside the MLP block
+    int w_off[5];                 // layer offsets inside the MLP block (W1..W5; network 1: W1, W_h.., W_out)
+    int net;                      // 0 BASELINE nets, 1 the paper's MLP (R24)
+    int hl;                       // network 1: hidden layers
+    int n_layers;
     int N;                        // samples per ray
     int density_act, obj_bg;
     float lambda_depth, lambda_density;

@@ -49,7 +49,8 @@ class ModelConfig(C.Structure):
                 ("precision", C.c_int32), ("density_act", C.c_int32), ("samples_per_ray", C.c_int32),
                 ("rays_per_iter", C.c_int32), ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("eps", C.c_float), ("lambda_depth", C.c_float), ("lambda_density", C.c_float),
-                ("loss_scale", C.c_float), ("obj_bg", C.c_int32), ("seed", C.c_uint64)]
+                ("loss_scale", C.c_float), ("obj_bg", C.c_int32), ("seed", C.c_uint64), ("network", C.c_int32),
+                ("hidden_layers", C.c_int32)]
 
 
 class TrainStats(C.Structure):
@@ -153,7 +154,7 @@ def model_config(**kw) -> ModelConfig:
     d = dict(levels=8, feats=2, log2_T=12, base_res=16, finest_res=2048.0, res_cap=128, width=64, density_out=16,
              color_hidden=2, dir_enc=16, precision=0, density_act=0, samples_per_ray=32, rays_per_iter=256, lr=1e-2,
              beta1=0.9, beta2=0.99, eps=1e-15, lambda_depth=0.5, lambda_density=0.01, loss_scale=128.0, obj_bg=0,
-             seed=0)
+             seed=0, network=0, hidden_layers=1)
     d.update(kw)
     c = ModelConfig()
     for k, v in d.items():
