@@ -47,6 +47,34 @@ def cfg1_kwargs(precision):
                 rays_per_iter=4096, precision=precision, seed=1)
 
 
+# the paper's own configuration (R24): T = 2^16, N_max = 2048,
+# single hidden layer of 64 on positions only, 4096 rays x N = 32; Table 4 varies T and layers
+PAPER_MS = {(16, 1): 0.706, (14, 1): 0.658, (18, 1): 0.921, (20, 1): 1.495, (16, 2): 0.862, (16, 3): 1.052}
+
+
+def paper_kwargs(log2_T=16, hidden_layers=1):
+    return dict(levels=16, log2_T=log2_T, base_res=16, finest_res=2048.0, res_cap=0, samples_per_ray=32,
+                rays_per_iter=4096, precision=1, seed=1, network=1, hidden_layers=hidden_layers)
+
+
+def workload_kwargs(args, precision):
+    if args.network == "paper":
+        return paper_kwargs(args.log2_T or 16, args.hidden_layers)
+    kw = cfg1_kwargs(precision)
+    if args.log2_T:
+        kw["log2_T"] = args.log2_T
+    return kw
+
+
+def paper_baseline_samples_per_s(kw):
+    """the paper's ray-samples/s for exactly this workload (4096 x 32 per
+    iteration / Table 3-4 iteration time on an RTX 4090), or None"""
+    if kw.get("network") != 1:
+        return None
+    ms = PAPER_MS.get((kw["log2_T"], kw["hidden_layers"]))
+    return None if ms is None else 4096 * 32 / (ms * 1e-3)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,7 +276,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     scene = load_scene()
-    kw = cfg1_kwargs(0)
+    kw = workload_kwargs(args, 0)
     rays = 256
     for _ in range(args.warmup):
         oracle_run(scene, kw, rays, 1)
@@ -293,7 +321,9 @@ def run_ours(args):
             precision = 1
         except R.RomapError:
             precision = 0
-    kw = cfg1_kwargs(precision)
+    if args.network == "paper":
+        precision = 1
+    kw = workload_kwargs(args, precision)
     scene = load_scene()
     from paper_2304_05735_b200.shard import partition, reduce_throughput
     objs = []
@@ -383,18 +413,27 @@ def run_ours(args):
     infer = measure_inference(ctx, objs[0], ob, scene.frames[0], torch) if rank == 0 else None
     if rank == 0:
         rf = roofline(prof, kw, precision, samples / args.steps, len(objs))
+        paper_sps = paper_baseline_samples_per_s(kw)
+        if args.network == "paper":
+            desc = (f"paper network (PAPER.md:222, R24): L=16 F=2 T=2^{kw['log2_T']} res 16->2048, "
+                    f"{kw['hidden_layers']} hidden layer(s) of 64 on positions -> sigma, rgb, 4096 rays x 32 "
+                    f"stratified samples per object, Adam")
+        else:
+            desc = ("L=16 F=2 T=2^16 res 16->512, density 32->64->16 + SH4 colour 32->64->64->3, "
+                    "4096 rays x 64 stratified samples per object, Adam")
         cpu = None if args.no_cpu_baseline else cpu_baseline(scene, kw)
         per_obj_ms = t_max_ms / args.steps / len(objs)
         line = {
             "metric": "NeRF train ray-samples/s", "value": value, "unit": "ray-samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.objects else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.objects else "weak",
+            "vs_baseline": (value / paper_sps) if paper_sps else None,
             "dtype": "f16-mma/f32" if precision == 1 else "f32",
             "data": "synthetic (seeded box-union-torus SDF object on a textured floor, 20 keyframes 640x480, 1 cm pose jitter)",
-            "config": {"workload": (f"cfg1 family: {n_total} object(s) over {ws} GPU(s) (LPT by cost)" if args.objects
-                                    else f"cfg1: {len(objs)} object(s) per GPU") +
-                                   ", L=16 F=2 T=2^16 res 16->512, density 32->64->16 + SH4 colour "
-                                   "32->64->64->3, 4096 rays x 64 stratified samples per object, Adam",
+            "config": {"workload": (f"{'paper' if args.network == 'paper' else 'cfg1'} family: {n_total} object(s) "
+                                    f"over {ws} GPU(s) (LPT by cost)" if args.objects
+                                    else f"{'paper' if args.network == 'paper' else 'cfg1'}: {len(objs)} object(s) per GPU")
+                                   + ", " + desc,
                        "objects_per_gpu": len(objs), "rays_per_iter": kw["rays_per_iter"],
                        "samples_per_ray": kw["samples_per_ray"], "keyframes": args.keyframes,
                        "precision": "mixed" if precision == 1 else "fp32",
@@ -404,7 +443,9 @@ def run_ours(args):
             "s_to_budget_per_object": BUDGET_SAMPLES / (value / max(1, ws * len(objs))),
             "ms_per_iteration_per_object": per_obj_ms,
             "paper_context": {"samples_per_s": PAPER_SAMPLES_PER_S, "ms_per_iteration": 0.706,
-                              "note": "RTX 4090, N=32, position-only 1x64 MLP (PAPER.md:222,307); not this workload"},
+                              "note": ("RTX 4090, N=32, position-only 1x64 MLP (PAPER.md:222,307); "
+                                       + ("this workload (vs_baseline = value / the paper's rate)" if paper_sps
+                                          else "not this workload"))},
             "hit_samples_per_step": samples / args.steps,
             "stage_ms_per_step": {k: v["ms"] / n_brk for k, v in prof_all.items() if v["launches"] or v["ms"]},
             "stage_ms_note": f"separate {n_brk}-iteration pass with every stage bracketed by events (not the timed region)",
@@ -425,6 +466,47 @@ def run_ours(args):
     return 0
 
 
+def run_table4(args):
+    """The paper's Table 4 grid on one GPU: ms per training iteration
+    of one object (4096 rays x 32, a1..a8 incl. Adam, L2 flushed before each iteration)
+    next to the paper's RTX 4090 numbers."""
+    import torch
+    from paper_2304_05735_b200 import romap as R
+
+    ctx = R.Context(0)
+    scene = load_scene()
+    ob = scene.objects[0]
+    rows = []
+    for (lt, hl), pms in sorted(PAPER_MS.items(), key=lambda x: (x[0][1], x[0][0])):
+        kw = paper_kwargs(lt, hl)
+        h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id)
+        for fr in scene.frames[:args.keyframes]:
+            ctx.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
+        ctx.train_step([h], args.warmup)
+        ctx.set_l2_flush(FLUSH_BYTES)
+        ctx.profile_enable(True, stages=["l2_flush"])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = ctx.train_step([h], args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+        fl = ctx.profile_read()["l2_flush"]["ms"]
+        ctx.profile_enable(False)
+        ctx.set_l2_flush(0)
+        ms = (e0.elapsed_time(e1) - fl) / args.steps
+        rows.append({"log2_T": lt, "hidden_layers": hl, "ms_per_iteration": ms,
+                     "ray_samples_per_s": st[0]["samples"] / (ms * 1e-3 * args.steps),
+                     "paper_ms_rtx4090": pms, "speedup_vs_paper": pms / ms})
+        ctx.destroy_object(h)
+    ctx.close()
+    print(json.dumps({"metric": "NeRF train ms per iteration (paper Table 4 grid)", "unit": "ms",
+                      "higher_is_better": False, "steps": args.steps, "warmup": args.warmup,
+                      "data": "synthetic cfg1-family object, 20 keyframes 640x480",
+                      "l2": "flushed before every iteration, flush time excluded", "table4": rows}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -439,11 +521,18 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--network", choices=["baseline", "paper"], default="baseline",
+                    help="baseline: BASELINE cfg1 (default, the headline); paper: PAPER.md:222 network (R24)")
+    ap.add_argument("--hidden-layers", type=int, default=1, help="--network paper: hidden layers (Table 4: 1..3)")
+    ap.add_argument("--log2-T", type=int, default=0, help="hash table size override (Table 4: 14..20)")
+    ap.add_argument("--table4", action="store_true", help="run the paper's Table 4 sweep (PAPER.md:353-357)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.table4:
+        return run_table4(args)
     return run_ours(args)
 
 
