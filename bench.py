@@ -89,7 +89,7 @@ def start_clock_sampler(dev_index):
     f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
     try:
         p = subprocess.Popen(["nvidia-smi", "-i", str(dev_index), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
-                              "-lms", "200"], stdout=f, stderr=subprocess.DEVNULL)
+                              "-lms", os.environ.get("BENCH_CLOCK_MS", "200")], stdout=f, stderr=subprocess.DEVNULL)
     except FileNotFoundError:
         return None, f.name
     return p, f.name
@@ -357,7 +357,9 @@ def run_ours(args):
         pg.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
+    th0 = time.perf_counter()
     stats = ctx.train_step(objs, args.steps)
+    host_ms = (time.perf_counter() - th0) * 1e3
     ev1.record(stream)
     torch.cuda.synchronize()
     if pg:
@@ -450,6 +452,8 @@ def run_ours(args):
             "stage_ms_per_step": {k: v["ms"] / n_brk for k, v in prof_all.items() if v["launches"] or v["ms"]},
             "stage_ms_note": f"separate {n_brk}-iteration pass with every stage bracketed by events (not the timed region)",
             "kernel_ms_per_step": sum(v["ms"] for k, v in prof_all.items() if k != "l2_flush") / n_brk,
+            "timed_region": {"total_ms": total_ms, "l2_flush_ms_subtracted": flush_ms, "host_ms_in_call": host_ms,
+                             "dominant_ms": prof.get(dominant, {}).get("ms")},
             "gpu_launches": launches,
             "roofline": rf,
             "cpu_baseline": cpu,

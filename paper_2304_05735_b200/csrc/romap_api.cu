@@ -13,6 +13,8 @@
 #include <map>
 #include <string>
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/romap.h"
@@ -730,12 +732,14 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     int K = 1;
     if (b.mixed) {
         const size_t per_iter = (size_t)b.total_slots * sizeof(RayRec) + S * 5 * sizeof(float);
-        K = (int)std::max<size_t>(1, std::min<size_t>(16, (64u << 20) / per_iter));
-        K = std::min(K, n_iters);
-        if (!grow(ctx, ctx->rays, ctx->rays_cap, (size_t)K * b.total_slots))
+        const int Kmax = (int)std::max<size_t>(1, std::min<size_t>(16, (64u << 20) / per_iter));
+        // capacity for Kmax slices on first use, whatever n_iters is: a later call
+        // with more iterations never reallocates (cudaFree synchronises the device)
+        if (!grow(ctx, ctx->rays, ctx->rays_cap, (size_t)Kmax * b.total_slots))
             return fail(ROMAP_E_OOM, "ray buffer allocation failed");
-        if (!grow(ctx, ctx->srec, ctx->srec_cap, (size_t)K * S * 5))
+        if (!grow(ctx, ctx->srec, ctx->srec_cap, (size_t)Kmax * S * 5))
             return fail(ROMAP_E_OOM, "sample record allocation failed");
+        K = std::min(Kmax, n_iters);
     }
     ctx->last_ray_base = (size_t)((n_iters - 1) % K) * b.total_slots;
     float* sigma = ctx->samp;
@@ -744,7 +748,15 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     float* delta = dist + S;
     float* dsigma = delta + S;
     float* drgb = dsigma + S;
+    // host-side cost of enqueueing (ROMAP_HOST_PROF=1: printed to stderr)
+    static const bool host_prof = getenv("ROMAP_HOST_PROF") != nullptr;
+    double hp[4] = {0, 0, 0, 0};
+    auto hnow = [] { return std::chrono::steady_clock::now(); };
+    auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
     for (int it = 0; it < n_iters; ++it) {
+        auto h0 = hnow();
         if (it == n_iters - 1) CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
         if (ctx->flush_bytes) {
             cudaEvent_t e0 = (ctx->prof.on && ((ctx->prof.mask >> ST_FLUSH) & 1u)) ? ctx->prof.get() : nullptr;
@@ -752,6 +764,8 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             CK(cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st));
             stage_end(ctx, ST_FLUSH, e0);
         }
+        auto h1 = hnow();
+        hp[0] += hms(h0, h1);
         if (b.mixed) {
             const int k = it % K;
             float4* srec = reinterpret_cast<float4*>(ctx->srec);
@@ -772,9 +786,15 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             STAGE(ST_BWD, launch_bwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dsigma, drgb,
                                           ctx->act, (long long)S));
         }
+        auto h2 = hnow();
+        hp[1] += hms(h1, h2);
         if (adam) STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed));
         CK(cudaGetLastError());
+        hp[2] += hms(h2, hnow());
     }
+    if (host_prof)
+        fprintf(stderr, "[romap host] %d iters: flush %.3f ms, raygen+fused %.3f ms, adam %.3f ms\n", n_iters, hp[0],
+                hp[1], hp[2]);
     std::vector<double> loss(4 * n);
     std::vector<unsigned long long> hits(n);
     int nf = 0;

@@ -10,17 +10,22 @@ import bench  # noqa: E402
 from paper_2304_05735_b200 import romap as R  # noqa: E402
 
 ctx = R.Context(0)
-kw = bench.cfg1_kwargs(1)
+kw = bench.paper_kwargs() if "--paper" in sys.argv else bench.cfg1_kwargs(1)
 sc = bench.load_scene()
 ob = sc.objects[0]
 h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id)
 for fr in sc.frames:
     ctx.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
 ctx.train_step([h], 10)
-for prof in (False, True):
+for prof in (None, ["l2_flush"], ["fused_mixed", "l2_flush"], "all"):
     for flush in (0, 512 << 20):
         ctx.set_l2_flush(flush)
-        ctx.profile_enable(prof)
+        if prof == "all":
+            ctx.profile_enable(True)
+        elif prof:
+            ctx.profile_enable(True, stages=prof)
+        else:
+            ctx.profile_enable(False)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
