@@ -835,3 +835,51 @@ def unflatten_mlp(vec, cfg):
         out.append(np.asarray(vec[off:off + o * i], np.float64).reshape(o, i).copy())
         off += o * i
     return out
+
+
+# --------------------------------------------------------------------------
+# f3 online policy (Eq. 5): keyframe gate and iteration budget
+# --------------------------------------------------------------------------
+def camera_centre(T_wc):
+    """camera centre in the world = translation column of T_wc (camera -> world, R8)"""
+    T = np.asarray(T_wc, np.float64).reshape(3, 4)
+    return T[:, 3].copy()
+
+
+def view_angle_deg(c_last, c_new, t_obj):
+    """Eq. 5: alpha = arccos(((t_Im - t_O) . (t_In - t_O)) / (|t_Im - t_O| |t_In - t_O|)),
+    in degrees (fp64)"""
+    a = np.asarray(c_last, np.float64) - np.asarray(t_obj, np.float64)
+    b = np.asarray(c_new, np.float64) - np.asarray(t_obj, np.float64)
+    c = float(a @ b) / (float(np.linalg.norm(a)) * float(np.linalg.norm(b)))
+    return math.degrees(math.acos(min(1.0, max(-1.0, c))))
+
+
+def keyframe_gate(last_centre, T_wc, t_obj, alpha_deg=25.0):
+    """the first observation of an object is always taken; later
+    ones iff alpha (Eq. 5, against the LAST ACCEPTED keyframe) exceeds the threshold.
+    Returns (accepted, alpha or None)."""
+    c = camera_centre(T_wc)
+    if last_centre is None:
+        return True, None
+    alpha = view_angle_deg(last_centre, c, t_obj)
+    return alpha > alpha_deg, alpha
+
+
+def schedule_budgets(pending: dict, chunk: int, max_iters: int):
+    """f3 scheduler (host policy, R25): while some object has pending
+    iterations and fewer than max_iters were run in this call, train all objects with
+    budget left for n = min(chunk, smallest pending) iterations in one batch.
+    Returns the list of (objects, n) batches and the remaining budgets."""
+    pending = dict(pending)
+    batches, done = [], 0
+    while done < max_iters:
+        live = sorted(k for k, v in pending.items() if v > 0)
+        if not live:
+            break
+        n = min(chunk, min(pending[k] for k in live), max_iters - done)
+        batches.append((live, n))
+        for k in live:
+            pending[k] -= n
+        done += n
+    return batches, pending

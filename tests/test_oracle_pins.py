@@ -663,3 +663,41 @@ def test_paper_network_step_gradient_central_differences(hl):
             an = grads["W"][a][b]
         fd = (loss_at(Pp) - loss_at(Pm)) / (2 * h)
         assert abs(fd - an) <= 1e-5 * max(1.0, abs(an)) + 1e-7, (kind, a, b, fd, an)
+
+
+# ---------------------------------------------------------------- f3 online policy (Eq. 5)
+def _pose_at(centre):
+    T = np.eye(3, 4)
+    T[:, 3] = centre
+    return T
+
+
+def test_view_angle_closed_forms():
+    o = np.array([1.0, 2.0, 0.5])
+    assert O.view_angle_deg(o + [1, 0, 0], o + [0, 3, 0], o) == pytest.approx(90.0)
+    assert O.view_angle_deg(o + [1, 0, 0], o + [2, 0, 0], o) == pytest.approx(0.0, abs=1e-6)
+    assert O.view_angle_deg(o + [1, 0, 0], o + [-1, 0, 0], o) == pytest.approx(180.0)
+    th = math.radians(30.0)
+    assert O.view_angle_deg(o + [2, 0, 0], o + [math.cos(th), math.sin(th), 0], o) == pytest.approx(30.0)
+
+
+def test_keyframe_gate_orbit():
+    # cameras every 10 degrees on a circle around the object: with alpha = 25 deg the
+    # gate accepts frames 0, 3, 6, ... (30 deg after the last accepted one)
+    o = np.array([0.3, -0.2, 0.4])
+    last, acc = None, []
+    for k in range(13):
+        c = o + 2.0 * np.array([math.cos(math.radians(10 * k)), math.sin(math.radians(10 * k)), 0.2])
+        ok, a = O.keyframe_gate(last, _pose_at(c), o, 25.0)
+        if ok:
+            last = c
+            acc.append(k)
+    assert acc == [0, 3, 6, 9, 12]
+
+
+def test_schedule_budgets():
+    b, rest = O.schedule_budgets({5: 300, 7: 120, 9: 0}, chunk=100, max_iters=1000)
+    assert b == [([5, 7], 100), ([5, 7], 20), ([5], 100), ([5], 80)]
+    assert rest == {5: 0, 7: 0, 9: 0}
+    b, rest = O.schedule_budgets({1: 300}, chunk=100, max_iters=150)
+    assert b == [([1], 100), ([1], 50)] and rest == {1: 150}
