@@ -230,6 +230,28 @@ romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n
 romap_status romap_render(romap_ctx* ctx, int32_t obj, const float T_wc[12], const romap_intrinsics* K,
                           int32_t samples_per_ray, float* rgb, float* depth, float* opacity, int32_t flags);
 
+/* Online policy (R25).
+ * offer_observation: Eq. 5 keyframe gate.  The frame becomes a training keyframe
+ * (as romap_add_observation) iff the object has none yet or the angle at the box
+ * centre between the camera centre of the LAST ACCEPTED keyframe and this frame's
+ * exceeds alpha_deg (25).  An accepted frame adds iters_per_update
+ * (300) iterations to the object's pending budget.  *accepted = 1/0;
+ * *alpha_out (nullable) = the angle in degrees, -1 for the first frame.  Errors as
+ * romap_add_observation; a rejected frame changes nothing. */
+romap_status romap_offer_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
+                                     const float T_wc[12], const romap_intrinsics* K,
+                                     const romap_depth_sample* depth, int32_t n_depth, float alpha_deg,
+                                     int32_t iters_per_update, int32_t* accepted, float* alpha_out);
+/* Pending training budget (iterations) of one object. */
+romap_status romap_pending_iters(romap_ctx* ctx, int32_t obj, int64_t* pending);
+/* Scheduler: while some object has budget left and fewer than max_iters iterations
+ * ran in this call, train every object with budget left (objects of one model
+ * configuration in ONE batched train_step) for n = min(chunk, smallest pending)
+ * iterations; an object whose budget is spent stops training.
+ * Writes up to cap (object id, iterations run) pairs, *n_out = pairs available. */
+romap_status romap_train_pending(romap_ctx* ctx, int32_t chunk, int32_t max_iters, int32_t* objs_out,
+                                 int32_t* iters_out, int32_t cap, int32_t* n_out);
+
 /* Render several objects (R20): per ray, intersect every box, sort the hit segments
  * by t_near, composite each segment's (C, A, D) front to back. */
 romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, const float T_wc[12],

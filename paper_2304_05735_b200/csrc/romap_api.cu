@@ -70,6 +70,10 @@ struct Object {
     bool grads_dirty = false;
     // last batch (debug dumps)
     int last_ray_begin = -1, last_n_rays = 0;
+    // f3 online policy (R25): camera centre of the last accepted keyframe, pending budget
+    bool has_gate_ref = false;
+    double gate_ref[3] = {0, 0, 0};
+    long long pending_iters = 0;
 };
 
 enum LastCall { LAST_NONE = 0, LAST_TRAIN = 1, LAST_FWDBWD = 2 };
@@ -855,6 +859,103 @@ romap_status romap_forward_backward(romap_ctx* ctx, const int32_t* objs, int32_t
     s = upload_batch(ctx, b, true);
     if (s) return s;
     return run_iterations(ctx, b, 1, false, out);
+}
+
+// ---------------------------------------------------------------------------
+// f3 online policy (R25): Eq. 5 keyframe gate, per-object
+// iteration budgets and a batching scheduler over them (the B200 replacement of
+// the paper's 8-thread pool: objects with budget left train together in one launch)
+romap_status romap_offer_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
+                                     const float T_wc[12], const romap_intrinsics* K,
+                                     const romap_depth_sample* depth, int32_t n_depth, float alpha_deg,
+                                     int32_t iters_per_update, int32_t* accepted, float* alpha_out) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!T_wc || !accepted) return fail(ROMAP_E_INVALID, "null pose / output");
+    if (!(alpha_deg >= 0.f) || iters_per_update < 0) return fail(ROMAP_E_INVALID, "bad gate parameters");
+    const double c[3] = {T_wc[3], T_wc[7], T_wc[11]};     // camera centre (R8: T_wc camera -> world)
+    double alpha = -1.0;
+    bool take = !ob->has_gate_ref;
+    if (ob->has_gate_ref) {
+        double a[3], b2[3], dot = 0, na = 0, nb = 0;
+        for (int k = 0; k < 3; ++k) {
+            a[k] = ob->gate_ref[k] - (double)ob->box.t[k];
+            b2[k] = c[k] - (double)ob->box.t[k];
+            dot += a[k] * b2[k];
+            na += a[k] * a[k];
+            nb += b2[k] * b2[k];
+        }
+        double cs = dot / (sqrt(na) * sqrt(nb));
+        cs = cs > 1.0 ? 1.0 : (cs < -1.0 ? -1.0 : cs);
+        alpha = acos(cs) * 180.0 / M_PI;                  // Eq. 5
+        take = alpha > (double)alpha_deg;
+    }
+    if (alpha_out) *alpha_out = (float)alpha;
+    *accepted = 0;
+    if (!take) return ROMAP_OK;
+    romap_status st = romap_add_observation(ctx, obj, rgb, mask, T_wc, K, depth, n_depth);
+    if (st) return st;
+    ob->has_gate_ref = true;
+    for (int k = 0; k < 3; ++k) ob->gate_ref[k] = c[k];
+    ob->pending_iters += iters_per_update;
+    *accepted = 1;
+    return ROMAP_OK;
+}
+
+romap_status romap_pending_iters(romap_ctx* ctx, int32_t obj, int64_t* pending) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!pending) return fail(ROMAP_E_INVALID, "null output");
+    *pending = ob->pending_iters;
+    return ROMAP_OK;
+}
+
+romap_status romap_train_pending(romap_ctx* ctx, int32_t chunk, int32_t max_iters, int32_t* objs_out,
+                                 int32_t* iters_out, int32_t cap, int32_t* n_out) {
+    CHECK_CTX();
+    if (chunk < 1 || max_iters < 0 || cap < 0 || !n_out || (cap > 0 && (!objs_out || !iters_out)))
+        return fail(ROMAP_E_INVALID, "bad scheduler arguments");
+    std::map<int, long long> ran;
+    int done = 0;
+    while (done < max_iters) {
+        // objects with budget left (ascending id), grouped by model configuration
+        std::vector<Object*> live;
+        for (auto& kv : ctx->objs)
+            if (kv.second->pending_iters > 0 && !kv.second->kfs.empty()) live.push_back(kv.second);
+        if (live.empty()) break;
+        std::vector<std::vector<Object*>> groups;
+        for (Object* ob : live) {
+            bool placed = false;
+            for (auto& g : groups)
+                if (same_model(g[0]->cfg, ob->cfg)) { g.push_back(ob); placed = true; break; }
+            if (!placed) groups.push_back({ob});
+        }
+        long long n = std::min<long long>(chunk, max_iters - done);
+        for (Object* ob : live) n = std::min(n, ob->pending_iters);
+        for (auto& g : groups) {
+            std::vector<int32_t> ids;
+            for (Object* ob : g) ids.push_back(ob->id);
+            romap_status st = romap_train_step(ctx, ids.data(), (int32_t)ids.size(), (int32_t)n, nullptr);
+            if (st) return st;
+            for (Object* ob : g) {
+                ob->pending_iters -= n;
+                ran[ob->id] += n;
+            }
+        }
+        done += (int)n;
+    }
+    int k = 0;
+    for (auto& kv : ran) {
+        if (k < cap) {
+            objs_out[k] = kv.first;
+            iters_out[k] = (int32_t)kv.second;
+        }
+        ++k;
+    }
+    *n_out = k;
+    return ROMAP_OK;
 }
 
 romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs) {

@@ -103,6 +103,10 @@ _SIGS = {
     "romap_profile_enable": [_P, _I],
     "romap_profile_read": [_P, _P, _I, C.POINTER(_I)],
     "romap_profile_stages": [_P, C.c_uint32],
+    "romap_offer_observation": [_P, _I, _P, _P, _P, C.POINTER(Intrinsics), _P, _I, C.c_float, _I, C.POINTER(_I),
+                                C.POINTER(C.c_float)],
+    "romap_pending_iters": [_P, _I, C.POINTER(C.c_int64)],
+    "romap_train_pending": [_P, _I, _I, _P, _P, _I, C.POINTER(_I)],
     "romap_set_l2_flush": [_P, C.c_int64],
 }
 
@@ -230,6 +234,38 @@ class Context:
             arr = (DepthSample * len(depth))(*[DepthSample(float(u), float(v), float(z)) for (u, v, z) in depth])
             dp, nd = C.cast(arr, C.c_void_p), len(depth)
         _check(_lib.romap_add_observation(self._h, obj, _ptr(rgb), _ptr(mask), _ptr(T), C.byref(intr), dp, nd))
+
+    def offer_observation(self, obj: int, rgb, mask, T_wc, K, depth=None, alpha_deg: float = 25.0,
+                          iters_per_update: int = 300):
+        """Eq. 5 keyframe gate (R25): returns (accepted, alpha in degrees or None)."""
+        rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        mask = np.ascontiguousarray(mask, dtype=np.uint16)
+        T = np.ascontiguousarray(np.asarray(T_wc, dtype=np.float32).reshape(12))
+        H, W = mask.shape
+        intr = Intrinsics(float(K[0]), float(K[1]), float(K[2]), float(K[3]), W, H)
+        dp, nd = None, 0
+        if depth is not None and len(depth):
+            d = np.ascontiguousarray(np.asarray(depth, dtype=np.float32).reshape(-1, 3))
+            dp, nd = _ptr(d), d.shape[0]
+        acc = C.c_int32()
+        alpha = C.c_float()
+        _check(_lib.romap_offer_observation(self._h, obj, _ptr(rgb), _ptr(mask), _ptr(T), C.byref(intr), dp, nd,
+                                            float(alpha_deg), int(iters_per_update), C.byref(acc), C.byref(alpha)))
+        return bool(acc.value), (None if alpha.value < 0 else float(alpha.value))
+
+    def pending_iters(self, obj: int) -> int:
+        p = C.c_int64()
+        _check(_lib.romap_pending_iters(self._h, obj, C.byref(p)))
+        return p.value
+
+    def train_pending(self, chunk: int = 100, max_iters: int = 1 << 30) -> dict:
+        """f3 scheduler: {object id: iterations run}."""
+        cap = 4096
+        ids = np.zeros(cap, np.int32)
+        its = np.zeros(cap, np.int32)
+        n = C.c_int32()
+        _check(_lib.romap_train_pending(self._h, int(chunk), int(max_iters), _ptr(ids), _ptr(its), cap, C.byref(n)))
+        return {int(ids[i]): int(its[i]) for i in range(min(n.value, cap))}
 
     def set_rays_per_iter(self, obj: int, rays: int):
         _check(_lib.romap_set_rays_per_iter(self._h, obj, int(rays)))
