@@ -36,6 +36,9 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   adam_update       closed form for constant gradient, zero-gradient no-op
                     (SPEC.md:271-273), sparse locality
   render / query    constant-density closed form, outside-box zero (R21)
+  marching_tetrahedra  single-vertex case counts (6 on the Kuhn diagonal, 2
+                    elsewhere), exact vertices for a linear field, sphere radius /
+                    area within the lattice step; mesh_metrics shifted-grid closed form
 No function is "parity unpinned".
 """
 from __future__ import annotations
@@ -883,3 +886,103 @@ def schedule_budgets(pending: dict, chunk: int, max_iters: int):
             pending[k] -= n
         done += n
     return batches, pending
+
+
+# --------------------------------------------------------------------------
+# f2 mesh extraction + metrics (R26)
+# --------------------------------------------------------------------------
+# Kuhn decomposition of a cube into 6 tetrahedra along the diagonal 0 -> 7; cube
+# vertex k = (k & 1, (k >> 1) & 1, (k >> 2) & 1)
+KUHN_TETS = [(0, 1 << p0, (1 << p0) | (1 << p1), 7)
+             for (p0, p1) in [(0, 1), (0, 2), (1, 0), (1, 2), (2, 0), (2, 1)]]
+
+
+def lattice_points(box_a, res):
+    """(res+1)^3 vertex lattice spanning [-a, a] (R21), indexed [ix, iy, iz], fp32"""
+    a = np.asarray(box_a, np.float64)
+    axes = [(-a[k] + 2.0 * a[k] * np.arange(res + 1) / res) for k in range(3)]
+    P = np.stack(np.meshgrid(*axes, indexing="ij"), -1)
+    return P.astype(f32)
+
+
+def marching_tetrahedra(sigma, points, iso):
+    """Isosurface sigma = iso of a vertex lattice (R26): every cell split into the 6
+    Kuhn tetrahedra; per tetrahedron with 1 or 3 vertices above iso one triangle on its
+    3 crossing edges, with 2 above a quad (2 triangles) on its 4 crossing edges; edge
+    points by linear interpolation p_a + (iso - s_a) / (s_b - s_a) (p_b - p_a).  Plain
+    loops (small lattices only).  Returns (T, 3, 3) fp64 triangles (cell order, tet
+    order), vertex order within a triangle as listed below."""
+    sigma = np.asarray(sigma, np.float64)
+    P = np.asarray(points, np.float64)
+    R = sigma.shape[0] - 1
+    tris = []
+
+    def edge(va, vb, sa, sb, pa, pb):
+        return pa + (iso - sa) / (sb - sa) * (pb - pa)
+    for ix in range(R):
+        for iy in range(R):
+            for iz in range(R):
+                cs = [sigma[ix + (k & 1), iy + ((k >> 1) & 1), iz + ((k >> 2) & 1)] for k in range(8)]
+                cp = [P[ix + (k & 1), iy + ((k >> 1) & 1), iz + ((k >> 2) & 1)] for k in range(8)]
+                for tet in KUHN_TETS:
+                    s = [cs[v] for v in tet]
+                    p = [cp[v] for v in tet]
+                    ins = [i for i in range(4) if s[i] > iso]
+                    out = [i for i in range(4) if not s[i] > iso]
+                    if len(ins) in (1, 3):
+                        a_ = ins[0] if len(ins) == 1 else out[0]
+                        others = [i for i in range(4) if i != a_]
+                        tris.append([edge(a_, o, s[a_], s[o], p[a_], p[o]) for o in others])
+                    elif len(ins) == 2:
+                        a_, b_ = ins
+                        c_, d_ = out
+                        q = [edge(a_, c_, s[a_], s[c_], p[a_], p[c_]), edge(a_, d_, s[a_], s[d_], p[a_], p[d_]),
+                             edge(b_, d_, s[b_], s[d_], p[b_], p[d_]), edge(b_, c_, s[b_], s[c_], p[b_], p[c_])]
+                        tris.append([q[0], q[1], q[2]])
+                        tris.append([q[0], q[2], q[3]])
+    return np.asarray(tris, np.float64).reshape(-1, 3, 3)
+
+
+def to_world(X, box_t, box_yaw):
+    """object frame -> world: x_w = R_z(yaw) x + t (R8, inverse of the ray transform)"""
+    c, s = math.cos(box_yaw), math.sin(box_yaw)
+    X = np.asarray(X, np.float64)
+    out = X.copy()
+    out[..., 0] = c * X[..., 0] - s * X[..., 1] + box_t[0]
+    out[..., 1] = s * X[..., 0] + c * X[..., 1] + box_t[1]
+    out[..., 2] = X[..., 2] + box_t[2]
+    return out
+
+
+def nearest_distances(A, B, chunk=2048):
+    """for every point of A the distance to its nearest point of B (brute force)"""
+    A = np.asarray(A, np.float64).reshape(-1, 3)
+    B = np.asarray(B, np.float64).reshape(-1, 3)
+    out = np.empty(A.shape[0])
+    for i in range(0, A.shape[0], chunk):
+        d2 = ((A[i:i + chunk, None, :] - B[None, :, :]) ** 2).sum(-1)
+        out[i:i + chunk] = np.sqrt(d2.min(axis=1))
+    return out
+
+
+def sample_mesh_points(tris, n, seed=0):
+    """n points uniformly on the surface of a triangle soup (area-weighted triangle
+    choice, uniform barycentric coordinates), deterministic in seed"""
+    T = np.asarray(tris, np.float64).reshape(-1, 3, 3)
+    area = 0.5 * np.linalg.norm(np.cross(T[:, 1] - T[:, 0], T[:, 2] - T[:, 0]), axis=1)
+    g = np.random.default_rng(seed)
+    idx = g.choice(len(T), size=n, p=area / area.sum())
+    r1, r2 = g.random(n), g.random(n)
+    s1 = np.sqrt(r1)
+    w0, w1, w2 = 1 - s1, s1 * (1 - r2), s1 * r2
+    return w0[:, None] * T[idx, 0] + w1[:, None] * T[idx, 1] + w2[:, None] * T[idx, 2]
+
+
+def mesh_metrics(rec_points, gt_points, tau):
+    """PAPER.md:255 (Acc / Comp / CR as in iMAP-style evaluations): accuracy = mean
+    distance from reconstructed points to the ground-truth surface samples, completion
+    = mean distance from ground-truth samples to the reconstruction, completion ratio =
+    fraction of ground-truth samples within tau"""
+    acc = nearest_distances(rec_points, gt_points).mean()
+    dc = nearest_distances(gt_points, rec_points)
+    return {"acc": float(acc), "comp": float(dc.mean()), "cr": float((dc < tau).mean())}

@@ -701,3 +701,56 @@ def test_schedule_budgets():
     assert rest == {5: 0, 7: 0, 9: 0}
     b, rest = O.schedule_budgets({1: 300}, chunk=100, max_iters=150)
     assert b == [([1], 100), ([1], 50)] and rest == {1: 150}
+
+
+# ---------------------------------------------------------------- f2 mesh extraction (R26)
+def test_mt_single_vertex_cases():
+    # vertex 0 (on the Kuhn diagonal) lies in all 6 tetrahedra -> 6 triangles;
+    # vertex 1 (+x) lies in the 2 tetrahedra whose first step is x -> 2 triangles
+    P = O.lattice_points([0.5, 0.5, 0.5], 1)
+    for k, n in [(0, 6), (7, 6), (1, 2), (2, 2), (4, 2), (3, 2), (5, 2), (6, 2)]:
+        s = np.zeros((2, 2, 2))
+        s[k & 1, (k >> 1) & 1, (k >> 2) & 1] = 1.0
+        assert O.marching_tetrahedra(s, P, 0.5).shape[0] == n, k
+    assert O.marching_tetrahedra(np.zeros((2, 2, 2)), P, 0.5).shape[0] == 0
+    assert O.marching_tetrahedra(np.ones((2, 2, 2)), P, 0.5).shape[0] == 0
+
+
+def test_mt_linear_field_exact():
+    # sigma linear in x: linear interpolation is exact, every vertex lies on the plane
+    P = O.lattice_points([0.4, 0.3, 0.2], 5).astype(np.float64)
+    s = 3.0 * P[..., 0] + 1.5 * P[..., 1] - 0.5 * P[..., 2] + 0.1
+    T = O.marching_tetrahedra(s, P, 0.35)
+    assert T.shape[0] > 0
+    v = T.reshape(-1, 3)
+    assert np.abs(3.0 * v[:, 0] + 1.5 * v[:, 1] - 0.5 * v[:, 2] + 0.1 - 0.35).max() < 1e-12
+
+
+def test_mt_sphere_and_metrics():
+    # sigma = r0 - |x| (iso 0): vertices on the sphere within the lattice step^2 and the
+    # area close to 4 pi r0^2; metrics of the mesh against exact sphere samples
+    r0 = 0.35
+    P = O.lattice_points([0.5, 0.5, 0.5], 12).astype(np.float64)
+    s = r0 - np.linalg.norm(P, axis=-1)
+    T = O.marching_tetrahedra(s, P, 0.0)
+    v = T.reshape(-1, 3)
+    h = 1.0 / 12
+    assert np.abs(np.linalg.norm(v, axis=1) - r0).max() < h * h
+    area = 0.5 * np.linalg.norm(np.cross(T[:, 1] - T[:, 0], T[:, 2] - T[:, 0]), axis=1).sum()
+    assert abs(area / (4 * np.pi * r0 * r0) - 1) < 0.05
+    # surface samples of the mesh lie on the sphere to O(h^2) (exact distance to the surface)
+    S = O.sample_mesh_points(T, 5000)
+    assert np.abs(np.linalg.norm(S, axis=1) - r0).mean() < h * h / 2
+    # metrics: a grid and the same grid shifted by dz along its normal: acc = comp = dz,
+    # completion ratio 1 above dz, 0 below
+    xs = np.linspace(0, 1, 21)
+    G = np.stack(np.meshgrid(xs, xs, [0.0], indexing="ij"), -1).reshape(-1, 3)
+    m = O.mesh_metrics(G + [0, 0, 0.013], G, tau=0.02)
+    assert abs(m["acc"] - 0.013) < 1e-12 and abs(m["comp"] - 0.013) < 1e-12 and m["cr"] == 1.0
+    assert O.mesh_metrics(G + [0, 0, 0.013], G, tau=0.01)["cr"] == 0.0
+    # to_world is the inverse of the object-frame transform of the rays (R8)
+    X = np.array([[0.1, 0.2, 0.3]])
+    W = O.to_world(X, [1.0, -2.0, 0.5], math.radians(30))
+    c, s_ = math.cos(math.radians(30)), math.sin(math.radians(30))
+    p = W[0] - [1.0, -2.0, 0.5]
+    assert np.allclose([c * p[0] + s_ * p[1], -s_ * p[0] + c * p[1], p[2]], X[0])
