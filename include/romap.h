@@ -263,6 +263,16 @@ romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, 
 romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, int64_t n, float* sigma,
                                  int32_t flags);
 
+/* Isosurface of one object's density (R26; the paper runs
+ * marching cubes on a 64^3 lattice): the (res+1)^3 vertex lattice
+ * over the box [-a, a], sigma by the object's query path, marching tetrahedra at
+ * sigma_iso (1/m).  Writes the triangles (9 floats each: 3 vertices x (x, y, z),
+ * WORLD frame, m) in the deterministic cell / tetrahedron order to tris (host, or
+ * device with ROMAP_DEVICE_PTRS) when they fit in cap_tris; *n_tris = triangle
+ * count either way (call with cap_tris = 0 to size the buffer).  1 <= res <= 1024. */
+romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float sigma_iso, float* tris,
+                                int64_t cap_tris, int64_t* n_tris, int32_t flags);
+
 /* Copy a parameter block (see ROMAP_BLOCK_*) to / from a host buffer of exactly the
  * block's size in bytes. */
 romap_status romap_get_params(romap_ctx* ctx, int32_t obj, int32_t block, void* buf, int64_t bytes);

@@ -26,6 +26,10 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
 bool fused_mixed_available();
 void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const RayRec* rays, int n_rays,
                       float* sigma, float* rgb, float* dist, float* delta);
+void launch_lattice(const LaunchCtx& lc, const ObjDev* obj, int R, float* pts);
+size_t mt_scan_bytes(long long ncell);
+void launch_mt(const LaunchCtx& lc, const ObjDev* obj, const float* sig, const float* pts, int R, float iso,
+               int* counts, int* offsets, void* tmp, size_t tmp_bytes, float* tris, bool emit);
 void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz,
                                 long long n, float* sigma);
 
@@ -129,6 +133,10 @@ struct romap_ctx {
     size_t stat_cap = 0;
     float* scene_d = nullptr;    // render_scene: per object C (rgb), A, D, t_near, HW floats each
     size_t scene_cap = 0;
+    float* mesh_d = nullptr;     // extract_mesh: lattice points | sigma | counts | offsets | CUB scratch
+    size_t mesh_cap = 0;
+    float* tris_d = nullptr;     // extract_mesh: triangles (device staging for host outputs)
+    size_t tris_cap = 0;
     float* io_d = nullptr;       // render / query staging
     size_t io_cap = 0;
     // last batch
@@ -418,6 +426,8 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->samp);
     dfree(ctx, ctx->srec);
     dfree(ctx, ctx->scene_d);
+    dfree(ctx, ctx->mesh_d);
+    dfree(ctx, ctx->tris_d);
     dfree(ctx, ctx->act);
     dfree(ctx, ctx->objdev_d);
     dfree(ctx, ctx->single_d);
@@ -1087,6 +1097,54 @@ romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, 
         if (opacity) CK(cudaMemcpyAsync(opacity, o_opa, HW * 4, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
     }
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// f2 mesh extraction (R26): lattice -> sigma (the object's query kernel) ->
+// marching tetrahedra count / scan / emit (k_mesh.cu)
+romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float sigma_iso, float* tris,
+                                int64_t cap_tris, int64_t* n_tris, int32_t flags) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (res < 1 || res > 1024 || !n_tris || cap_tris < 0 || (cap_tris > 0 && !tris))
+        return fail(ROMAP_E_INVALID, "bad mesh arguments");
+    const long long n1 = res + 1, nv = n1 * n1 * n1, nc = (long long)res * res * res;
+    const size_t scan_bytes = mt_scan_bytes(nc);
+    // floats: points 3 nv | sigma nv | counts nc + 1 | offsets nc + 1 | scratch
+    const size_t need = (size_t)(4 * nv + 2 * (nc + 1)) + scan_bytes / 4 + 64;
+    if (!grow(ctx, ctx->mesh_d, ctx->mesh_cap, need)) return fail(ROMAP_E_OOM, "mesh scratch");
+    float* pts = ctx->mesh_d;
+    float* sig = pts + 3 * nv;
+    int* counts = reinterpret_cast<int*>(sig + nv);
+    int* offsets = counts + (nc + 1);
+    void* tmp = reinterpret_cast<void*>(((uintptr_t)(offsets + (nc + 1)) + 255) & ~(uintptr_t)255);
+    ObjDev od = make_objdev(ob);
+    CK(cudaMemcpyAsync(ctx->single_d, &od, sizeof od, cudaMemcpyHostToDevice, ctx->st));
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    launch_lattice(lc, ctx->single_d, res, pts);
+    if (ob->cfg.precision == 1)
+        launch_query_density_mixed(lc, ob->cdev, ctx->single_d, pts, nv, sig);
+    else
+        launch_query_density(lc, ob->cdev, ctx->single_d, pts, nv, sig);
+    launch_mt(lc, ctx->single_d, sig, pts, res, sigma_iso, counts, offsets, tmp, scan_bytes, nullptr, false);
+    CK(cudaGetLastError());
+    int total = 0;
+    CK(cudaMemcpyAsync(&total, offsets + nc, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    *n_tris = total;
+    if (total == 0 || total > cap_tris) return ROMAP_OK;
+    const bool dev = flags & ROMAP_DEVICE_PTRS;
+    float* out = tris;
+    if (!dev) {
+        if (!grow(ctx, ctx->tris_d, ctx->tris_cap, (size_t)total * 9)) return fail(ROMAP_E_OOM, "triangle buffer");
+        out = ctx->tris_d;
+    }
+    launch_mt(lc, ctx->single_d, sig, pts, res, sigma_iso, counts, offsets, tmp, scan_bytes, out, true);
+    CK(cudaGetLastError());
+    if (!dev) CK(cudaMemcpyAsync(tris, out, (size_t)total * 36, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
     return ROMAP_OK;
 }
 

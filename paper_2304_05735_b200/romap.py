@@ -103,6 +103,7 @@ _SIGS = {
     "romap_profile_enable": [_P, _I],
     "romap_profile_read": [_P, _P, _I, C.POINTER(_I)],
     "romap_profile_stages": [_P, C.c_uint32],
+    "romap_extract_mesh": [_P, _I, _I, C.c_float, _P, C.c_int64, C.POINTER(C.c_int64), _I],
     "romap_offer_observation": [_P, _I, _P, _P, _P, C.POINTER(Intrinsics), _P, _I, C.c_float, _I, C.POINTER(_I),
                                 C.POINTER(C.c_float)],
     "romap_pending_iters": [_P, _I, C.POINTER(C.c_int64)],
@@ -308,6 +309,15 @@ class Context:
         _check(_lib.romap_render_scene(self._h, _ptr(ids), n, _ptr(T), C.byref(intr), samples_per_segment, _ptr(rgb),
                                        _ptr(dep), _ptr(opa), 0))
         return rgb, dep, opa
+
+    def extract_mesh(self, obj: int, res: int = 64, sigma_iso: float = 20.0):
+        """Marching-tetrahedra isosurface (R26): (T, 3, 3) float32 world-frame triangles."""
+        n = C.c_int64()
+        _check(_lib.romap_extract_mesh(self._h, obj, int(res), float(sigma_iso), None, 0, C.byref(n), 0))
+        out = np.zeros((max(n.value, 1), 3, 3), np.float32)
+        if n.value:
+            _check(_lib.romap_extract_mesh(self._h, obj, int(res), float(sigma_iso), _ptr(out), n.value, C.byref(n), 0))
+        return out[:n.value]
 
     def query_density(self, obj: int, xyz):
         """xyz: numpy (n,3) float32 (host) or a CUDA torch tensor (device pointers)."""
