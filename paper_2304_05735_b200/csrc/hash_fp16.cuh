@@ -60,8 +60,8 @@ __device__ __forceinline__ int4 level_params(const CfgDev& cfg, int l) {
 
 // encode two levels (P0/P1 at offsets off0/off1) of one point into two half2
 // features: x-neighbour corner pairs as one LDG.128 (+ a 4-byte load when the
-// pair straddles a 16-byte chunk), packed-fp16 trilinear lerps (x, y, z); zeros
-// when !on
+// pair straddles a 16-byte chunk), trilinear lerps (x, y, z) in fp32 of the fp16
+// corners, rounded once to fp16; zeros when !on
 __device__ __forceinline__ void encode_pair_fp16(const uint32_t* __restrict__ tab, const float u[3], const int4 P[2],
                                                  const unsigned off[2], unsigned hmask, bool on, __half2 (&fq)[2]) {
     uint4 qv[2][4];
@@ -80,21 +80,20 @@ __device__ __forceinline__ void encode_pair_fp16(const uint32_t* __restrict__ ta
     }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        const __half2 fx = __float2half2_rn(cl[q].f[0]), fy = __float2half2_rn(cl[q].f[1]),
-                      fz = __float2half2_rn(cl[q].f[2]);
-        __half2 vx[4];
+        float2 vx[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
             const unsigned ea = e[q][2 * p], eb = e[q][2 * p + 1];
             const bool same = (ea >> 2) == (eb >> 2);
             const uint32_t h0 = sel4(qv[q][p], ea & 3);
             const uint32_t h1 = same ? sel4(qv[q][p], eb & 3) : xv[q][p];
-            const __half2 a = *reinterpret_cast<const __half2*>(&h0);
-            const __half2 c = *reinterpret_cast<const __half2*>(&h1);
-            vx[p] = __hfma2(fx, __hsub2(c, a), a);
+            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h0));
+            const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h1));
+            vx[p] = make_float2(a.x + cl[q].f[0] * (c.x - a.x), a.y + cl[q].f[0] * (c.y - a.y));
         }
-        const __half2 vy0 = __hfma2(fy, __hsub2(vx[1], vx[0]), vx[0]);
-        const __half2 vy1 = __hfma2(fy, __hsub2(vx[3], vx[2]), vx[2]);
-        fq[q] = __hfma2(fz, __hsub2(vy1, vy0), vy0);
+        const float fy = cl[q].f[1], fz = cl[q].f[2];
+        const float2 y0 = make_float2(vx[0].x + fy * (vx[1].x - vx[0].x), vx[0].y + fy * (vx[1].y - vx[0].y));
+        const float2 y1 = make_float2(vx[2].x + fy * (vx[3].x - vx[2].x), vx[2].y + fy * (vx[3].y - vx[2].y));
+        fq[q] = __floats2half2_rn(y0.x + fz * (y1.x - y0.x), y0.y + fz * (y1.y - y0.y));
     }
 }
