@@ -85,16 +85,43 @@ __device__ __forceinline__ void count_hit(unsigned long long* hit_count, int lo,
     }
 }
 
+// thread per ray slot; blockIdx.y = k: iteration step + 1 + k, slice k of rays
 __global__ void __launch_bounds__(128) k_raygen(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
                                                 int total_slots, RayRec* __restrict__ rays,
                                                 unsigned long long* __restrict__ hit_count) {
     int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= total_slots) return;
+    const int k = blockIdx.y;
     RayRec rr;
     bool active;
-    int lo = make_ray_rec(cfg, objs, n_objs, g, 0, rr, active);
-    rays[g] = rr;
+    int lo = make_ray_rec(cfg, objs, n_objs, g, k, rr, active);
+    rays[(long long)k * total_slots + g] = rr;
     count_hit(hit_count, lo, active);
+}
+
+// mixed path, second phase: thread per sample of slice k = blockIdx.y, from the
+// ray records k_raygen wrote: srec = (u, dist) (u = -1 for inactive rays),
+// sdelta = delta (R12, R6; the same device functions as the fp32 path)
+__global__ void __launch_bounds__(256) k_samples(CfgDev cfg, const ObjDev* __restrict__ objs, int total_slots,
+                                                 const RayRec* __restrict__ rays, float4* __restrict__ srec,
+                                                 float* __restrict__ sdelta) {
+    const int N = cfg.N, k = blockIdx.y;
+    const long long S = (long long)total_slots * N;
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int g = (int)(s / N), i = (int)(s - (long long)g * N);
+    const RayRec rr = rays[(long long)k * total_slots + g];
+    float4 o = make_float4(-1.f, -1.f, -1.f, 0.f);
+    float delta = 0.f;
+    if (rr.flags & RF_ACTIVE) {
+        const ObjDev& ob = objs[rr.slot];
+        unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1 + k);
+        float dist, u[3];
+        sample_geometry(rr, i, N, pre, g - ob.ray_begin, ob.a, dist, delta, u);
+        o = make_float4(u[0], u[1], u[2], dist);
+    }
+    srec[k * S + s] = o;
+    sdelta[k * S + s] = delta;
 }
 
 // mixed path: thread per SAMPLE, for a chunk of consecutive iterations
@@ -161,10 +188,14 @@ void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, i
 
 void launch_raygen_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
                            int n_iters, RayRec* rays, float4* srec, float* sdelta, unsigned long long* hit_count) {
-    long long S = (long long)total_slots * cfg.N;
-    dim3 grid((unsigned)((S + 127) / 128), (unsigned)n_iters);
-    if (grid.x > 0 && n_iters > 0)
-        k_raygen_samples<<<grid, 128, 0, lc.st>>>(cfg, objs, n_objs, total_slots, rays, srec, sdelta, hit_count);
+    // two phases: every ray of the chunk in one wave (the per-ray chain of dependent
+    // loads is latency-bound), then every sample from the ray records
+    const long long S = (long long)total_slots * cfg.N;
+    if (total_slots == 0 || n_iters == 0) return;
+    k_raygen<<<dim3((unsigned)((total_slots + 127) / 128), (unsigned)n_iters), 128, 0, lc.st>>>(
+        cfg, objs, n_objs, total_slots, rays, hit_count);
+    k_samples<<<dim3((unsigned)((S + 255) / 256), (unsigned)n_iters), 256, 0, lc.st>>>(cfg, objs, total_slots, rays,
+                                                                                       srec, sdelta);
 }
 
 // inference rays: every pixel of a W x H image from pose `cam` (R12, R20)
