@@ -124,62 +124,6 @@ __global__ void __launch_bounds__(256) k_samples(CfgDev cfg, const ObjDev* __res
     sdelta[k * S + s] = delta;
 }
 
-// mixed path: thread per SAMPLE, for a chunk of consecutive iterations
-// (blockIdx.y = k: the iteration `step + 1 + k`, R13).  The N threads of a ray
-// rebuild its record (identical loads, broadcast), thread i = 0 stores it and
-// counts the hit, and every thread stores its sample's geometry (R12, R6):
-// srec[s] = (u, dist) with u = (-1, -1, -1) for samples of inactive rays,
-// sdelta[s] = delta.  Bit-exact with the per-sample recomputation of the fp32
-// path (same device functions).  Output slice k starts at rays + k * slots and
-// srec / sdelta + k * slots * N.
-__global__ void __launch_bounds__(128) k_raygen_samples(CfgDev cfg, const ObjDev* __restrict__ objs, int n_objs,
-                                                        int total_slots, RayRec* __restrict__ rays,
-                                                        float4* __restrict__ srec, float* __restrict__ sdelta,
-                                                        unsigned long long* __restrict__ hit_count) {
-    const int N = cfg.N;
-    const int k = blockIdx.y;
-    const long long S = (long long)total_slots * N;
-    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = (int)(s / N);
-    const bool in = g < total_slots;          // (always true for the mixed path: S % 128 == 0)
-    const int i = (int)(s - (long long)g * N);
-    // one lane per ray segment of the warp builds the record, the others receive
-    // the fields the samples need by shuffle (rays never straddle a warp segment:
-    // segments of min(N, 32) lanes are aligned)
-    const int lane = threadIdx.x & 31, seg = N < 32 ? N : 32, src = lane & ~(seg - 1);
-    RayRec rr;
-    bool active = false;
-    int lo = 0;
-    if (lane == src && in) {
-        lo = make_ray_rec(cfg, objs, n_objs, g, k, rr, active);
-        if (i == 0) rays[(long long)k * total_slots + g] = rr;
-    }
-    __syncwarp();
-    const unsigned full = 0xffffffffu;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        rr.o[c] = __shfl_sync(full, rr.o[c], src);
-        rr.d[c] = __shfl_sync(full, rr.d[c], src);
-    }
-    rr.tn = __shfl_sync(full, rr.tn, src);
-    rr.tf = __shfl_sync(full, rr.tf, src);
-    active = __shfl_sync(full, active ? 1 : 0, src) != 0;
-    lo = __shfl_sync(full, lo, src);
-    count_hit(hit_count, lo, active && i == 0);
-    if (!in) return;
-    float4 o = make_float4(-1.f, -1.f, -1.f, 0.f);
-    float delta = 0.f;
-    if (active) {
-        const ObjDev& ob = objs[lo];
-        unsigned long long pre = rng_prefix(cfg.seed, ob.obj_id, *ob.step + 1 + k);
-        float dist, u[3];
-        sample_geometry(rr, i, N, pre, g - ob.ray_begin, ob.a, dist, delta, u);
-        o = make_float4(u[0], u[1], u[2], dist);
-    }
-    srec[k * S + s] = o;
-    sdelta[k * S + s] = delta;
-}
-
 void launch_raygen(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
                    RayRec* rays, unsigned long long* hit_count) {
     int blocks = (total_slots + 127) / 128;
