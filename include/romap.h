@@ -52,6 +52,7 @@ typedef int32_t romap_status;
 
 /* flags */
 #define ROMAP_DEVICE_PTRS 1           /* buffers are device pointers (see above)      */
+#define ROMAP_MESH_CARVE 2            /* extract_mesh: zero sigma where no keyframe sees the lattice (R26) */
 
 typedef struct romap_ctx romap_ctx;
 
@@ -269,7 +270,10 @@ romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, 
  * sigma_iso (1/m).  Writes the triangles (9 floats each: 3 vertices x (x, y, z),
  * WORLD frame, m) in the deterministic cell / tetrahedron order to tris (host, or
  * device with ROMAP_DEVICE_PTRS) when they fit in cap_tris; *n_tris = triangle
- * count either way (call with cap_tris = 0 to size the buffer).  1 <= res <= 1024. */
+ * count either way (call with cap_tris = 0 to size the buffer).  1 <= res <= 1024.
+ * flags & ROMAP_MESH_CARVE: before extraction, sigma := 0 at vertices that lie in
+ * front of no keyframe camera inside its detection box (R26; E_STATE without
+ * keyframes). */
 romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float sigma_iso, float* tris,
                                 int64_t cap_tris, int64_t* n_tris, int32_t flags);
 

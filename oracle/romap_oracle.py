@@ -986,3 +986,28 @@ def mesh_metrics(rec_points, gt_points, tau):
     acc = nearest_distances(rec_points, gt_points).mean()
     dc = nearest_distances(gt_points, rec_points)
     return {"acc": float(acc), "comp": float(dc.mean()), "cr": float((dc < tau).mean())}
+
+
+def observed_mask(points, box_t, box_yaw, kfs):
+    """R26 visibility carve: a lattice vertex (object frame) is observed iff it lies in
+    front of some keyframe's camera and projects into that keyframe's detection box
+    (the pixels training rays come from).  fp32, one rounding per
+    operation in the order written (bit-exact with the GPU): x_w = R_z x + t,
+    d = x_w - c (c = camera centre), x_c = R^T d, u = fx (x_c0 / x_c2) + cx,
+    v = fy (x_c1 / x_c2) + cy; in box iff x0 <= u < x0 + w and y0 <= v < y0 + h."""
+    P = np.asarray(points, f32).reshape(-1, 3)
+    c = f32(math.cos(box_yaw))
+    s = f32(math.sin(box_yaw))
+    t = np.asarray(box_t, f32)
+    xw = [(c * P[:, 0] - s * P[:, 1]) + t[0], (s * P[:, 0] + c * P[:, 1]) + t[1], P[:, 2] + t[2]]
+    seen = np.zeros(P.shape[0], bool)
+    for kf in kfs:
+        T = np.asarray(kf.T_wc, f32).reshape(3, 4)
+        d = [xw[k] - T[k, 3] for k in range(3)]
+        xc = [(T[0, k] * d[0] + T[1, k] * d[1]) + T[2, k] * d[2] for k in range(3)]
+        fx, fy, cx, cy = [f32(v) for v in kf.K]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            u = fx * (xc[0] / xc[2]) + cx
+            v = fy * (xc[1] / xc[2]) + cy
+        seen |= (xc[2] > 0) & (u >= kf.x0) & (u < kf.x0 + kf.w) & (v >= kf.y0) & (v < kf.y0 + kf.h)
+    return seen

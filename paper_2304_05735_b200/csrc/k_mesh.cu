@@ -131,7 +131,38 @@ __global__ void k_mt_emit(const ObjDev* __restrict__ obj, const float* __restric
     }
 }
 
+// R26 visibility carve: sigma := 0 at lattice vertices that no keyframe sees
+// inside its detection box (fp32, one rounding per operation, oracle order)
+__global__ void k_carve(const ObjDev* __restrict__ obj, const float* __restrict__ pts, long long nv,
+                        float* __restrict__ sig) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const ObjDev& ob = *obj;
+    const float x = pts[3 * v], y = pts[3 * v + 1], z = pts[3 * v + 2];
+    const float xw[3] = {__fadd_rn(__fsub_rn(__fmul_rn(ob.c, x), __fmul_rn(ob.s, y)), ob.t[0]),
+                         __fadd_rn(__fadd_rn(__fmul_rn(ob.s, x), __fmul_rn(ob.c, y)), ob.t[1]),
+                         __fadd_rn(z, ob.t[2])};
+    bool seen = false;
+    for (int k = 0; k < ob.n_kf && !seen; ++k) {
+        const KfDev& kf = ob.kfs[k];
+        const float d[3] = {__fsub_rn(xw[0], kf.T[3]), __fsub_rn(xw[1], kf.T[7]), __fsub_rn(xw[2], kf.T[11])};
+        float xc[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            xc[c] = __fadd_rn(__fadd_rn(__fmul_rn(kf.T[c], d[0]), __fmul_rn(kf.T[4 + c], d[1])), __fmul_rn(kf.T[8 + c], d[2]));
+        const float u = __fadd_rn(__fmul_rn(kf.fx, __fdiv_rn(xc[0], xc[2])), kf.cx);
+        const float w = __fadd_rn(__fmul_rn(kf.fy, __fdiv_rn(xc[1], xc[2])), kf.cy);
+        seen = xc[2] > 0.f && u >= (float)kf.x0 && u < (float)(kf.x0 + kf.w) && w >= (float)kf.y0 &&
+               w < (float)(kf.y0 + kf.h);
+    }
+    if (!seen) sig[v] = 0.f;
+}
+
 }  // namespace
+
+void launch_carve(const LaunchCtx& lc, const ObjDev* obj, const float* pts, long long nv, float* sig) {
+    k_carve<<<(unsigned)((nv + 255) / 256), 256, 0, lc.st>>>(obj, pts, nv, sig);
+}
 
 void launch_lattice(const LaunchCtx& lc, const ObjDev* obj, int R, float* pts) {
     const long long n1 = R + 1, n = n1 * n1 * n1;

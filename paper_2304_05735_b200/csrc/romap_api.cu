@@ -27,6 +27,7 @@ bool fused_mixed_available();
 void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const RayRec* rays, int n_rays,
                       float* sigma, float* rgb, float* dist, float* delta);
 void launch_lattice(const LaunchCtx& lc, const ObjDev* obj, int R, float* pts);
+void launch_carve(const LaunchCtx& lc, const ObjDev* obj, const float* pts, long long nv, float* sig);
 size_t mt_scan_bytes(long long ncell);
 void launch_mt(const LaunchCtx& lc, const ObjDev* obj, const float* sig, const float* pts, int R, float iso,
                int* counts, int* offsets, void* tmp, size_t tmp_bytes, float* tris, bool emit);
@@ -1128,6 +1129,10 @@ romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float 
         launch_query_density_mixed(lc, ob->cdev, ctx->single_d, pts, nv, sig);
     else
         launch_query_density(lc, ob->cdev, ctx->single_d, pts, nv, sig);
+    if (flags & ROMAP_MESH_CARVE) {
+        if (ob->kfs.empty()) return fail(ROMAP_E_STATE, "carving needs keyframes");
+        launch_carve(lc, ctx->single_d, pts, nv, sig);
+    }
     launch_mt(lc, ctx->single_d, sig, pts, res, sigma_iso, counts, offsets, tmp, scan_bytes, nullptr, false);
     CK(cudaGetLastError());
     int total = 0;

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("ROMAP_LIB") or os.path.join(_HERE, "libromap.so")   #
 OK = 0
 E_INVALID, E_NOT_FOUND, E_OOM, E_CUDA, E_NONFINITE, E_CONFIG_MISMATCH, E_STATE = -1, -2, -3, -4, -5, -6, -7
 DEVICE_PTRS = 1
+MESH_CARVE = 2
 BLOCK_TABLE, BLOCK_MLP, BLOCK_GRAD_TABLE, BLOCK_GRAD_MLP = 0, 1, 2, 3
 BLOCK_M_TABLE, BLOCK_M_MLP, BLOCK_V_TABLE, BLOCK_V_MLP, BLOCK_STEP = 4, 5, 6, 7, 8
 DUMP_RAYS, DUMP_SAMPLES, DUMP_HASH_IDX, DUMP_FEATURES, DUMP_FIELD, DUMP_RAY_GRADS = 0, 1, 2, 3, 4, 5
@@ -310,13 +311,16 @@ class Context:
                                        _ptr(dep), _ptr(opa), 0))
         return rgb, dep, opa
 
-    def extract_mesh(self, obj: int, res: int = 64, sigma_iso: float = 20.0):
-        """Marching-tetrahedra isosurface (R26): (T, 3, 3) float32 world-frame triangles."""
+    def extract_mesh(self, obj: int, res: int = 64, sigma_iso: float = 20.0, carve: bool = False):
+        """Marching-tetrahedra isosurface (R26): (T, 3, 3) float32 world-frame triangles;
+        carve: zero the density where no keyframe sees the lattice."""
         n = C.c_int64()
-        _check(_lib.romap_extract_mesh(self._h, obj, int(res), float(sigma_iso), None, 0, C.byref(n), 0))
+        fl = MESH_CARVE if carve else 0
+        _check(_lib.romap_extract_mesh(self._h, obj, int(res), float(sigma_iso), None, 0, C.byref(n), fl))
         out = np.zeros((max(n.value, 1), 3, 3), np.float32)
         if n.value:
-            _check(_lib.romap_extract_mesh(self._h, obj, int(res), float(sigma_iso), _ptr(out), n.value, C.byref(n), 0))
+            _check(_lib.romap_extract_mesh(self._h, obj, int(res), float(sigma_iso), _ptr(out), n.value, C.byref(n),
+                                           fl))
         return out[:n.value]
 
     def query_density(self, obj: int, xyz):

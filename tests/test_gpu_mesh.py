@@ -50,3 +50,33 @@ def test_trained_sphere_reconstruction():
     m = O.mesh_metrics(O.sample_mesh_points(T, 8000), gt, tau=0.08)
     assert m["comp"] < 0.04 and m["cr"] > 0.9, m
     c.close()
+
+
+def test_carved_mesh_matches_oracle_and_improves_accuracy():
+    c = R.Context(0)
+    sc = scenes.sphere_scene(0, n_views=8)
+    h, st = make_pair(R, c, sc, CFG0M, avoid_kinks=False)
+    res = 12
+    P = O.lattice_points(st.box_a, res)
+    sig = c.query_density(h, P.reshape(-1, 3)).reshape(res + 1, res + 1, res + 1)
+    seen = O.observed_mask(P.reshape(-1, 3), st.box_t, st.box_yaw, st.kfs).reshape(sig.shape)
+    assert 0 < seen.sum() < seen.size                # the views leave box corners unseen
+    iso = float(np.median(sig))
+    T = c.extract_mesh(h, res, iso, carve=True)
+    To = O.to_world(O.marching_tetrahedra(np.where(seen, sig, 0.0), P, iso), st.box_t, st.box_yaw)
+    assert T.shape == To.shape and np.abs(T - To).max() < 1e-5
+    c.close()
+    # trained sphere: carving removes the untrained box regions -> accuracy
+    c = R.Context(0)
+    ob = sc.objects[0]
+    h = c.create_object(ob.t, ob.yaw, ob.a, R.model_config(**dict(CFG0M, rays_per_iter=1024)), ob.instance_id)
+    for fr in sc.frames:
+        c.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
+    c.train_step([h], 600)
+    g = np.random.default_rng(0).normal(size=(4000, 3))
+    gt = 0.4 * g / np.linalg.norm(g, axis=1, keepdims=True) + np.asarray(ob.t, np.float64)
+    m0 = O.mesh_metrics(O.sample_mesh_points(c.extract_mesh(h, 64, 20.0), 8000), gt, tau=0.08)
+    m1 = O.mesh_metrics(O.sample_mesh_points(c.extract_mesh(h, 64, 20.0, carve=True), 8000), gt, tau=0.08)
+    assert m1["acc"] < m0["acc"] and m1["comp"] < 0.04 and m1["cr"] > 0.9, (m0, m1)
+    print("uncarved", m0, "carved", m1)
+    c.close()

@@ -754,3 +754,16 @@ def test_mt_sphere_and_metrics():
     c, s_ = math.cos(math.radians(30)), math.sin(math.radians(30))
     p = W[0] - [1.0, -2.0, 0.5]
     assert np.allclose([c * p[0] + s_ * p[1], -s_ * p[0] + c * p[1], p[2]], X[0])
+
+
+def test_observed_mask_projection():
+    # one camera at z = 2 looking down -z (OpenCV: camera z -> world -z), f = 100,
+    # detection box = the central 20 x 20 pixels of a 100 x 100 image: a point at the
+    # origin is seen, points 0.5 m off-axis (u = 50 + 100 * 0.5 / 2 = 75) are not
+    T = np.array([[1, 0, 0, 0], [0, -1, 0, 0], [0, 0, -1, 2.0]], np.float32)
+    kf = O.Keyframe(T_wc=T, K=np.array([100, 100, 50, 50], np.float32), x0=40, y0=40, w=20, h=20,
+                    rgb=None, cls=None, depth=None)
+    P = np.array([[0, 0, 0], [0.5, 0, 0], [0, 0.5, 0], [0.15, 0.15, 0], [0, 0, 3.0]], np.float32)
+    assert O.observed_mask(P, [0, 0, 0], 0.0, [kf]).tolist() == [True, False, False, True, False]
+    # the box pose moves the points: a box translated by 0.5 m in x puts its origin off-axis
+    assert O.observed_mask(P[:1], [0.5, 0, 0], 0.0, [kf]).tolist() == [False]
