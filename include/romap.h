@@ -253,6 +253,25 @@ romap_status romap_pending_iters(romap_ctx* ctx, int32_t obj, int64_t* pending);
 romap_status romap_train_pending(romap_ctx* ctx, int32_t chunk, int32_t max_iters, int32_t* objs_out,
                                  int32_t* iters_out, int32_t cap, int32_t* n_out);
 
+/* Asynchronous online trainer (f3: frames flow one way from the
+ * SLAM side and never block it).  async_start spawns a worker thread that owns the
+ * context: it takes queued frames through offer_observation (alpha_deg,
+ * iters_per_update) and, when the queue is empty, trains pending budgets one chunk
+ * at a time (train_pending).  async_offer copies the frame (rgb H*W*3, mask H*W,
+ * pose, intrinsics) into a queue of queue_cap frames and returns at once: *queued =
+ * 1, or 0 when the queue is full (the frame is dropped, the producer never waits).
+ * While the worker runs every other call on the context returns E_STATE.
+ * async_stop joins the worker after draining the queue, and first trains every
+ * pending budget when finish_pending; it returns the worker's first error, if any. */
+typedef struct {
+    int64_t offered, dropped, accepted, iterations, max_queue_depth;
+} romap_async_stats;
+romap_status romap_async_start(romap_ctx* ctx, int32_t chunk, float alpha_deg, int32_t iters_per_update,
+                               int32_t queue_cap);
+romap_status romap_async_offer(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
+                               const float T_wc[12], const romap_intrinsics* K, int32_t* queued);
+romap_status romap_async_stop(romap_ctx* ctx, int32_t finish_pending, romap_async_stats* out);
+
 /* Render several objects (R20): per ray, intersect every box, sort the hit segments
  * by t_near, composite each segment's (C, A, D) front to back. */
 romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, const float T_wc[12],

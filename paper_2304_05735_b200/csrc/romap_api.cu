@@ -13,6 +13,11 @@
 #include <map>
 #include <string>
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <chrono>
 #include <cstdlib>
 #include <vector>
@@ -104,6 +109,28 @@ struct Profiler {
     }
 };
 
+struct AsyncFrame {
+    int obj;
+    std::vector<uint8_t> rgb;
+    std::vector<uint16_t> mask;
+    float T[12];
+    romap_intrinsics K;
+};
+
+// f3 asynchronous online trainer (romap_async_*): a worker thread owns the context
+struct AsyncState {
+    std::thread worker;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<AsyncFrame> queue;
+    bool stop = false, finish = false;
+    int chunk = 100, iters_per_update = 300, cap = 64;
+    float alpha_deg = 25.f;
+    long long offered = 0, dropped = 0, accepted = 0, iterations = 0, max_depth = 0;
+    romap_status error = 0;
+    std::string error_msg;
+};
+
 struct romap_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -146,6 +173,7 @@ struct romap_ctx {
     int last_call = LAST_NONE;
     int last_total_slots = 0;
     Profiler prof;
+    AsyncState* async = nullptr;    // non-null while the async worker runs
     void* flush_buf = nullptr;
     size_t flush_bytes = 0;
 };
@@ -219,10 +247,15 @@ static bool grow(romap_ctx* c, T*& ptr, size_t& cap, size_t need) {
         }                                                                                         \
     } while (0)
 
+// true on the async worker thread (it may use the context while async runs)
+static thread_local bool t_async_worker = false;
+
 #define CHECK_CTX()                                                                 \
     do {                                                                            \
         if (!ctx) return fail(ROMAP_E_INVALID, "null context");                     \
         if (ctx->poisoned) return fail(ROMAP_E_CUDA, "context poisoned by an earlier CUDA error"); \
+        if (ctx->async && !t_async_worker)                                         \
+            return fail(ROMAP_E_STATE, "the async worker owns the context (romap_async_stop first)"); \
         cudaSetDevice(ctx->device);                                                 \
     } while (0)
 
@@ -420,6 +453,7 @@ static void free_object(romap_ctx* ctx, Object* ob) {
 
 romap_status romap_ctx_destroy(romap_ctx* ctx) {
     if (!ctx) return fail(ROMAP_E_INVALID, "null context");
+    if (ctx->async) romap_async_stop(ctx, 0, nullptr);
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->st);
     for (auto& kv : ctx->objs) free_object(ctx, kv.second);
@@ -966,6 +1000,126 @@ romap_status romap_train_pending(romap_ctx* ctx, int32_t chunk, int32_t max_iter
         ++k;
     }
     *n_out = k;
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// f3 asynchronous online trainer (the SLAM side hands frames to
+// the training side and is never blocked by it).  romap_async_offer copies the
+// frame into a bounded queue and returns at once; the worker thread takes queued
+// frames through the Eq. 5 gate and, when the queue is empty, trains pending
+// budgets one chunk at a time.
+static void async_worker(romap_ctx* ctx) {
+    t_async_worker = true;
+    AsyncState* as = ctx->async;
+    cudaSetDevice(ctx->device);
+    for (;;) {
+        AsyncFrame fr;
+        bool have = false, train = false;
+        {
+            std::unique_lock<std::mutex> lk(as->mu);
+            for (;;) {
+                if (!as->queue.empty()) {
+                    fr = std::move(as->queue.front());
+                    as->queue.pop_front();
+                    have = true;
+                    break;
+                }
+                bool pending = false;
+                for (auto& kv : ctx->objs) pending |= kv.second->pending_iters > 0 && !kv.second->kfs.empty();
+                if (pending && (!as->stop || as->finish)) { train = true; break; }
+                if (as->stop) return;
+                as->cv.wait_for(lk, std::chrono::milliseconds(2));
+            }
+        }
+        romap_status st = ROMAP_OK;
+        if (have) {
+            int32_t acc = 0;
+            st = romap_offer_observation(ctx, fr.obj, fr.rgb.data(), fr.mask.data(), fr.T, &fr.K, nullptr, 0,
+                                         as->alpha_deg, as->iters_per_update, &acc, nullptr);
+            std::lock_guard<std::mutex> lk(as->mu);
+            as->accepted += acc;
+        } else if (train) {
+            std::vector<int32_t> ids(ctx->objs.size() + 1), its(ctx->objs.size() + 1);
+            int32_t n = 0;
+            st = romap_train_pending(ctx, as->chunk, as->chunk, ids.data(), its.data(), (int32_t)ids.size(), &n);
+            long long mx = 0;
+            for (int i = 0; i < n; ++i) mx = std::max<long long>(mx, its[i]);
+            std::lock_guard<std::mutex> lk(as->mu);
+            as->iterations += mx;
+        }
+        if (st) {                                    // record the first error and stop working
+            std::lock_guard<std::mutex> lk(as->mu);
+            if (!as->error) { as->error = st; as->error_msg = g_err; }
+            return;
+        }
+    }
+}
+
+romap_status romap_async_start(romap_ctx* ctx, int32_t chunk, float alpha_deg, int32_t iters_per_update,
+                                int32_t queue_cap) {
+    CHECK_CTX();
+    if (chunk < 1 || !(alpha_deg >= 0.f) || iters_per_update < 0 || queue_cap < 1)
+        return fail(ROMAP_E_INVALID, "bad async parameters");
+    auto* as = new AsyncState();
+    as->chunk = chunk;
+    as->alpha_deg = alpha_deg;
+    as->iters_per_update = iters_per_update;
+    as->cap = queue_cap;
+    ctx->async = as;
+    as->worker = std::thread(async_worker, ctx);
+    return ROMAP_OK;
+}
+
+romap_status romap_async_offer(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
+                               const float T_wc[12], const romap_intrinsics* K, int32_t* queued) {
+    if (!ctx || !ctx->async) return fail(ROMAP_E_STATE, "async worker not running");
+    if (!rgb || !mask || !T_wc || !K || !queued || K->width < 1 || K->height < 1)
+        return fail(ROMAP_E_INVALID, "bad frame");
+    AsyncState* as = ctx->async;
+    const size_t npx = (size_t)K->width * K->height;
+    AsyncFrame fr;
+    fr.obj = obj;
+    fr.rgb.assign(rgb, rgb + 3 * npx);              // the caller's buffers are free on return
+    fr.mask.assign(mask, mask + npx);
+    memcpy(fr.T, T_wc, sizeof fr.T);
+    fr.K = *K;
+    std::lock_guard<std::mutex> lk(as->mu);
+    as->offered++;
+    if ((int)as->queue.size() >= as->cap) {         // never block the producer: drop
+        as->dropped++;
+        *queued = 0;
+        return ROMAP_OK;
+    }
+    as->queue.push_back(std::move(fr));
+    as->max_depth = std::max<long long>(as->max_depth, (long long)as->queue.size());
+    as->cv.notify_one();
+    *queued = 1;
+    return ROMAP_OK;
+}
+
+romap_status romap_async_stop(romap_ctx* ctx, int32_t finish_pending, romap_async_stats* out) {
+    if (!ctx || !ctx->async) return fail(ROMAP_E_STATE, "async worker not running");
+    AsyncState* as = ctx->async;
+    {
+        std::lock_guard<std::mutex> lk(as->mu);
+        as->stop = true;
+        as->finish = finish_pending != 0;
+        as->cv.notify_one();
+    }
+    as->worker.join();
+    ctx->async = nullptr;
+    if (out) {
+        out->offered = as->offered;
+        out->dropped = as->dropped;
+        out->accepted = as->accepted;
+        out->iterations = as->iterations;
+        out->max_queue_depth = as->max_depth;
+    }
+    romap_status err = as->error;
+    std::string msg = as->error_msg;
+    delete as;
+    if (err) return fail(err, "async worker: %s", msg.c_str());
     return ROMAP_OK;
 }
 

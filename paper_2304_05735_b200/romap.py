@@ -104,6 +104,9 @@ _SIGS = {
     "romap_profile_enable": [_P, _I],
     "romap_profile_read": [_P, _P, _I, C.POINTER(_I)],
     "romap_profile_stages": [_P, C.c_uint32],
+    "romap_async_start": [_P, _I, C.c_float, _I, _I],
+    "romap_async_offer": [_P, _I, _P, _P, _P, C.POINTER(Intrinsics), C.POINTER(_I)],
+    "romap_async_stop": [_P, _I, _P],
     "romap_extract_mesh": [_P, _I, _I, C.c_float, _P, C.c_int64, C.POINTER(C.c_int64), _I],
     "romap_offer_observation": [_P, _I, _P, _P, _P, C.POINTER(Intrinsics), _P, _I, C.c_float, _I, C.POINTER(_I),
                                 C.POINTER(C.c_float)],
@@ -254,6 +257,27 @@ class Context:
         _check(_lib.romap_offer_observation(self._h, obj, _ptr(rgb), _ptr(mask), _ptr(T), C.byref(intr), dp, nd,
                                             float(alpha_deg), int(iters_per_update), C.byref(acc), C.byref(alpha)))
         return bool(acc.value), (None if alpha.value < 0 else float(alpha.value))
+
+    # ------------------------------------------------------------- async online trainer (f3)
+    def async_start(self, chunk: int = 100, alpha_deg: float = 25.0, iters_per_update: int = 300,
+                    queue_cap: int = 64):
+        _check(_lib.romap_async_start(self._h, int(chunk), float(alpha_deg), int(iters_per_update), int(queue_cap)))
+
+    def async_offer(self, obj: int, rgb, mask, T_wc, K) -> bool:
+        """Queue a frame for the worker; returns False if the queue was full (dropped)."""
+        rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        mask = np.ascontiguousarray(mask, dtype=np.uint16)
+        T = np.ascontiguousarray(np.asarray(T_wc, dtype=np.float32).reshape(12))
+        H, W = mask.shape
+        intr = Intrinsics(float(K[0]), float(K[1]), float(K[2]), float(K[3]), W, H)
+        q = C.c_int32()
+        _check(_lib.romap_async_offer(self._h, obj, _ptr(rgb), _ptr(mask), _ptr(T), C.byref(intr), C.byref(q)))
+        return bool(q.value)
+
+    def async_stop(self, finish_pending: bool = True) -> dict:
+        st = (C.c_int64 * 5)()
+        _check(_lib.romap_async_stop(self._h, 1 if finish_pending else 0, C.cast(st, C.c_void_p)))
+        return dict(zip(["offered", "dropped", "accepted", "iterations", "max_queue_depth"], list(st)))
 
     def pending_iters(self, obj: int) -> int:
         p = C.c_int64()
