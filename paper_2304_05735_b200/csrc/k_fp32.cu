@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256) k_composite(int N, const RayRec* __restri
                                                    const float* __restrict__ sigma, const float* __restrict__ rgb,
                                                    const float* __restrict__ dist, const float* __restrict__ delta,
                                                    float* __restrict__ out_rgb, float* __restrict__ out_depth,
-                                                   float* __restrict__ out_opa) {
+                                                   float* __restrict__ out_opa, const int* __restrict__ out_idx) {
     const int lane = threadIdx.x & 31;
     const int ray = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (ray >= n_rays) return;
@@ -588,18 +588,39 @@ __global__ void __launch_bounds__(256) k_composite(int N, const RayRec* __restri
         }
     }
     if (lane == 0) {
-        if (out_rgb) { out_rgb[3 * ray] = Cs[0]; out_rgb[3 * ray + 1] = Cs[1]; out_rgb[3 * ray + 2] = Cs[2]; }
-        if (out_depth) out_depth[ray] = D;
-        if (out_opa) out_opa[ray] = A;
+        const int o = out_idx ? out_idx[ray] : ray;     // compacted rays write to their pixel
+        if (out_rgb) { out_rgb[3 * o] = Cs[0]; out_rgb[3 * o + 1] = Cs[1]; out_rgb[3 * o + 2] = Cs[2]; }
+        if (out_depth) out_depth[o] = D;
+        if (out_opa) out_opa[o] = A;
     }
 }
 
 void launch_composite(const LaunchCtx& lc, int N, const RayRec* rays, int n_rays, const float* sigma,
                       const float* rgb, const float* dist, const float* delta, float* out_rgb, float* out_depth,
-                      float* out_opacity) {
+                      float* out_opacity, const int* out_idx) {
     if (n_rays == 0) return;
     k_composite<<<(n_rays + 7) / 8, 256, 0, lc.st>>>(N, rays, n_rays, sigma, rgb, dist, delta, out_rgb, out_depth,
-                                                     out_opacity);
+                                                     out_opacity, out_idx);
+}
+
+// render: the rays that hit the box, packed (order arbitrary; out_idx keeps the pixel)
+__global__ void __launch_bounds__(256) k_compact_rays(const RayRec* __restrict__ rays, int n, RayRec* __restrict__ out,
+                                                      int* __restrict__ idx, int* __restrict__ count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = i < n && (rays[i].flags & RF_ACTIVE);
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    int base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (act) {
+        const int pos = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+        out[pos] = rays[i];
+        idx[pos] = i;
+    }
+}
+
+void launch_compact_rays(const LaunchCtx& lc, const RayRec* rays, int n, RayRec* out, int* idx, int* count) {
+    if (n > 0) k_compact_rays<<<(n + 255) / 256, 256, 0, lc.st>>>(rays, n, out, idx, count);
 }
 
 // ---------------------------------------------------------------------------

@@ -159,6 +159,10 @@ struct romap_ctx {
     unsigned long long* hits_d = nullptr;
     int* nonfinite_d = nullptr;
     size_t stat_cap = 0;
+    RayRec* rays_c = nullptr;    // render: rays that hit the box, packed
+    size_t rays_c_cap = 0;
+    int* ray_idx = nullptr;      // render: pixel of each packed ray (+ the packed count)
+    size_t ray_idx_cap = 0;
     float* scene_d = nullptr;    // render_scene: per object C (rgb), A, D, t_near, HW floats each
     size_t scene_cap = 0;
     float* mesh_d = nullptr;     // extract_mesh: lattice points | sigma | counts | offsets | CUB scratch
@@ -461,6 +465,8 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->samp);
     dfree(ctx, ctx->srec);
     dfree(ctx, ctx->scene_d);
+    dfree(ctx, ctx->rays_c);
+    dfree(ctx, ctx->ray_idx);
     dfree(ctx, ctx->mesh_d);
     dfree(ctx, ctx->tris_d);
     dfree(ctx, ctx->act);
@@ -1174,19 +1180,31 @@ static romap_status render_one(romap_ctx* ctx, Object* ob, const float T_wc[12],
     }
     LaunchCtx lc{ctx->st, ctx->num_sms};
     launch_render_rays(lc, ctx->single_d, ctx->cam_d, W, H, ctx->rays);
+    // only rays that hit the box reach the MLP: pack them (k_compact_rays), composite
+    // writes each packed ray to its pixel, every other pixel stays 0 (over black)
+    if (!grow(ctx, ctx->rays_c, ctx->rays_c_cap, (size_t)HW)) return fail(ROMAP_E_OOM, "ray buffer");
+    if (!grow(ctx, ctx->ray_idx, ctx->ray_idx_cap, (size_t)HW + 1)) return fail(ROMAP_E_OOM, "ray index buffer");
+    int* d_count = ctx->ray_idx + HW;
+    CK(cudaMemsetAsync(d_count, 0, sizeof(int), ctx->st));
+    if (o_rgb) CK(cudaMemsetAsync(o_rgb, 0, HW * 3 * 4, ctx->st));
+    if (o_dep) CK(cudaMemsetAsync(o_dep, 0, HW * 4, ctx->st));
+    if (o_opa) CK(cudaMemsetAsync(o_opa, 0, HW * 4, ctx->st));
+    launch_compact_rays(lc, ctx->rays, (int)HW, ctx->rays_c, ctx->ray_idx, d_count);
+    int n_act = 0;
+    CK(cudaMemcpyAsync(&n_act, d_count, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
     float* sg = ctx->samp;
     float* cl = sg + S;
     float* ds = cl + 3 * S;
     float* dl = ds + S;
-    for (long long r0 = 0; r0 < HW; r0 += chunk) {
-        int nr = (int)(HW - r0 < chunk ? HW - r0 : chunk);
+    for (long long r0 = 0; r0 < n_act; r0 += chunk) {
+        int nr = (int)(n_act - r0 < chunk ? n_act - r0 : chunk);
         // rays of this chunk all belong to slot 0 (ctx->single_d)
         if (ob->cfg.precision == 1)   // mixed objects: fp16 tables / MLP on the tensor cores (k_infer_mixed.cu)
-            launch_fwd_mixed(lc, cfg, ctx->single_d, ctx->rays + r0, nr, sg, cl, ds, dl);
+            launch_fwd_mixed(lc, cfg, ctx->single_d, ctx->rays_c + r0, nr, sg, cl, ds, dl);
         else
-            launch_fwd_fp32(lc, cfg, ctx->single_d, ctx->rays + r0, nr, false, true, sg, cl, ds, dl, nullptr, 0);
-        launch_composite(lc, N, ctx->rays + r0, nr, sg, cl, ds, dl, o_rgb ? o_rgb + 3 * r0 : nullptr,
-                         o_dep ? o_dep + r0 : nullptr, o_opa ? o_opa + r0 : nullptr);
+            launch_fwd_fp32(lc, cfg, ctx->single_d, ctx->rays_c + r0, nr, false, true, sg, cl, ds, dl, nullptr, 0);
+        launch_composite(lc, N, ctx->rays_c + r0, nr, sg, cl, ds, dl, o_rgb, o_dep, o_opa, ctx->ray_idx + r0);
     }
     CK(cudaGetLastError());
     if (!dev) {

@@ -308,7 +308,8 @@ void launch_zero_grads(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj
 void launch_render_rays(const LaunchCtx& lc, const ObjDev* obj, const KfDev* cam, int W, int H, RayRec* rays);
 void launch_composite(const LaunchCtx& lc, int N, const RayRec* rays, int n_rays, const float* sigma,
                       const float* rgb, const float* dist, const float* delta, float* out_rgb, float* out_depth,
-                      float* out_opacity);
+                      float* out_opacity, const int* out_idx = nullptr);
+void launch_compact_rays(const LaunchCtx& lc, const RayRec* rays, int n, RayRec* out, int* idx, int* count);
 void launch_seg_tnear(const LaunchCtx& lc, const RayRec* rays, long long n, float* tn);
 void launch_scene_composite(const LaunchCtx& lc, int n_obj, long long HW, const float* seg, float* rgb, float* depth,
                             float* opa);
