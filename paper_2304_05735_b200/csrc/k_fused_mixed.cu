@@ -494,24 +494,19 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
                         issue = issue && ((lane - run0) & wmask) == 0;
                     }
-                    if (issue) {
 #pragma unroll
-                        for (int p = 0; p < 4; ++p) {
-                            // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
-                            // REDG.F32x4, else two REDG.F32x2
-                            const unsigned ea = es[2 * p], eb = es[2 * p + 1];
-                            if ((ea >> 1) == (eb >> 1)) {
-                                if (ea < eb)
-                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + ea), v[4 * p], v[4 * p + 1],
-                                               v[4 * p + 2], v[4 * p + 3]);
-                                else
-                                    red_add_f4(reinterpret_cast<float4*>(g_m2 + eb), v[4 * p + 2], v[4 * p + 3],
-                                               v[4 * p], v[4 * p + 1]);
-                            } else {
-                                red_add_f2(g_m2 + ea, v[4 * p], v[4 * p + 1]);
-                                red_add_f2(g_m2 + eb, v[4 * p + 2], v[4 * p + 3]);
-                            }
-                        }
+                    for (int p = 0; p < 4; ++p) {
+                        // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
+                        // REDG.F32x4 (lower entry first), else two REDG.F32x2; predicated,
+                        // not branched (every warp has lanes of both kinds)
+                        const unsigned ea = es[2 * p], eb = es[2 * p + 1];
+                        const bool pair = (ea >> 1) == (eb >> 1), a_lo = (ea & 1u) == 0u;
+                        const float4 w4 = a_lo ? make_float4(v[4 * p], v[4 * p + 1], v[4 * p + 2], v[4 * p + 3])
+                                               : make_float4(v[4 * p + 2], v[4 * p + 3], v[4 * p], v[4 * p + 1]);
+                        red_add_f4_if(issue && pair, reinterpret_cast<float4*>(g_m2 + (ea & ~1u)), w4.x, w4.y, w4.z,
+                                      w4.w);
+                        red_add_f2_if(issue && !pair, g_m2 + ea, v[4 * p], v[4 * p + 1]);
+                        red_add_f2_if(issue && !pair, g_m2 + eb, v[4 * p + 2], v[4 * p + 3]);
                     }
                 }
             }
@@ -538,7 +533,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
 #else
                         const bool same = (ea >> 2) == (eb >> 2);
                         const uint32_t h0 = sel4(qv[q][p], ea & 3);
-                        const uint32_t h1 = same ? sel4(qv[q][p], eb & 3) : xv[q][p];
+                        const uint32_t h1 = selp_u32(same, sel4(qv[q][p], eb & 3), xv[q][p]);
 #endif
 #ifndef ROMAP_LERP16
                         // fp32 lerps of the fp16 corners

@@ -227,6 +227,22 @@ __device__ __forceinline__ void red_add_f1(float* p, float a) {
 __device__ __forceinline__ void red_add_f4(float4* p, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
 }
+// predicated forms (one @p REDG each, no branch: the hash-grid scatter issues
+// them for every lane and lets the predicate drop the ones it does not need)
+__device__ __forceinline__ void red_add_f4_if(bool on, float4* p, float a, float b, float c, float d) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.global.add.v4.f32 [%1], {%2, %3, %4, %5};\n}"
+                 :: "r"((int)on), "l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
+}
+__device__ __forceinline__ void red_add_f2_if(bool on, float2* p, float a, float b) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.global.add.v2.f32 [%1], {%2, %3};\n}"
+                 :: "r"((int)on), "l"(p), "f"(a), "f"(b));
+}
+// a when p else b, as one SEL the compiler cannot turn into a branch
+__device__ __forceinline__ uint32_t selp_u32(bool p, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %1, 0;\n selp.b32 %0, %2, %3, q;\n}" : "=r"(r) : "r"((int)p), "r"(a), "r"(b));
+    return r;
+}
 __device__ __forceinline__ uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ uint32_t ldg_u32(const void* p) { return __ldg(reinterpret_cast<const unsigned*>(p)); }
 __device__ __forceinline__ uint32_t sel4(const uint4& q, int k) {
