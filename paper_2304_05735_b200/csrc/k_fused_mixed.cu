@@ -39,6 +39,16 @@ bool fused_mixed_available() { return true; }
 // phase summed over CTAs, read back with romap_debug_fused_prof
 #ifdef ROMAP_FUSED_PROF
 __device__ unsigned long long g_fprof[16];
+__device__ unsigned long long g_cta_ns[2 * 1024];   // per CTA: %globaltimer at entry, at exit (last launch)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+extern "C" __attribute__((visibility("default"))) int romap_debug_fused_cta_ns(unsigned long long* out, int n) {
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpyFromSymbol(out, g_cta_ns, sizeof(unsigned long long) * 2 * (n < 1024 ? n : 1024));
+}
 #define FP_MARK(var) const long long var = clock64()
 #define FP_ACC(slot, a, b) do { if (fp_on) atomicAdd(&g_fprof[slot], (unsigned long long)((b) - (a))); } while (0)
 extern "C" __attribute__((visibility("default"))) int romap_debug_fused_prof(unsigned long long* out, int reset) {
@@ -145,86 +155,88 @@ __device__ __forceinline__ float warp_incl(float x, int sw, int lane) {
     return incl;
 }
 
-// exclusive product scan (transmittance T_i) and the ray total T_N
-__device__ __forceinline__ float m_scan_mul(float x, int N, float* xw, float& total) {
+// all render scans of a tile with ONE cross-warp exchange (Eq. 6 forward and
+// backward).  Per sample i of a ray: T_i (exclusive product of alpha), the ray's
+// T_N, w_i = T_i o_i, the ray sums of w c_k, w dist and sigma, and the exclusive
+// suffix sums suf_k,i = sum_{j>i} w_j q_j, q = (c_0, c_1, c_2, dist).  Within a
+// warp segment everything is computed with the local transmittance T^loc (product
+// restarted at the segment); a ray over several warps (N > 32) then exchanges each
+// warp's segment product A_w and segment sums S_w once: with carry_w = product of
+// A over the ray's earlier warps, T = carry T^loc, w = carry w^loc, ray sum =
+// sum_w carry_w S_w, suffix = carry suf^loc + sum_{later w} carry_w S_w.
+struct RScan {
+    float T, TN, w, sums[5], suf[4];
+};
+__device__ __forceinline__ void m_render_scan(float alpha, float o, bool active, const float c[3], float dist,
+                                              float sig, int N, float* xw, RScan& R) {
     const int lane = threadIdx.x & 31, mw = (threadIdx.x - NG) >> 5;
     const int sw = N < 32 ? N : 32;
-    const float incl = warp_incl<true>(x, sw, lane);
-    float excl = __shfl_up_sync(0xffffffffu, incl, 1, sw);
-    if ((lane & (sw - 1)) == 0) excl = 1.f;
-    if (N <= 32) {
-        total = __shfl_sync(0xffffffffu, incl, sw - 1, sw);
-        return excl;
-    }
-    if (lane == 31) xw[mw * 8 + 0] = incl;
-    tc::bar_sync(BAR_M, NM);
-    const int wpr = N >> 5, w0 = mw - (mw % wpr);
-    float carry = 1.f, tot = 1.f;
-    for (int w = w0; w < w0 + wpr; ++w) {
-        const float v = xw[w * 8 + 0];
-        if (w < mw) carry *= v;
-        tot *= v;
-    }
-    total = tot;
-    return carry * excl;
-}
-
-// ray totals of K values at once (one cross-warp exchange), slots 1..K
-template <int K>
-__device__ __forceinline__ void m_ray_sums(float (&v)[K], int N, float* xw) {
-    const int lane = threadIdx.x & 31, mw = (threadIdx.x - NG) >> 5;
-    const int sw = N < 32 ? N : 32;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1)
-            if (off < sw) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off, sw);
-    if (N <= 32) return;
-    if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < K; ++k) xw[mw * 8 + 1 + k] = v[k];
-    tc::bar_sync(BAR_M, NM);
-    const int wpr = N >> 5, w0 = mw - (mw % wpr);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        float tot = 0.f;
-        for (int w = w0; w < w0 + wpr; ++w) tot += xw[w * 8 + 1 + k];
-        v[k] = tot;
-    }
-}
-
-// two exclusive suffix sums (sum over later samples of the ray), slots 6, 7
-__device__ __forceinline__ void m_suffix2(float x0, float x1, int N, float* xw, float& s0, float& s1) {
-    const int lane = threadIdx.x & 31, mw = (threadIdx.x - NG) >> 5;
-    const int sw = N < 32 ? N : 32;
-    float i0 = x0, i1 = x1;
+    const int sl = lane & (sw - 1);
+    const float incl = warp_incl<true>(alpha, sw, lane);
+    float Tl = __shfl_up_sync(0xffffffffu, incl, 1, sw);
+    if (sl == 0) Tl = 1.f;
+    const float A = __shfl_sync(0xffffffffu, incl, sw - 1, sw);
+    const float wl = active ? Tl * o : 0.f;
+    float qi[4] = {wl * c[0], wl * c[1], wl * c[2], wl * dist};
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         if (off >= sw) break;
-        const float y0 = __shfl_down_sync(0xffffffffu, i0, off, sw);
-        const float y1 = __shfl_down_sync(0xffffffffu, i1, off, sw);
-        if ((lane & (sw - 1)) + off < sw) {
-            i0 += y0;
-            i1 += y1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float y = __shfl_down_sync(0xffffffffu, qi[k], off, sw);
+            if (sl + off < sw) qi[k] += y;
         }
     }
-    float e0 = __shfl_down_sync(0xffffffffu, i0, 1, sw);
-    float e1 = __shfl_down_sync(0xffffffffu, i1, 1, sw);
-    if ((lane & (sw - 1)) == sw - 1) e0 = e1 = 0.f;
-    if (N > 32) {
-        if (lane == 0) {
-            xw[mw * 8 + 6] = i0;
-            xw[mw * 8 + 7] = i1;
-        }
-        tc::bar_sync(BAR_M, NM);
-        const int wpr = N >> 5, w0 = mw - (mw % wpr);
-        for (int w = mw + 1; w < w0 + wpr; ++w) {
-            e0 += xw[w * 8 + 6];
-            e1 += xw[w * 8 + 7];
-        }
+    float qe[4], qt[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        qe[k] = __shfl_down_sync(0xffffffffu, qi[k], 1, sw);
+        if (sl == sw - 1) qe[k] = 0.f;
+        qt[k] = __shfl_sync(0xffffffffu, qi[k], 0, sw);
     }
-    s0 = e0;
-    s1 = e1;
+    float ss = sig;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+        if (off < sw) ss += __shfl_xor_sync(0xffffffffu, ss, off, sw);
+    if (N <= 32) {
+        R.T = Tl;
+        R.TN = A;
+        R.w = wl;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            R.sums[k] = qt[k];
+            R.suf[k] = qe[k];
+        }
+        R.sums[4] = ss;
+        return;
+    }
+    if (lane == 0) {
+        xw[mw * 8 + 0] = A;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xw[mw * 8 + 1 + k] = qt[k];
+        xw[mw * 8 + 5] = ss;
+    }
+    tc::bar_sync(BAR_M, NM);
+    const int wpr = N >> 5, w0 = mw - (mw % wpr);
+    float carry = 1.f, cw = 1.f, later[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) R.sums[k] = 0.f;
+    for (int w = w0; w < w0 + wpr; ++w) {
+        if (w == mw) carry = cw;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float v = cw * xw[w * 8 + 1 + k];
+            R.sums[k] += v;
+            if (w > mw) later[k] += v;
+        }
+        R.sums[4] += xw[w * 8 + 5];
+        cw *= xw[w * 8 + 0];
+    }
+    R.TN = cw;
+    R.T = carry * Tl;
+    R.w = carry * wl;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) R.suf[k] = carry * qe[k] + later[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -357,6 +369,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     const unsigned hmask = (unsigned)cfg.T - 1u;
     const float inv_scale = 1.0f / cfg.loss_scale;
     const uint32_t df_lane = tc::taddr(tm, q4 * 32, TM_DF);
+    const unsigned ray_key = (unsigned)(lane / N) << 24;   // ray of this lane within the warp (N = 2^k)
 
     // tile j of this CTA = tile0 + j * tstride (strided over the grid: all CTAs
     // work on neighbouring tiles, i.e. on the same object, at any time)
@@ -472,7 +485,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         // contiguous run of samples, so equal keys are contiguous lanes
                         // (with N < 32 several rays share a warp and may cross the same cell)
                         const unsigned key = as_ ? ((unsigned)cs.c[0] | ((unsigned)cs.c[1] << 8) |
-                                                    ((unsigned)cs.c[2] << 16) | ((unsigned)(lane / N) << 24))
+                                                    ((unsigned)cs.c[2] << 16) | ray_key)
                                                  : (0x80000000u | (unsigned)lane);
                         const int omax = P[q].x < MERGE8_RES ? 4 : 2;
                         const unsigned wmask = 2u * omax - 1u;
@@ -815,16 +828,13 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         const float x = active ? sigma * delta : 0.f;
         const float alpha = expf(-x);
         const float o = -expm1f(-x);
-        float TN;
         FP_MARK(m_r0);
-        const float Ti = m_scan_mul(alpha, N, xw, TN);
-        FP_MARK(m_r1);
-        FP_ACC(11, m_r0, m_r1);
-        const float w = active ? Ti * o : 0.f;
-        float sums[5] = {w * c[0], w * c[1], w * c[2], w * dist, active ? sigma : 0.f};
-        m_ray_sums<5>(sums, N, xw);
+        RScan R;
+        m_render_scan(alpha, o, active, c, dist, active ? sigma : 0.f, N, xw, R);
+        const float Ti = R.T, TN = R.TN, w = R.w;
+        const float* sums = R.sums;
         FP_MARK(m_r2);
-        FP_ACC(12, m_r1, m_r2);
+        FP_ACC(12, m_r0, m_r2);
         float dsig = 0.f, dcol[3] = {0.f, 0.f, 0.f};
         float gC[3] = {0.f, 0.f, 0.f};
         float gD = 0.f, gCb = 0.f;
@@ -854,12 +864,10 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             }
         }
         const float gc = gC[0] * c[0] + gC[1] * c[1] + gC[2] * c[2];
-        float S, Sd;
+        // S = sum_{j>i} w_j gc_j = gC . suf(c), Sd = sum_{j>i} w_j dist_j (gC is per ray)
+        const float S = gC[0] * R.suf[0] + gC[1] * R.suf[1] + gC[2] * R.suf[2], Sd = R.suf[3];
         FP_MARK(m_r3);
         FP_ACC(13, m_r2, m_r3);
-        m_suffix2(w * gc, w * dist, N, xw, S, Sd);
-        FP_MARK(m_r4);
-        FP_ACC(14, m_r3, m_r4);
         if (active) {
             const float Tn1 = Ti * alpha;
             dsig = delta * (Tn1 * gc - S - TN * gCb) + delta * gD * (Tn1 * dist - Sd) +
@@ -1017,6 +1025,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         FP_ACC(3, m_t3, m_t4);
         FP_ACC(4, m_t4, m_t5);
     }
+    FP_MARK(m_fl0);
     if (cur >= 0) {
         tc::mbar_wait(&misc->tile_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
         tc::fence_after();
@@ -1024,6 +1033,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     }
     FP_MARK(m_end);
     FP_ACC(0, m_start, m_end);
+    FP_ACC(15, m_fl0, m_end);
 }
 
 }  // namespace
@@ -1038,6 +1048,13 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     extern __shared__ __align__(1024) uint8_t smem[];
     Misc* misc = reinterpret_cast<Misc*>(smem + OFF_MISC);
     const int t = threadIdx.x, warp = t >> 5;
+#ifdef ROMAP_FUSED_PROF
+    const bool fp_on = t == 0;
+#endif
+    FP_MARK(cta_start);
+#ifdef ROMAP_FUSED_PROF
+    if (t == 0 && blockIdx.x < 1024) g_cta_ns[2 * blockIdx.x] = gtimer();
+#endif
     if (warp == 0) tc::tmem_alloc(&misc->tmem, TM_COLS);
     if (t == 32) {
         tc::mbar_init(&misc->mbar_mma, 1);
@@ -1056,6 +1073,8 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    FP_MARK(cta_setup);
+    FP_ACC(5, cta_start, cta_setup);
     const uint32_t tm = misc->tmem;
     const int tile0 = blockIdx.x, tstride = gridDim.x;
     const int n = tile0 < n_tiles ? (n_tiles - 1 - tile0) / tstride + 1 : 0;
@@ -1067,6 +1086,11 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     }
     tc::fence_before();
     __syncthreads();
+    FP_MARK(cta_end);
+    FP_ACC(7, cta_start, cta_end);
+#ifdef ROMAP_FUSED_PROF
+    if (t == 0 && blockIdx.x < 1024) g_cta_ns[2 * blockIdx.x + 1] = gtimer();
+#endif
     if (warp == 0) tc::tmem_dealloc(tm, TM_COLS);
 }
 

@@ -29,8 +29,23 @@ fn(buf, 1)
 v = list(buf)
 tiles = 4096 * 64 // 128 * iters
 ctas = 148 * iters
-names = {0: "M total", 1: "M wait x0_full", 2: "M fwd chain", 3: "M render", 4: "M bwd chain", 6: "M tile top", 11: "  render T scan", 12: "  render sums", 13: "  render loss", 14: "  render suffix",
+names = {5: "CTA setup", 7: "CTA total", 15: "M final flush", 0: "M total", 1: "M wait x0_full", 2: "M fwd chain", 3: "M render", 4: "M bwd chain", 6: "M tile top", 12: "  render scans", 13: "  render loss",
          8: "G total (per WG)", 9: "G wait tile_done", 10: "G level loop"}
 for k, n in names.items():
-    per = v[k] / (2 * tiles if k >= 8 else tiles)
-    print(f"{n:20s} {per:10.0f} cycles/tile   ({v[k] / ctas / 1965:.1f} us per CTA-iteration{' per WG' if k >= 8 else ''})")
+    per = v[k] / (2 * tiles if 8 <= k <= 10 else tiles)
+    print(f"{n:20s} {per:10.0f} cycles/tile   ({v[k] / ctas / 1965:.1f} us per CTA-iteration{' per WG' if 8 <= k <= 10 else ''})")
+
+# CTA lifetimes of the last launch (%globaltimer, ns)
+fc = lib.romap_debug_fused_cta_ns
+fc.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+nb = 148
+cb = (C.c_ulonglong * (2 * nb))()
+fc(cb, nb)
+st = [cb[2 * i] for i in range(nb)]
+en = [cb[2 * i + 1] for i in range(nb)]
+t0 = min(st)
+life = sorted(e - s for s, e in zip(st, en))
+print(f"last launch: span {(max(en) - t0) / 1e3:.1f} us, CTA start skew {(max(st) - t0) / 1e3:.2f} us, "
+      f"lifetime min/median/max {life[0] / 1e3:.1f}/{life[nb // 2] / 1e3:.1f}/{life[-1] / 1e3:.1f} us")
+ends = sorted((e - t0) / 1e3 for e in en)
+print("CTA end times (us) deciles:", [round(ends[min(nb - 1, i * nb // 10)], 1) for i in range(11)])
