@@ -479,7 +479,9 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         v[4 * p + 2] = wb * g0;
                         v[4 * p + 3] = wb * g1;
                     }
-                    bool issue = as_;
+                    // fine levels: every lane issues (an inactive sample adds zeros: one
+                    // request, no branch); coarse levels: the run leaders of active samples
+                    bool issue = true;
                     if (P[q].x < MERGE_RES) {                     // warp-uniform
                         // key = (ray of the warp, cell): a straight ray visits each cell in one
                         // contiguous run of samples, so equal keys are contiguous lanes
@@ -505,21 +507,23 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const unsigned kp = __shfl_up_sync(0xffffffffu, key, 1);
                         const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || kp != key);
                         const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
-                        issue = issue && ((lane - run0) & wmask) == 0;
+                        issue = as_ && ((lane - run0) & wmask) == 0;
                     }
+                    if (issue) {
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
-                        // x-neighbour pair in one aligned 16-B pair of fp32 entries -> one
-                        // REDG.F32x4 (lower entry first), else two REDG.F32x2; predicated,
-                        // not branched (every warp has lanes of both kinds)
+                        // one REDG.F32x4 at the aligned 16-B pair of fp32 entries holding the
+                        // base corner (its x-neighbour's slot carries the neighbour's values when
+                        // it shares the pair, else zeros), plus a REDG.F32x2 for a neighbour
+                        // outside the pair; only that one is conditional
                         const unsigned ea = es[2 * p], eb = es[2 * p + 1];
                         const bool pair = (ea >> 1) == (eb >> 1), a_lo = (ea & 1u) == 0u;
-                        const float4 w4 = a_lo ? make_float4(v[4 * p], v[4 * p + 1], v[4 * p + 2], v[4 * p + 3])
-                                               : make_float4(v[4 * p + 2], v[4 * p + 3], v[4 * p], v[4 * p + 1]);
-                        red_add_f4_if(issue && pair, reinterpret_cast<float4*>(g_m2 + (ea & ~1u)), w4.x, w4.y, w4.z,
-                                      w4.w);
-                        red_add_f2_if(issue && !pair, g_m2 + ea, v[4 * p], v[4 * p + 1]);
-                        red_add_f2_if(issue && !pair, g_m2 + eb, v[4 * p + 2], v[4 * p + 3]);
+                        const float n0 = pair ? v[4 * p + 2] : 0.f, n1 = pair ? v[4 * p + 3] : 0.f;
+                        const float4 w4 = a_lo ? make_float4(v[4 * p], v[4 * p + 1], n0, n1)
+                                               : make_float4(n0, n1, v[4 * p], v[4 * p + 1]);
+                        red_add_f4(reinterpret_cast<float4*>(g_m2 + (ea & ~1u)), w4.x, w4.y, w4.z, w4.w);
+                        if (!pair) red_add_f2(g_m2 + eb, v[4 * p + 2], v[4 * p + 3]);
+                    }
                     }
                 }
             }
