@@ -4,23 +4,6 @@
 #pragma once
 #include "romap_internal.cuh"
 
-// 32-byte gather (LDG.E.256) of 8 table words, zeros when !on
-__device__ __forceinline__ void ldg_v8(const uint32_t* p, bool on, uint32_t (&w)[8]) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = 0u;
-    if (on)
-        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-                     : "l"(p));
-}
-// word k (0..7) of 8 by a 3-level select tree
-__device__ __forceinline__ uint32_t sel8(const uint32_t (&w)[8], unsigned k) {
-    const bool b0 = k & 1u, b1 = k & 2u, b2 = k & 4u;
-    const uint32_t a0 = b0 ? w[1] : w[0], a1 = b0 ? w[3] : w[2], a2 = b0 ? w[5] : w[4], a3 = b0 ? w[7] : w[6];
-    const uint32_t c0 = b1 ? a1 : a0, c1 = b1 ? a3 : a2;
-    return b2 ? c1 : c0;
-}
-
 // cell and the 8 corner entries of one level (R5), as absolute entry indices
 // (level offset `off` added): P = {res, y multiplier, z multiplier, dense};
 // dense: x + (N+1) y + (N+1)^2 z; hashed: (x * 1 ^ y * 2654435761 ^
@@ -70,12 +53,13 @@ __device__ __forceinline__ void encode_pair_fp16(const uint32_t* __restrict__ ta
     Cell cl[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        level_entries(u, P[q], off[q], hmask, cl[q], e[q]);
+        level_entries(u, P[q], 0u, hmask, cl[q], e[q]);    // level-relative; block at tab + off (R5)
+        const uint32_t* tl = tab + off[q];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
             const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
-            qv[q][p] = on ? ldg_v4(tab + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
-            xv[q][p] = (on && !same) ? ldg_u32(tab + e[q][2 * p + 1]) : 0u;
+            qv[q][p] = on ? ldg_v4(tl + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+            xv[q][p] = (on && !same) ? ldg_u32(tl + e[q][2 * p + 1]) : 0u;
         }
     }
 #pragma unroll

@@ -67,8 +67,43 @@ extern "C" __attribute__((visibility("default"))) int romap_debug_fused_prof(uns
 
 namespace {
 
+// experiment hooks (timing only, wrong results): -DROMAP_EXP_NORED drops the
+// scatter REDs, -DROMAP_EXP_NOLDG the gathers; operands stay live via empty asm
+#ifdef ROMAP_EXP_NORED
+__device__ __forceinline__ void xred4(float4* p, float a, float b, float c, float d) {
+    asm volatile("" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
+}
+__device__ __forceinline__ void xred2(float2* p, float a, float b) { asm volatile("" :: "l"(p), "f"(a), "f"(b)); }
+#else
+#define xred4 red_add_f4
+#define xred2 red_add_f2
+#endif
+#ifdef ROMAP_EXP_NOLDG
+__device__ __forceinline__ uint4 xldg4(const void* p) {
+    uint4 v;
+    asm volatile("mov.b64 {%0, %1}, %4;\n mov.b64 {%2, %3}, %4;" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    const uint32_t k = 0x33ff33ffu;             // finite fp16 halves
+    return make_uint4(v.x & k, v.y & k, v.z & k, v.w & k);
+}
+__device__ __forceinline__ uint32_t xldg1(const void* p) {
+    uint32_t v, w;
+    asm volatile("mov.b64 {%0, %1}, %2;" : "=r"(v), "=r"(w) : "l"(p));
+    return (v ^ w) & 0x33ff33ffu;
+}
+#else
+#define xldg4 ldg_v4
+#define xldg1 ldg_u32
+#endif
+
 constexpr int TILE = 128;                      // samples per tile
-constexpr int NGW = 2;                         // gather/scatter warpgroups
+#ifndef ROMAP_NGW
+#define ROMAP_NGW 2
+#endif
+#ifndef ROMAP_LPT
+#define ROMAP_LPT 2
+#endif
+constexpr int NGW = ROMAP_NGW;                 // gather/scatter warpgroups
+constexpr int LPT = ROMAP_LPT;                 // hash levels per trip of a G thread
 constexpr int NG = 128 * NGW;                  // gather/scatter threads
 constexpr int NM = 128;                        // MLP/render threads (M)
 constexpr int NT = NG + NM;
@@ -374,7 +409,8 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     // tile j of this CTA = tile0 + j * tstride (strided over the grid: all CTAs
     // work on neighbouring tiles, i.e. on the same object, at any time)
     float4 u_next = srec[(long long)tile0 * TILE + r];
-    int slot_next = rays[(int)(((long long)tile0 * TILE) / N)].slot;
+    const int lgN = __ffs(N) - 1;                      // N is a power of two (romap_create_object)
+    int slot_next = rays[(int)(((long long)tile0 * TILE) >> lgN)].slot;
     int slot_tab = -1;
     const uint32_t* tab = nullptr;                // fp16 table: one 4-byte (half2) word per entry
     float2* g_cur = nullptr;
@@ -389,12 +425,13 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     for (int it = 0; it < n + 2; ++it) {
         const bool dg = it < n, ds = it >= 2;
         const int b = it & 1;
+        const bool ag = u_next.x >= 0.f;              // sample of an active ray (k_raygen_samples)
         const float ug[3] = {u_next.x, u_next.y, u_next.z};
         const int slot_g = slot_next;
         if (it + 1 < n) {
             const long long tn = (long long)tile0 + (long long)(it + 1) * tstride;
             u_next = srec[tn * TILE + r];
-            slot_next = rays[(int)((tn * TILE) / N)].slot;
+            slot_next = rays[(int)((tn * TILE) >> lgN)].slot;
         }
         if (dg && slot_g != slot_tab) {
             tab = reinterpret_cast<const uint32_t*>(objs[slot_g].p16);
@@ -408,52 +445,46 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
         }
         FP_MARK(g_w1);
         FP_ACC(9, g_w0, g_w1);
-#ifdef ROMAP_EXP_NOG
-        const bool ag = false, as = false;            // experiment: G without memory traffic
-#else
-        const bool ag = dg && ug[0] >= 0.f;          // sample of an active ray (k_raygen_samples)
-        const bool as = ds && um2[0] >= 0.f;
-#endif
-        const unsigned flags_it = (dg ? 1u : 0u) | (ds ? 2u : 0u) | (ag ? 4u : 0u) | (as ? 8u : 0u);
+        const bool as = ds && um2[0] >= 0.f;          // scattered sample of an active ray
+        const unsigned flags_it = (dg ? 1u : 0u) | (ds ? 2u : 0u) | (dg && ag ? 4u : 0u) | (as ? 8u : 0u);
         uint8_t* X0 = smem + OFF_X0 + b * X0_BYTES;
 #pragma unroll 1
-        for (int pp = WG; pp < L / 2; pp += NGW) {   // level pairs of this warpgroup
+        for (int pp = WG; pp < L / LPT; pp += NGW) {   // level groups (LPT levels) of this warpgroup
             // opaque copy of the iteration flags: keeps the compiler from
             // unswitching this loop into one copy per flag combination
             unsigned fl;
             asm volatile("mov.b32 %0, %1;" : "=r"(fl) : "r"(flags_it));
             const bool dg_ = fl & 1u, ds_ = fl & 2u, ag_ = fl & 4u, as_ = fl & 8u;
-            const int l = 2 * pp;
-            const int4 P[2] = {misc->lv[l], misc->lv[l + 1]};
-            const unsigned off[2] = {(unsigned)misc->lvoff[l], (unsigned)misc->lvoff[l + 1]};
+            const int l = LPT * pp;
+            int4 P[LPT];
+            unsigned off[LPT];
+#pragma unroll
+            for (int q = 0; q < LPT; ++q) {
+                P[q] = misc->lv[l + q];
+                off[q] = (unsigned)misc->lvoff[l + q];
+            }
             // (1) gathers of levels l, l+1 of tile it.  x-neighbour corners (b, b|1)
             // share a 16-byte chunk of the fp16 table in 3 of 4 cases (dense:
             // entries e, e+1; hashed: e ^ (x ^ (x+1)) with the x prime = 1), so each
             // corner pair is one 16-B gather (+ a 4-B one otherwise); level blocks
             // are 16-entry aligned (R5).
-#ifdef ROMAP_LDG256
-            // 32-byte gathers: the aligned 8-entry group holds the x-neighbour in
-            // 7 of 8 cases (hashed: e ^ 1, e ^ 3, e ^ 7; dense: e + 1)
-            uint32_t qw[2][4][8];
-#else
-            uint4 qv[2][4];
-#endif
-            uint32_t xv[2][4];
-            unsigned e[2][8];
-            Cell cl[2];
+            uint4 qv[LPT][4];
+            uint32_t xv[LPT][4];
+            unsigned e[LPT][8];
+            Cell cl[LPT];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                level_entries(ug, P[q], off[q], hmask, cl[q], e[q]);
+            for (int q = 0; q < LPT; ++q) {
+                // level-relative entries; the level's block starts at tab + off
+                // (16-entry aligned, R5, so chunk / pair alignment is the same)
+                level_entries(ug, P[q], 0u, hmask, cl[q], e[q]);
+                const uint32_t* tl = tab + off[q];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
-#ifdef ROMAP_LDG256
-                    const bool same = (e[q][2 * p] >> 3) == (e[q][2 * p + 1] >> 3);
-                    ldg_v8(tab + (e[q][2 * p] & ~7u), ag_, qw[q][p]);
-#else
                     const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
-                    qv[q][p] = ag_ ? ldg_v4(tab + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
-#endif
-                    xv[q][p] = (ag_ && !same) ? ldg_u32(tab + e[q][2 * p + 1]) : 0u;
+                    // inactive samples (u = -1) read zeros: bounded features for their
+                    // (masked) MLP rows
+                    qv[q][p] = ag_ ? xldg4(tl + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+                    xv[q][p] = (ag_ && !same) ? xldg1(tl + e[q][2 * p + 1]) : 0u;
                 }
             }
             // (2) scatter of the same levels of tile it-2 (fire-and-forget REDs).
@@ -465,10 +496,11 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                 float g[4];
                 tc::tmem_ld4_sync(df_lane + 32 * b + 2 * l, g);
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
+                for (int q = 0; q < LPT; ++q) {
                     Cell cs;
                     unsigned es[8];
-                    level_entries(um2, P[q], off[q], hmask, cs, es);
+                    level_entries(um2, P[q], 0u, hmask, cs, es);
+                    float2* gl = g_m2 + off[q];
                     const float g0 = as_ ? g[2 * q] * inv_scale : 0.f, g1 = as_ ? g[2 * q + 1] * inv_scale : 0.f;
                     float v[16];
 #pragma unroll
@@ -521,8 +553,8 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const float n0 = pair ? v[4 * p + 2] : 0.f, n1 = pair ? v[4 * p + 3] : 0.f;
                         const float4 w4 = a_lo ? make_float4(v[4 * p], v[4 * p + 1], n0, n1)
                                                : make_float4(n0, n1, v[4 * p], v[4 * p + 1]);
-                        red_add_f4(reinterpret_cast<float4*>(g_m2 + (ea & ~1u)), w4.x, w4.y, w4.z, w4.w);
-                        if (!pair) red_add_f2(g_m2 + eb, v[4 * p + 2], v[4 * p + 3]);
+                        xred4(reinterpret_cast<float4*>(gl + (ea & ~1u)), w4.x, w4.y, w4.z, w4.w);
+                        if (!pair) xred2(gl + eb, v[4 * p + 2], v[4 * p + 3]);
                     }
                     }
                 }
@@ -531,9 +563,9 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             // then z lerps in fp32 (-DROMAP_LERP16: packed-fp16 lerps, 2 % faster,
             // ~25 % larger first-layer / table gradient error) -> fp16 X0[b]
             if (dg_) {
-                __half2 fq[2];
+                __half2 fq[LPT];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
+                for (int q = 0; q < LPT; ++q) {
                     const __half2 fx = __float2half2_rn(cl[q].f[0]), fy = __float2half2_rn(cl[q].f[1]),
                                   fz = __float2half2_rn(cl[q].f[2]);
                     __half2 vx[4];
@@ -543,15 +575,9 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
                         const unsigned ea = e[q][2 * p], eb = e[q][2 * p + 1];
-#ifdef ROMAP_LDG256
-                        const bool same = (ea >> 3) == (eb >> 3);
-                        const uint32_t h0 = sel8(qw[q][p], ea & 7);
-                        const uint32_t h1 = same ? sel8(qw[q][p], eb & 7) : xv[q][p];
-#else
                         const bool same = (ea >> 2) == (eb >> 2);
                         const uint32_t h0 = sel4(qv[q][p], ea & 3);
                         const uint32_t h1 = selp_u32(same, sel4(qv[q][p], eb & 3), xv[q][p]);
-#endif
 #ifndef ROMAP_LERP16
                         // fp32 lerps of the fp16 corners
                         const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h0));
@@ -574,7 +600,10 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                     fq[q] = __hfma2(fz, __hsub2(vy1, vy0), vy0);
 #endif
                 }
-                *reinterpret_cast<uint2*>(X0 + tc::il_offset(r, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
+                if constexpr (LPT == 2)
+                    *reinterpret_cast<uint2*>(X0 + tc::il_offset(r, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
+                else
+                    *reinterpret_cast<__half2*>(X0 + tc::il_offset(r, 2 * l, LF)) = fq[0];
             }
         }
         if (ds) {                                     // DF[b] read: M may overwrite it (tile it)
@@ -590,7 +619,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             um2[k] = um1[k];
-            um1[k] = dg ? ug[k] : -1.f;
+            um1[k] = (dg && ag) ? ug[k] : -1.f;
         }
         g_m2 = g_m1;
         g_m1 = g_cur;
@@ -608,8 +637,8 @@ struct MIn {
     int flags, slot;
 };
 __device__ __forceinline__ MIn m_load(const RayRec* __restrict__ rays, const float4* __restrict__ srec,
-                                      const float* __restrict__ sdelta, long long s, int N) {
-    const RayRec* rp = rays + (int)(s / N);
+                                      const float* __restrict__ sdelta, long long s, int lgN) {
+    const RayRec* rp = rays + (int)(s >> lgN);      // N = 2^lgN samples per ray
     MIn v;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -669,15 +698,16 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     const bool fp_on = m == 0;
 #endif
     FP_MARK(m_start);
-    MIn nx = m_load(rays, srec, sdelta, (long long)tile0 * TILE + m, N);
+    const int lgN = __ffs(N) - 1;                      // N is a power of two (romap_create_object)
+    MIn nx = m_load(rays, srec, sdelta, (long long)tile0 * TILE + m, lgN);
     for (int j = 0; j < n; ++j) {
         FP_MARK(m_t0);
         const long long tile = (long long)tile0 + (long long)j * tstride;
         const int b = j & 1;
         const long long s = (long long)tile * TILE + m;
-        const int i = (int)(s % N);
+        const int i = (int)(s & (N - 1));
         const MIn rr = nx;
-        if (j + 1 < n) nx = m_load(rays, srec, sdelta, s + (long long)tstride * TILE, N);
+        if (j + 1 < n) nx = m_load(rays, srec, sdelta, s + (long long)tstride * TILE, lgN);
         const float delta = rr.delta;
         const bool active = (rr.flags & RF_ACTIVE) != 0;
         if (rr.slot != cur) {                      // uniform: a tile holds rays of one object
