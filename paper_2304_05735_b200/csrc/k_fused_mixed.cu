@@ -18,9 +18,10 @@
 // Pipeline.  G0 / G1 (threads 0-255) own hash levels [0, L/2) / [L/2, L) of
 // sample t % 128; M (threads 256-383) owns the whole MLP / render chain of
 // sample t - 256.  In G iteration `it` the gathers of tile `it` are interleaved,
-// level pair by level pair, with the fire-and-forget scatter of tile `it - 2`,
-// so the REDs fill the gathers' L2 latency; meanwhile M runs tile `it - 1`.
-// Hand-offs are mbarriers in shared memory (two slots, b = tile & 1):
+// level pair by level pair, with the fire-and-forget scatter of tile `it - NB`
+// (NB = 3), so the REDs fill the gathers' L2 latency; meanwhile M runs one of the
+// tiles in between (three slots absorb the tile-to-tile variation of either role).
+// Hand-offs are mbarriers in shared memory (NB slots, b = tile % NB):
 //   x0_full[b]   G -> M   encoded features of the tile are in X0[b]   (8 warp arrivals)
 //   tile_done[b] M -> G   the tile's last MMAs completed: dfeat is in TMEM DF[b]
 //                         and X0[b] is free                           (tcgen05.commit)
@@ -104,6 +105,10 @@ constexpr int TILE = 128;                      // samples per tile
 #endif
 constexpr int NGW = ROMAP_NGW;                 // gather/scatter warpgroups
 constexpr int LPT = ROMAP_LPT;                 // hash levels per trip of a G thread
+#ifndef ROMAP_NB
+#define ROMAP_NB 3
+#endif
+constexpr int NB = ROMAP_NB;                   // G <-> M hand-off slots (X0, DF, barriers)
 constexpr int NG = 128 * NGW;                  // gather/scatter threads
 constexpr int NM = 128;                        // MLP/render threads (M)
 constexpr int NT = NG + NM;
@@ -125,8 +130,8 @@ constexpr int OFF_W4 = OFF_W3 + 64 * 32 * 2;   // 64 x 64
 constexpr int OFF_W5 = OFF_W4 + 64 * 64 * 2;   // 16 x 64 (rows 3..15 zero)
 constexpr int OFF_WH2 = OFF_W5 + 16 * 64 * 2;  // network 1: second 64 x 64 hidden layer
 constexpr int X0_BYTES = TILE * 32 * 2;
-constexpr int OFF_X0 = OFF_WH2 + 64 * 64 * 2;  // 2 slots x 128 x LF
-constexpr int OFF_H1 = OFF_X0 + 2 * X0_BYTES;  // 128 x 64
+constexpr int OFF_X0 = OFF_WH2 + 64 * 64 * 2;  // NB slots x 128 x LF
+constexpr int OFF_H1 = OFF_X0 + NB * X0_BYTES; // 128 x 64
 constexpr int OFF_CIN = OFF_H1 + TILE * 64 * 2;
 constexpr int OFF_G1 = OFF_CIN + TILE * 32 * 2;
 constexpr int OFF_G2 = OFF_G1 + TILE * 64 * 2;
@@ -138,7 +143,7 @@ constexpr int SMEM_BYTES = OFF_MISC + 1024;
 
 // TMEM columns (one CTA per SM, so the whole 512-column allocation is free)
 constexpr int TM_WK = 0;      // working accumulator (<= 64 cols)
-constexpr int TM_DF = 64;     // 2 x 32: dfeat of tile slot b at TM_DF + 32 b
+constexpr int TM_DF = 384;    // NB x 32: dfeat of tile slot b at TM_DF + 32 b
 constexpr int TM_DW1 = 128;   // dW1   [64 x LF]
 constexpr int TM_DW3 = 160;   // dW3   [64 x 32]
 constexpr int TM_DW4 = 192;   // dW4   [64 x 64]
@@ -152,9 +157,9 @@ constexpr int TM_COLS = 512;
 
 struct Misc {
     uint64_t mbar_mma;        // M: completion of its own MMA groups
-    uint64_t x0_full[2];
-    uint64_t tile_done[2];
-    uint64_t df_empty[2];
+    uint64_t x0_full[NB];
+    uint64_t tile_done[NB];
+    uint64_t df_empty[NB];
     uint32_t tmem;
     int pad;
     float loss[4];
@@ -414,17 +419,21 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     int slot_tab = -1;
     const uint32_t* tab = nullptr;                // fp16 table: one 4-byte (half2) word per entry
     float2* g_cur = nullptr;
-    float um1[3] = {-1.f, -1.f, -1.f}, um2[3] = {-1.f, -1.f, -1.f};
-    float2* g_m1 = nullptr;
-    float2* g_m2 = nullptr;
+    float um[NB][3];                              // positions of tiles it-1 .. it-NB (-1: inactive)
+    float2* gm[NB];                               // their gradient tables
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        um[k][0] = um[k][1] = um[k][2] = -1.f;
+        gm[k] = nullptr;
+    }
 
 #ifdef ROMAP_FUSED_PROF
     const bool fp_on = (t & 127) == 0;
 #endif
     FP_MARK(g_start);
-    for (int it = 0; it < n + 2; ++it) {
-        const bool dg = it < n, ds = it >= 2;
-        const int b = it & 1;
+    for (int it = 0; it < n + NB; ++it) {
+        const bool dg = it < n, ds = it >= NB;       // gather tile it, scatter tile it - NB
+        const int b = it % NB;
         const bool ag = u_next.x >= 0.f;              // sample of an active ray (k_raygen_samples)
         const float ug[3] = {u_next.x, u_next.y, u_next.z};
         const int slot_g = slot_next;
@@ -439,13 +448,13 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             slot_tab = slot_g;
         }
         FP_MARK(g_w0);
-        if (ds) {                                     // dfeat of tile it-2 is in DF[b]
-            tc::mbar_wait(&misc->tile_done[b], ((it - 2) >> 1) & 1);
+        if (ds) {                                     // dfeat of tile it-NB is in DF[b], X0[b] is free
+            tc::mbar_wait(&misc->tile_done[b], ((it - NB) / NB) & 1);
             tc::fence_after();
         }
         FP_MARK(g_w1);
         FP_ACC(9, g_w0, g_w1);
-        const bool as = ds && um2[0] >= 0.f;          // scattered sample of an active ray
+        const bool as = ds && um[NB - 1][0] >= 0.f;   // scattered sample of an active ray
         const unsigned flags_it = (dg ? 1u : 0u) | (ds ? 2u : 0u) | (dg && ag ? 4u : 0u) | (as ? 8u : 0u);
         uint8_t* X0 = smem + OFF_X0 + b * X0_BYTES;
 #pragma unroll 1
@@ -499,8 +508,8 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                 for (int q = 0; q < LPT; ++q) {
                     Cell cs;
                     unsigned es[8];
-                    level_entries(um2, P[q], 0u, hmask, cs, es);
-                    float2* gl = g_m2 + off[q];
+                    level_entries(um[NB - 1], P[q], 0u, hmask, cs, es);
+                    float2* gl = gm[NB - 1] + off[q];
                     const float g0 = as_ ? g[2 * q] * inv_scale : 0.f, g1 = as_ ? g[2 * q + 1] * inv_scale : 0.f;
                     float v[16];
 #pragma unroll
@@ -617,12 +626,14 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             if (lane == 0) tc::mbar_arrive(&misc->x0_full[b]);
         }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            um2[k] = um1[k];
-            um1[k] = (dg && ag) ? ug[k] : -1.f;
+        for (int q = NB - 1; q > 0; --q) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) um[q][k] = um[q - 1][k];
+            gm[q] = gm[q - 1];
         }
-        g_m2 = g_m1;
-        g_m1 = g_cur;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) um[0][k] = (dg && ag) ? ug[k] : -1.f;
+        gm[0] = g_cur;
         FP_MARK(g_w2);
         FP_ACC(10, g_w1, g_w2);
     }
@@ -703,7 +714,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     for (int j = 0; j < n; ++j) {
         FP_MARK(m_t0);
         const long long tile = (long long)tile0 + (long long)j * tstride;
-        const int b = j & 1;
+        const int b = j % NB;
         const long long s = (long long)tile * TILE + m;
         const int i = (int)(s & (N - 1));
         const MIn rr = nx;
@@ -713,7 +724,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         if (rr.slot != cur) {                      // uniform: a tile holds rays of one object
             if (cur >= 0) {
                 // every MMA of the previous tile (they read W and write dW) has completed
-                tc::mbar_wait(&misc->tile_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                tc::mbar_wait(&misc->tile_done[(j - 1) % NB], ((j - 1) / NB) & 1);
                 tc::fence_after();
                 m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
             }
@@ -729,11 +740,11 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             tc::st16(CIN, m, 16, 32, sh);
         }
         FP_MARK(m_t1);
-        tc::mbar_wait(&misc->x0_full[b], (j >> 1) & 1);
+        tc::mbar_wait(&misc->x0_full[b], (j / NB) & 1);
         FP_MARK(m_t2);
 #ifdef ROMAP_EXP_NOM
         if (leader) {                                  // experiment: M hands the tile straight back
-            if (j >= 2) tc::mbar_wait(&misc->df_empty[b], ((j - 2) >> 1) & 1);
+            if (j >= NB) tc::mbar_wait(&misc->df_empty[b], ((j - NB) / NB) & 1);
             tc::fence_after();
             tc::commit(&misc->tile_done[b]);
         }
@@ -1039,7 +1050,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         // B1: DF[b][128 x LF] = DB(dh1) . W1[64 x LF];  dW1[64 x LF] += DB^T . X0[b]
         // (DF[b] must have been read by G: scatter of tile j-2)
         if (leader) {
-            if (j >= 2) tc::mbar_wait(&misc->df_empty[b], ((j - 2) >> 1) & 1);
+            if (j >= NB) tc::mbar_wait(&misc->df_empty[b], ((j - NB) / NB) & 1);
             tc::fence_after();
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
@@ -1061,7 +1072,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     }
     FP_MARK(m_fl0);
     if (cur >= 0) {
-        tc::mbar_wait(&misc->tile_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
+        tc::mbar_wait(&misc->tile_done[(n - 1) % NB], ((n - 1) / NB) & 1);
         tc::fence_after();
         m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
     }
@@ -1092,7 +1103,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     if (warp == 0) tc::tmem_alloc(&misc->tmem, TM_COLS);
     if (t == 32) {
         tc::mbar_init(&misc->mbar_mma, 1);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
             tc::mbar_init(&misc->x0_full[b], NG / 32);
             tc::mbar_init(&misc->tile_done[b], 1);
             tc::mbar_init(&misc->df_empty[b], NG / 32);
