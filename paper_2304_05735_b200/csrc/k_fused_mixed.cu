@@ -137,8 +137,9 @@ constexpr int OFF_G1 = OFF_CIN + TILE * 32 * 2;
 constexpr int OFF_G2 = OFF_G1 + TILE * 64 * 2;
 constexpr int OFF_DC = OFF_G2 + TILE * 64 * 2;  // 128 x 16
 constexpr int OFF_DR = OFF_DC + TILE * 16 * 2;  // 128 x 16
-constexpr int OFF_DB = OFF_DR + TILE * 16 * 2;  // 128 x 64 (dg2 -> dg1 -> dh1)
-constexpr int OFF_MISC = OFF_DB + TILE * 64 * 2;
+constexpr int OFF_DB = OFF_DR + TILE * 16 * 2;  // 128 x 64 (dg2, dh1)
+constexpr int OFF_DB2 = OFF_DB + TILE * 64 * 2; // 128 x 64 (dg1): its producer overlaps the dW MMAs reading DB
+constexpr int OFF_MISC = OFF_DB2 + TILE * 64 * 2;
 constexpr int SMEM_BYTES = OFF_MISC + 1024;
 
 // TMEM columns (one CTA per SM, so the whole 512-column allocation is free)
@@ -686,6 +687,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
                    sCIN = tc::smem_u32(smem + OFF_CIN), sG1 = tc::smem_u32(smem + OFF_G1),
                    sG2 = tc::smem_u32(smem + OFF_G2), sDC = tc::smem_u32(smem + OFF_DC),
                    sDR = tc::smem_u32(smem + OFF_DR), sDB = tc::smem_u32(smem + OFF_DB),
+                   sDB2 = tc::smem_u32(smem + OFF_DB2),
                    sWH2 = tc::smem_u32(smem + OFF_WH2);
     uint8_t* H1 = smem + OFF_H1;
     uint8_t* CIN = smem + OFF_CIN;
@@ -694,6 +696,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     uint8_t* DC = smem + OFF_DC;
     uint8_t* DR = smem + OFF_DR;
     uint8_t* DB = smem + OFF_DB;
+    uint8_t* DB2 = smem + OFF_DB2;
     float* xw = &misc->xw[0][0];
     uint32_t phase = 0;
     auto mma_wait = [&]() {
@@ -936,14 +939,17 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         const float dr0_extra = dsig * density_act_grad(r0, sigma, cfg.density_act) * scale;
         m_sync_for_mma();
         // B5: WK[128 x 64] = DC[128 x 16] . W5[16 x 64];  dW5^T[64 x 16] += G2^T . DC
+        // (each stage commits after its dX product: the epilogue overlaps the dW
+        // MMAs, which the next stage's commit covers; no epilogue overwrites an
+        // operand of the dW MMAs still in flight)
         if (leader) {
             tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDC, 16, 0), tc::desc_mnmajor(sW5, 64, 0),
                         tc::idesc_f16(128, 64, false, true), 0);
+            tc::commit(&misc->mbar_mma);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW5, tc::desc_mnmajor(sG2, 64, ks), tc::desc_mnmajor(sDC, 16, ks),
                             tc::idesc_f16(64, 16, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
         epi_mask64(wk, DB, G2, m);
@@ -954,26 +960,26 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             for (int ks = 0; ks < 4; ++ks)
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW4, 64, ks),
                             tc::idesc_f16(128, 64, false, true), ks > 0);
+            tc::commit(&misc->mbar_mma);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW4, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sG1, 64, ks),
                             tc::idesc_f16(64, 64, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
-        epi_mask64(wk, DB, G1, m);
+        epi_mask64(wk, DB2, G1, m);
         m_sync_for_mma();
-        // B3: WK[128 x 16] = DB(dg1) . W3[:, 0:16];  dW3[64 x 32] += DB^T . CIN
+        // B3: WK[128 x 16] = DB2(dg1) . W3[:, 0:16];  dW3[64 x 32] += DB2^T . CIN
         if (leader) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-                tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW3, 32, ks),
+                tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB2, 64, ks), tc::desc_mnmajor(sW3, 32, ks),
                             tc::idesc_f16(128, 16, false, true), ks > 0);
+            tc::commit(&misc->mbar_mma);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-                tc::mma_f16(tm + TM_DW3, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sCIN, 32, ks),
+                tc::mma_f16(tm + TM_DW3, tc::desc_mnmajor(sDB2, 64, ks), tc::desc_mnmajor(sCIN, 32, ks),
                             tc::idesc_f16(64, 32, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
         {
@@ -990,11 +996,11 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
         if (leader) {
             tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDR, 16, 0), tc::desc_mnmajor(sW2, 64, 0),
                         tc::idesc_f16(128, 64, false, true), 0);
+            tc::commit(&misc->mbar_mma);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 tc::mma_f16(tm + TM_DW2, tc::desc_mnmajor(sH1, 64, ks), tc::desc_mnmajor(sDR, 16, ks),
                             tc::idesc_f16(64, 16, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-            tc::commit(&misc->mbar_mma);
         }
         mma_wait();
         epi_mask64(wk, DB, H1, m);
@@ -1017,48 +1023,52 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             if (leader) {
                 tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDC, 16, 0), tc::desc_mnmajor(sW2, 64, 0),
                             tc::idesc_f16(128, 64, false, true), 0);
+                tc::commit(&misc->mbar_mma);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)
                     tc::mma_f16(tm + TM_DW2, tc::desc_mnmajor(sHL, 64, ks), tc::desc_mnmajor(sDC, 16, ks),
                                 tc::idesc_f16(64, 16, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-                tc::commit(&misc->mbar_mma);
             }
             mma_wait();
             epi_mask64(wk, DB, cfg.hl == 1 ? H1 : (cfg.hl == 2 ? G1 : G2), m);
             m_sync_for_mma();
         }
         for (int k = cfg.hl - 1; k >= 1; --k) {
-            // B_k: WK = DB(dh_{k+1}) . W_k;  dW_k[64 x 64] += DB^T . h_k
+            // B_k: WK = D(dh_{k+1}) . W_k;  dW_k[64 x 64] += D^T . h_k  (D alternates DB / DB2)
             const uint32_t sW = k == 1 ? sW4 : sWH2, sHk = k == 1 ? sH1 : sG1;
             const int tdw = k == 1 ? TM_DW4 : TM_DWH2;
+            const bool odd = ((cfg.hl - 1 - k) & 1) != 0;
+            const uint32_t sD = odd ? sDB2 : sDB;
             if (leader) {
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
-                    tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW, 64, ks),
+                    tc::mma_f16(tm + TM_WK, tc::desc_kmajor(sD, 64, ks), tc::desc_mnmajor(sW, 64, ks),
                                 tc::idesc_f16(128, 64, false, true), ks > 0);
+                tc::commit(&misc->mbar_mma);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)
-                    tc::mma_f16(tm + tdw, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sHk, 64, ks),
+                    tc::mma_f16(tm + tdw, tc::desc_mnmajor(sD, 64, ks), tc::desc_mnmajor(sHk, 64, ks),
                                 tc::idesc_f16(64, 64, true, true), (dw_fresh && ks == 0) ? 0 : 1);
-                tc::commit(&misc->mbar_mma);
             }
             mma_wait();
-            epi_mask64(wk, DB, k == 1 ? H1 : G1, m);
+            epi_mask64(wk, odd ? DB : DB2, k == 1 ? H1 : G1, m);
             m_sync_for_mma();
         }
         }
-        // B1: DF[b][128 x LF] = DB(dh1) . W1[64 x LF];  dW1[64 x LF] += DB^T . X0[b]
-        // (DF[b] must have been read by G: scatter of tile j-2)
+        // dh1 for B1: DB (network 0; network 1 after an even number of hidden-layer steps) or DB2
+        const uint32_t sD1 = (NET == 0 || ((cfg.hl - 1) & 1) == 0) ? sDB : sDB2;
+        // B1: DF[b][128 x LF] = D(dh1) . W1[64 x LF];  dW1[64 x LF] += D^T . X0[b]
+        // (DF[b] must have been read by G: scatter of tile j - NB)
         if (leader) {
             if (j >= NB) tc::mbar_wait(&misc->df_empty[b], ((j - NB) / NB) & 1);
             tc::fence_after();
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-                tc::mma_f16(tm + TM_DF + 32 * b, tc::desc_kmajor(sDB, 64, ks), tc::desc_mnmajor(sW1, LF, ks),
+                tc::mma_f16(tm + TM_DF + 32 * b, tc::desc_kmajor(sD1, 64, ks), tc::desc_mnmajor(sW1, LF, ks),
                             tc::idesc_f16(128, LF, false, true), ks > 0);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-                tc::mma_f16(tm + TM_DW1, tc::desc_mnmajor(sDB, 64, ks), tc::desc_mnmajor(sX0, LF, ks),
+                tc::mma_f16(tm + TM_DW1, tc::desc_mnmajor(sD1, 64, ks), tc::desc_mnmajor(sX0, LF, ks),
                             tc::idesc_f16(64, LF, true, true), (dw_fresh && ks == 0) ? 0 : 1);
             tc::commit(&misc->tile_done[b]);
         }
