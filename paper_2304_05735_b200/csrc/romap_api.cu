@@ -101,6 +101,9 @@ struct Profiler {
     double ms[ST_COUNT] = {};
     std::vector<cudaEvent_t> pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<char> pending_shared;  // start event is the previous interval's end (not pooled twice)
+    cudaEvent_t tail = nullptr;        // last end event recorded on the stream ...
+    bool tail_valid = false;           // ... with nothing enqueued after it
     cudaEvent_t get() {
         if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
         cudaEvent_t e;
@@ -183,11 +186,22 @@ struct romap_ctx {
 };
 
 // bracket one launch: stage_begin returns the start event (or null)
+// (back-to-back bracketed launches share one event: the end of one interval is
+// the start of the next, so a timed step carries as few event records as possible)
 static cudaEvent_t stage_begin(romap_ctx* ctx, int stage) {
     ctx->prof.launches[stage]++;
-    if (!ctx->prof.on || !((ctx->prof.mask >> stage) & 1u)) return nullptr;
+    if (!ctx->prof.on || !((ctx->prof.mask >> stage) & 1u)) {
+        ctx->prof.tail_valid = false;           // an unbracketed launch follows
+        return nullptr;
+    }
+    if (ctx->prof.tail_valid) {
+        ctx->prof.tail_valid = false;
+        ctx->prof.pending_shared.push_back(1);
+        return ctx->prof.tail;
+    }
     cudaEvent_t e = ctx->prof.get();
     cudaEventRecord(e, ctx->st);
+    ctx->prof.pending_shared.push_back(0);
     return e;
 }
 static void stage_end(romap_ctx* ctx, int stage, cudaEvent_t e0) {
@@ -195,16 +209,23 @@ static void stage_end(romap_ctx* ctx, int stage, cudaEvent_t e0) {
     cudaEvent_t e1 = ctx->prof.get();
     cudaEventRecord(e1, ctx->st);
     ctx->prof.pending.push_back({stage, {e0, e1}});
+    ctx->prof.tail = e1;
+    ctx->prof.tail_valid = true;
 }
+// anything else enqueued on the stream ends the chain of shared events
+static void stage_break(romap_ctx* ctx) { ctx->prof.tail_valid = false; }
 // after a stream sync: fold pending intervals into the totals
 static void prof_collect(romap_ctx* ctx) {
-    for (auto& p : ctx->prof.pending) {
+    for (size_t i = 0; i < ctx->prof.pending.size(); ++i) {
+        auto& p = ctx->prof.pending[i];
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) ctx->prof.ms[p.first] += ms;
-        ctx->prof.pool.push_back(p.second.first);
+        if (!ctx->prof.pending_shared[i]) ctx->prof.pool.push_back(p.second.first);
         ctx->prof.pool.push_back(p.second.second);
     }
     ctx->prof.pending.clear();
+    ctx->prof.pending_shared.clear();
+    ctx->prof.tail_valid = false;
 }
 #define STAGE(stage, launch)                      \
     do {                                          \
@@ -812,10 +833,12 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     };
     for (int it = 0; it < n_iters; ++it) {
         auto h0 = hnow();
-        if (it == n_iters - 1) CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
+        if (it == n_iters - 1) {
+            CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
+            stage_break(ctx);
+        }
         if (ctx->flush_bytes) {
-            cudaEvent_t e0 = (ctx->prof.on && ((ctx->prof.mask >> ST_FLUSH) & 1u)) ? ctx->prof.get() : nullptr;
-            if (e0) cudaEventRecord(e0, ctx->st);
+            cudaEvent_t e0 = stage_begin(ctx, ST_FLUSH);
             CK(cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st));
             stage_end(ctx, ST_FLUSH, e0);
         }
@@ -825,10 +848,12 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             const int k = it % K;
             float4* srec = reinterpret_cast<float4*>(ctx->srec);
             float* sdelta = ctx->srec + 4 * S * K;
-            if (k == 0)
+            if (k == 0) {
                 STAGE(ST_RAYGEN, launch_raygen_samples(lc, b.cfg, ctx->objdev_d, n, b.total_slots,
                                                        std::min(K, n_iters - it), ctx->rays, srec, sdelta,
                                                        ctx->hits_d));
+                ctx->prof.launches[ST_RAYGEN]++;      // two kernels: k_raygen + k_samples
+            }
             STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays + (size_t)k * b.total_slots,
                                                srec + (size_t)k * S, sdelta + (size_t)k * S, b.total_slots,
                                                ctx->loss_d, ctx->nonfinite_d, adam ? nullptr : ctx->samp));
