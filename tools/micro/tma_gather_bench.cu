@@ -74,6 +74,21 @@ __global__ void k_redh(uint4* tab, uint32_t rows) {
     }
 }
 
+// the fused kernel's mix: one LDG.128 gather (4 MB table) and one RED.v4.f32
+// (8 MB table) per step -- do the two request streams add up or overlap?
+__global__ void k_mix(const uint4* __restrict__ tab, uint32_t rows, float4* tab2, uint32_t* out) {
+    uint32_t acc = 0, seed = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 16
+    for (int i = 0; i < PER / 2; ++i) {
+        const uint32_t h = hsh(seed * PER + i);
+        uint4 v = __ldg(tab + (h % rows));
+        acc += v.x ^ v.w;
+        float4* p = tab2 + (hsh(h) % (2 * rows));
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %1, %1, %1};" :: "l"(p), "f"(1.0f));
+    }
+    if (acc == 0x12345) out[0] = acc;
+}
+
 // TMA gather4: one elected lane per warp issues 32*PER/4 gather4 (same number of
 // 16-B rows as the warp's 32*PER LDGs) into a per-warp smem ring
 __global__ void k_tma_gather(const __grid_constant__ CUtensorMap tm, uint32_t rows, uint32_t* out) {
@@ -137,6 +152,9 @@ int main() {
     void* tab;
     CK(cudaMalloc(&tab, (size_t)rows * 16));
     CK(cudaMemset(tab, 0, (size_t)rows * 16));
+    void* tab2;
+    CK(cudaMalloc(&tab2, (size_t)rows * 32));
+    CK(cudaMemset(tab2, 0, (size_t)rows * 32));
     uint32_t* out;
     CK(cudaMalloc(&out, 16));
     EncodeFn enc = nullptr;
@@ -161,7 +179,7 @@ int main() {
     for (int blocks_per_sm : {2}) {
         const int grid = sms * blocks_per_sm;
         const double acc = accesses * blocks_per_sm;
-        for (int mode = 0; mode < 8; ++mode) {
+        for (int mode = 0; mode < 9; ++mode) {
             float best = 1e30f;
             for (int rep = 0; rep < 5; ++rep) {
                 cudaEventRecord(e0);
@@ -173,6 +191,7 @@ int main() {
                 if (mode == 5) k_ldg32<<<grid, 256>>>((const uint32_t*)tab, rows * 4, out);
                 if (mode == 6) k_red2<<<grid, 256>>>((float2*)tab, rows * 2);
                 if (mode == 7) k_redh<<<grid, 256>>>((uint4*)tab, rows);
+                if (mode == 8) k_mix<<<grid, 256>>>((const uint4*)tab, rows, (float4*)tab2, out);
                 cudaEventRecord(e1);
                 CK(cudaEventSynchronize(e1));
                 float ms;
@@ -180,8 +199,9 @@ int main() {
                 if (ms < best) best = ms;
             }
             CK(cudaGetLastError());
-            const char* names[8] = {"LDG.128 gather", "RED.v4.f32", "TMA gather4", "TMA reduce scatter4",
-                                    "LDG.256 gather", "LDG.32 gather", "RED.v2.f32", "RED.v4.f16x2"};
+            const char* names[9] = {"LDG.128 gather", "RED.v4.f32", "TMA gather4", "TMA reduce scatter4",
+                                    "LDG.256 gather", "LDG.32 gather", "RED.v2.f32", "RED.v4.f16x2",
+                                    "LDG.128 + RED.v4 1:1"};
             double per_cyc = acc / (best * 1e-3) / ((double)clk * 1e3) / sms;
             printf("%d CTA/SM %-20s %8.3f ms  %6.3f accesses/cycle/SM\n", blocks_per_sm, names[mode], best, per_cyc);
         }
