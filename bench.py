@@ -167,6 +167,27 @@ def ncu_traffic(kernel):
         return None
 
 
+# measured ceiling of the fused kernel's request mix (tools/micro/tma_gather_bench.cu,
+# profiles/r1_micro.md): random 16-B LDG.128 gathers + RED.v4.f32 scatters 1:1 over
+# L2-resident tables, per SM and cycle
+REQ_CEILING = 0.828
+
+
+def request_roofline(samples_per_launch, ms, sm_clk, n_sm):
+    """L1 sector requests of the gathers + REDs per SM-cycle against the measured
+    random-access ceiling; sectors per hit sample from the committed ncu capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_requests.json")))
+    except Exception:
+        return None
+    req = d["sectors_per_hit_sample"] * samples_per_launch
+    achieved = req / (ms * 1e-3 * sm_clk * n_sm)
+    return {"bound": "l1_l2_random_requests", "achieved": achieved, "peak": REQ_CEILING,
+            "unit": "sector requests / SM / cycle", "frac": achieved / REQ_CEILING,
+            "source": f"{d['sectors_per_hit_sample']:.1f} sectors per hit sample ({d['profile']}); "
+                      "ceiling tools/micro/tma_gather_bench.cu"}
+
+
 def roofline(prof, kw, precision, samples_per_launch, n_objs):
     peaks, src = load_measured_peaks()
     work = algorithmic_per_sample(kw, precision)
@@ -182,6 +203,11 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
         achieved = bytes_ / (ms * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
         out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s"}
+        # sectors per hit sample were captured on cfg1's model (any number of objects)
+        rq = request_roofline(samples_per_launch, ms, sm_clk, 148) if \
+            {k: v for k, v in kw.items() if not k.startswith("_")} == cfg1_kwargs(1) else None
+        if rq:
+            out["request_roofline"] = rq
     elif dom in ("fwd_fp32", "bwd_fp32"):
         flop = samples_per_launch * (work["mlp_fwd_flop"] if dom == "fwd_fp32" else work["mlp_bwd_flop"])
         achieved = flop / (ms * 1e-3) / 1e12

@@ -19,7 +19,12 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
            "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
-           "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
+           "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+           # request-rate roofline of the hash-grid gathers / scatters
+           "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum",
+           "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+           "lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed",
+           "lts__t_requests_srcunit_ltcfabric.sum", "sm__issue_active.avg.pct_of_peak_sustained_elapsed"]
 
 
 def norm(name):
@@ -65,7 +70,7 @@ def to_bytes(s):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
 
-def main(tag, launch_csv, rep):
+def main(tag, launch_csv, rep, hit_samples=None):
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     L = launches(launch_csv) if launch_csv and os.path.exists(launch_csv) else {}
     F = full(rep) if rep and os.path.exists(rep) else []
@@ -84,6 +89,18 @@ def main(tag, launch_csv, rep):
         md.append("")
         if "dram__bytes_read.sum" in d and d["kernel"] in STAGE:
             traffic[STAGE[d["kernel"]]] = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
+    # L1 sector requests (gathers + REDs) per hit ray-sample of the fused kernel:
+    # bench.py's request roofline
+    fm = [d for d in F if d["kernel"] == "k_fused_mixed" and "l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum" in d]
+    if fm and hit_samples:
+        sec = [float(d["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"].split()[0]) +
+               float(d["l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum"].split()[0]) for d in fm]
+        req = {"kernel": "k_fused_mixed", "profile": f"profiles/{tag}_ncu.json",
+               "sectors_per_launch": sum(sec) / len(sec), "hit_samples_per_launch": float(hit_samples),
+               "sectors_per_hit_sample": sum(sec) / len(sec) / float(hit_samples)}
+        json.dump(req, open(os.path.join(ROOT, "profiles", "ncu_requests.json"), "w"), indent=1)
+        md += ["## request rate", "", f"- L1 sector requests (global ld + red) per hit ray-sample: "
+               f"{req['sectors_per_hit_sample']:.1f}", ""]
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu.md"), "w").write("\n".join(md) + "\n")
     json.dump({"launches": L, "full": F}, open(os.path.join(ROOT, "profiles", f"{tag}_ncu.json"), "w"), indent=1)
     json.dump(traffic, open(traffic_path, "w"), indent=1)
@@ -91,4 +108,6 @@ def main(tag, launch_csv, rep):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, sys.argv[3] if len(sys.argv) > 3 else None)
+    # usage: ncu_summary.py <tag> [launch csv] [ncu-rep] [hit ray-samples per launch of the captured run]
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, sys.argv[3] if len(sys.argv) > 3 else None,
+         sys.argv[4] if len(sys.argv) > 4 else None)
