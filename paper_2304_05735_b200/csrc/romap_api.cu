@@ -183,6 +183,16 @@ struct romap_ctx {
     AsyncState* async = nullptr;    // non-null while the async worker runs
     void* flush_buf = nullptr;
     size_t flush_bytes = 0;
+    // a9: CUDA graph of one chunk of K training iterations of the mixed path
+    // (raygen of K slices, then K x [flush], fused, Adam), replayed while the batch,
+    // its config and every buffer it touches stay the same
+    struct TrainGraph {
+        cudaGraphExec_t exec = nullptr;
+        CfgDev cfg;
+        int n = 0, total_slots = 0, K = 0;
+        const void* ptrs[8] = {};
+        size_t flush_bytes = 0;
+    } tg;
 };
 
 // bracket one launch: stage_begin returns the start event (or null)
@@ -499,6 +509,7 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->nonfinite_d);
     dfree(ctx, ctx->io_d);
     dfree(ctx, ctx->flush_buf);
+    if (ctx->tg.exec) cudaGraphExecDestroy(ctx->tg.exec);
     prof_collect(ctx);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
     delete ctx;
@@ -831,27 +842,27 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
-    for (int it = 0; it < n_iters; ++it) {
+    // one iteration: [loss reset], [L2 flush], (raygen of `kslices` slices when
+    // slice k == 0), forward/backward, Adam
+    auto enqueue_iter = [&](int it, int k, int kslices, bool reset_loss) {
         auto h0 = hnow();
-        if (it == n_iters - 1) {
-            CK(cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st));
+        if (reset_loss) {
+            cudaMemsetAsync(ctx->loss_d, 0, n * 4 * sizeof(double), ctx->st);
             stage_break(ctx);
         }
         if (ctx->flush_bytes) {
             cudaEvent_t e0 = stage_begin(ctx, ST_FLUSH);
-            CK(cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st));
+            cudaMemsetAsync(ctx->flush_buf, it & 0xff, ctx->flush_bytes, ctx->st);
             stage_end(ctx, ST_FLUSH, e0);
         }
         auto h1 = hnow();
         hp[0] += hms(h0, h1);
         if (b.mixed) {
-            const int k = it % K;
             float4* srec = reinterpret_cast<float4*>(ctx->srec);
             float* sdelta = ctx->srec + 4 * S * K;
             if (k == 0) {
-                STAGE(ST_RAYGEN, launch_raygen_samples(lc, b.cfg, ctx->objdev_d, n, b.total_slots,
-                                                       std::min(K, n_iters - it), ctx->rays, srec, sdelta,
-                                                       ctx->hits_d));
+                STAGE(ST_RAYGEN, launch_raygen_samples(lc, b.cfg, ctx->objdev_d, n, b.total_slots, kslices, ctx->rays,
+                                                       srec, sdelta, ctx->hits_d));
                 ctx->prof.launches[ST_RAYGEN]++;      // two kernels: k_raygen + k_samples
             }
             STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays + (size_t)k * b.total_slots,
@@ -869,8 +880,57 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
         auto h2 = hnow();
         hp[1] += hms(h1, h2);
         if (adam) STAGE(ST_ADAM, launch_adam(lc, b.cfg, ctx->objdev_d, n, ctx->nonfinite_d, b.mixed));
-        CK(cudaGetLastError());
         hp[2] += hms(h2, hnow());
+    };
+    // a9: full chunks of K iterations replay one CUDA graph (mixed training, no
+    // per-stage timing events: those need per-launch records); ROMAP_NO_GRAPH=1 off
+    static const bool no_graph = getenv("ROMAP_NO_GRAPH") != nullptr;
+    int it0 = 0;
+    const int n_chunks = (b.mixed && adam && !ctx->prof.on && !no_graph && K >= 2) ? n_iters / K : 0;
+    if (n_chunks > 0) {
+        auto& g = ctx->tg;
+        const void* ptrs[8] = {ctx->objdev_d, ctx->rays, ctx->srec, ctx->loss_d, ctx->hits_d, ctx->nonfinite_d,
+                               ctx->flush_buf, nullptr};
+        const bool same = g.exec && g.n == n && g.total_slots == b.total_slots && g.K == K &&
+                          g.flush_bytes == ctx->flush_bytes && !memcmp(g.ptrs, ptrs, sizeof ptrs) &&
+                          !memcmp(&g.cfg, &b.cfg, sizeof(CfgDev));
+        if (!same) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            g.exec = nullptr;
+            cudaGraph_t graph = nullptr;
+            long long saved[ST_COUNT];                  // capturing is not launching
+            memcpy(saved, ctx->prof.launches, sizeof saved);
+            if (cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                // the loss partials of a call are those of its last iteration: the
+                // chunk resets them before its last iteration
+                for (int k = 0; k < K; ++k) enqueue_iter(k, k, K, k == K - 1);
+                const cudaError_t ec = cudaStreamEndCapture(ctx->st, &graph);
+                if (ec == cudaSuccess && graph && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) g.exec = nullptr;
+                if (graph) cudaGraphDestroy(graph);
+            }
+            cudaGetLastError();                       // a failed capture falls back to plain launches
+            memcpy(ctx->prof.launches, saved, sizeof saved);
+            if (g.exec) {
+                g.cfg = b.cfg;
+                g.n = n;
+                g.total_slots = b.total_slots;
+                g.K = K;
+                g.flush_bytes = ctx->flush_bytes;
+                memcpy(g.ptrs, ptrs, sizeof ptrs);
+            }
+        }
+        if (g.exec) {
+            for (int c = 0; c < n_chunks; ++c) CK(cudaGraphLaunch(g.exec, ctx->st));
+            it0 = n_chunks * K;
+            ctx->prof.launches[ST_RAYGEN] += 2LL * n_chunks;   // (capture counted one chunk already)
+            ctx->prof.launches[ST_FUSED] += (long long)K * n_chunks;
+            ctx->prof.launches[ST_ADAM] += (long long)K * n_chunks;
+            if (ctx->flush_bytes) ctx->prof.launches[ST_FLUSH] += (long long)K * n_chunks;
+        }
+    }
+    for (int it = it0; it < n_iters; ++it) {
+        enqueue_iter(it, it % K, std::min(K, n_iters - it), it == n_iters - 1);
+        CK(cudaGetLastError());
     }
     if (host_prof)
         fprintf(stderr, "[romap host] %d iters: flush %.3f ms, raygen+fused %.3f ms, adam %.3f ms\n", n_iters, hp[0],

@@ -1,0 +1,63 @@
+"""the iteration driver replays a CUDA graph of K training
+iterations (mixed path, timing events off).  A multi-iteration train_step must
+train exactly like K single iterations: the oracle tracks it, and the graph
+replay agrees with plain launches (profiling on disables the graph) up to the
+summation order of the fp32 atomics."""
+import numpy as np
+import pytest
+
+import oracle as O
+import scenes
+from gpu_common import make_pair, norm_rel
+
+pytestmark = pytest.mark.gpu
+
+from paper_2304_05735_b200 import romap as R  # noqa: E402
+
+CFG0M = dict(levels=8, log2_T=12, base_res=16, finest_res=2048.0, res_cap=128, samples_per_ray=32, rays_per_iter=256,
+             precision=1, seed=0)
+
+
+def _scene():
+    return scenes.sphere_scene(0, n_views=8)
+
+
+def test_graph_chunks_track_the_oracle():
+    c = R.Context(0)
+    sc = _scene()
+    h, st = make_pair(R, c, sc, CFG0M)
+    n_iters = 40                                   # 2 graph chunks of 16 + an 8-iteration tail
+    s = c.train_step([h], n_iters)[0]
+    for _ in range(n_iters):
+        o, _, _ = O.train_iteration(st)
+    assert s["step"] == n_iters
+    # losses of the last iteration, 40 Adam steps in: fp16 operands, same samples
+    assert abs(s["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (s, o)
+    t = c.get_params(h, R.BLOCK_TABLE).reshape(-1, 2)
+    assert norm_rel(t, st.params["table"]) < 5e-2
+    c.close()
+
+
+def test_graph_matches_plain_launches():
+    sc = _scene()
+    res = []
+    for plain in (False, True, True):
+        c = R.Context(0)
+        h, _ = make_pair(R, c, sc, CFG0M, param_seed=7)
+        if plain:
+            c.profile_enable(True)                 # per-stage events: no graph
+        s1 = c.train_step([h], 32)[0]              # graph: two chunks
+        s2 = c.train_step([h], 17)[0]              # graph replayed once + 1 plain iteration
+        res.append((s1, s2, c.get_params(h, R.BLOCK_TABLE), c.get_params(h, R.BLOCK_MLP)))
+        c.close()
+    (a1, a2, ta, ma), (b1, b2, tb, mb), (_, _, tc_, mc) = res
+    assert a2["step"] == b2["step"] == 49
+    # same rays and samples (the RNG is keyed by the device step counters)
+    assert a1["hit_rays"] == b1["hit_rays"] and a2["hit_rays"] == b2["hit_rays"]
+    for k in ("l_total", "l_rgb", "l_density"):
+        assert abs(a2[k] - b2[k]) <= 1e-2 * max(abs(b2[k]), 1e-4), (k, a2, b2)
+    # parameters: the fp32 atomics sum in a different order on every run and 49
+    # Adam steps amplify that; graph vs plain must differ no more than plain vs plain
+    d_gp = max(norm_rel(ta, tb), norm_rel(ma, mb))
+    d_pp = max(norm_rel(tc_, tb), norm_rel(mc, mb))
+    assert d_gp <= 2.0 * d_pp + 5e-3, (d_gp, d_pp)
