@@ -385,13 +385,19 @@ __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const uint32_t off = tc::il_offset(r, 32 * h + 8 * c, 64);
+#ifdef ROMAP_EXP_NOMSTS
+            uint4 a4;
+            asm volatile("mov.b32 %0, 0x3c003c00;\n mov.b32 %1, 0;\n mov.b32 %2, 0x3c000000;\n mov.b32 %3, 0x3c00;"
+                         : "=r"(a4.x), "=r"(a4.y), "=r"(a4.z), "=r"(a4.w));
+#else
             uint4 a4 = *reinterpret_cast<const uint4*>(act + off);
+#endif
             const __half2* a = reinterpret_cast<const __half2*>(&a4);
             __half2 q[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 q[k] = __hmul2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), __hgt2(a[k], z));
-            *reinterpret_cast<uint4*>(out + off) = *reinterpret_cast<uint4*>(q);
+            tc::sts128(out + off, *reinterpret_cast<uint4*>(q));
         }
     }
 }
@@ -1121,6 +1127,9 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
         tc::fence_mbar_init();
     }
     if (t < 4) misc->loss[t] = 0.f;
+#ifdef ROMAP_EXP_NOMSTS
+    for (int o = OFF_H1 + 16 * t; o < OFF_MISC; o += 16 * NT) *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
+#endif
     if (t < L) {
         misc->lv[t] = level_params(cfg, t);
         misc->lvoff[t] = cfg.off[t];

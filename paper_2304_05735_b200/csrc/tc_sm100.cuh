@@ -167,12 +167,22 @@ __device__ __forceinline__ uint32_t taddr(uint32_t base, int lane_base, int col)
     return base + ((uint32_t)lane_base << 16) + (uint32_t)col;
 }
 
+// 16-byte shared store (-DROMAP_EXP_NOMSTS, timing experiment only: dropped,
+// operands kept live)
+__device__ __forceinline__ void sts128(void* p, uint4 v) {
+#ifdef ROMAP_EXP_NOMSTS
+    asm volatile("" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+#else
+    *reinterpret_cast<uint4*>(p) = v;
+#endif
+}
+
 // store 8 fp16 (16 B) at an interleaved position (row r, column block starting at c)
 __device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, int C, const float* v8) {
     __half2 h[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v8[2 * i], v8[2 * i + 1]);
-    *reinterpret_cast<uint4*>(buf + il_offset(r, c, C)) = *reinterpret_cast<uint4*>(h);
+    sts128(buf + il_offset(r, c, C), *reinterpret_cast<uint4*>(h));
 }
 
 
@@ -195,7 +205,7 @@ __device__ __forceinline__ void epi_relu64(uint32_t wk, uint8_t* buf, int r) {
             __half2 q[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) q[k] = __hmax2(__floats2half2_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]), z);
-            *reinterpret_cast<uint4*>(buf + il_offset(r, 32 * h + 8 * c, 64)) = *reinterpret_cast<uint4*>(q);
+            sts128(buf + il_offset(r, 32 * h + 8 * c, 64), *reinterpret_cast<uint4*>(q));
         }
     }
 }
