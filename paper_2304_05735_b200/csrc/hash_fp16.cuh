@@ -54,11 +54,11 @@ __device__ __forceinline__ void encode_pair_fp16(const uint32_t* __restrict__ ta
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
         level_entries(u, P[q], 0u, hmask, cl[q], e[q]);    // level-relative; block at tab + off (R5)
-        const uint32_t* tl = tab + off[q];
+        const uint32_t* tl = opaque_ptr(tab + off[q]);
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
             const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
-            qv[q][p] = on ? ldg_v4(tl + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+            qv[q][p] = on ? ldg_v4(tl + opaque_u32(e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
             xv[q][p] = (on && !same) ? ldg_u32(tl + e[q][2 * p + 1]) : 0u;
         }
     }

@@ -493,13 +493,13 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                 // level-relative entries; the level's block starts at tab + off
                 // (16-entry aligned, R5, so chunk / pair alignment is the same)
                 level_entries(ug, P[q], 0u, hmask, cl[q], e[q]);
-                const uint32_t* tl = tab + off[q];
+                const uint32_t* tl = opaque_ptr(tab + off[q]);
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     const bool same = (e[q][2 * p] >> 2) == (e[q][2 * p + 1] >> 2);
                     // inactive samples (u = -1) read zeros: bounded features for their
                     // (masked) MLP rows
-                    qv[q][p] = ag_ ? xldg4(tl + (e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
+                    qv[q][p] = ag_ ? xldg4(tl + opaque_u32(e[q][2 * p] & ~3u)) : make_uint4(0, 0, 0, 0);
                     xv[q][p] = (ag_ && !same) ? xldg1(tl + e[q][2 * p + 1]) : 0u;
                 }
             }
@@ -516,7 +516,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                     Cell cs;
                     unsigned es[8];
                     level_entries(um[NB - 1], P[q], 0u, hmask, cs, es);
-                    float2* gl = gm[NB - 1] + off[q];
+                    float2* gl = opaque_ptr(gm[NB - 1] + off[q]);
                     const float g0 = as_ ? g[2 * q] * inv_scale : 0.f, g1 = as_ ? g[2 * q + 1] * inv_scale : 0.f;
                     float v[16];
 #pragma unroll
@@ -569,7 +569,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const float n0 = pair ? v[4 * p + 2] : 0.f, n1 = pair ? v[4 * p + 3] : 0.f;
                         const float4 w4 = a_lo ? make_float4(v[4 * p], v[4 * p + 1], n0, n1)
                                                : make_float4(n0, n1, v[4 * p], v[4 * p + 1]);
-                        xred4(reinterpret_cast<float4*>(gl + (ea & ~1u)), w4.x, w4.y, w4.z, w4.w);
+                        xred4(reinterpret_cast<float4*>(gl + opaque_u32(ea & ~1u)), w4.x, w4.y, w4.z, w4.w);
                         if (!pair) xred2(gl + eb, v[4 * p + 2], v[4 * p + 3]);
                     }
                     }

@@ -237,6 +237,18 @@ __device__ __forceinline__ void red_add_f2_if(bool on, float2* p, float a, float
     asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.global.add.v2.f32 [%1], {%2, %3};\n}"
                  :: "r"((int)on), "l"(p), "f"(a), "f"(b));
 }
+// the same pointer, opaque to the compiler: addresses p + e then compile to one
+// IMAD.WIDE.U32 each instead of re-associated 64-bit (base + off + e) * 4 chains
+template <typename T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+    unsigned long long v = reinterpret_cast<unsigned long long>(p);
+    asm("mov.b64 %0, %0;" : "+l"(v));
+    return reinterpret_cast<T*>(v);
+}
+__device__ __forceinline__ unsigned opaque_u32(unsigned v) {
+    asm("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
 // a when p else b, as one SEL the compiler cannot turn into a branch
 __device__ __forceinline__ uint32_t selp_u32(bool p, uint32_t a, uint32_t b) {
     uint32_t r;
