@@ -17,11 +17,15 @@
 namespace {
 
 constexpr int QT = 128;
+// network 0 needs W1, X0 and the misc block only (13 KB: 8 CTAs per SM, the
+// whole TMEM); network 1 adds the hidden activations and hidden-layer weights
 constexpr int Q_OFF_W1 = 0;                   // 64 x LF fp16 (interleaved)
-constexpr int Q_OFF_WH = 64 * 32 * 2;         // network 1: hidden layers 2, 3 (64 x 64 each)
-constexpr int Q_OFF_X0 = Q_OFF_WH + 2 * 64 * 64 * 2;   // 128 x LF fp16 (interleaved)
-constexpr int Q_OFF_H = Q_OFF_X0 + QT * 32 * 2;         // 128 x 64 hidden activations
-constexpr int Q_OFF_MISC = Q_OFF_H + QT * 64 * 2;
+constexpr int Q_OFF_X0 = 64 * 32 * 2;         // 128 x LF fp16 (interleaved)
+constexpr int Q_OFF_MISC = Q_OFF_X0 + QT * 32 * 2;
+constexpr int Q_OFF_H = Q_OFF_MISC + 1024;              // network 1: 128 x 64 hidden activations
+constexpr int Q_OFF_WH = Q_OFF_H + QT * 64 * 2;         // network 1: hidden layers 2, 3 (64 x 64 each)
+constexpr int Q_SMEM0 = Q_OFF_H;
+constexpr int Q_SMEM1 = Q_OFF_WH + 2 * 64 * 64 * 2;
 
 struct QMisc {
     uint64_t mbar;
@@ -31,7 +35,7 @@ struct QMisc {
     int lvoff[ROMAP_MAX_LEVELS];
     float w2[64];                              // density output row (network 0: W2 row 0, 1: W_out row 0)
 };
-constexpr int Q_SMEM = Q_OFF_MISC + (int)((sizeof(QMisc) + 127) / 128 * 128);
+static_assert(sizeof(QMisc) <= 1024, "query misc block");
 
 }  // namespace
 
@@ -160,18 +164,20 @@ void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const Ob
     if (n == 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_query_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
-        cudaFuncSetAttribute(k_query_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
+        cudaFuncSetAttribute(k_query_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM1);
+        cudaFuncSetAttribute(k_query_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM1);
         attr = true;
     }
     const long long tiles = (n + QT - 1) / QT;
-    // 8 CTAs per SM (64 TMEM columns each = the whole TMEM), persistent over tiles
-    long long grid = (long long)lc.num_sms * 8;
+    // persistent over tiles, as many CTAs as are resident: network 0 8 per SM (64
+    // TMEM columns each = the whole TMEM), network 1 3 per SM (62 KB of smem each)
+    const int smem = cfg.net == 1 ? Q_SMEM1 : Q_SMEM0;
+    long long grid = (long long)lc.num_sms * (cfg.net == 1 ? 3 : 8);
     if (grid > tiles) grid = tiles;
     if (cfg.L == 16)
-        k_query_mixed<16><<<(unsigned)grid, QT, Q_SMEM, lc.st>>>(cfg, obj, xyz, n, sigma);
+        k_query_mixed<16><<<(unsigned)grid, QT, smem, lc.st>>>(cfg, obj, xyz, n, sigma);
     else
-        k_query_mixed<8><<<(unsigned)grid, QT, Q_SMEM, lc.st>>>(cfg, obj, xyz, n, sigma);
+        k_query_mixed<8><<<(unsigned)grid, QT, smem, lc.st>>>(cfg, obj, xyz, n, sigma);
 }
 
 // ---------------------------------------------------------------------------
@@ -187,12 +193,17 @@ constexpr int F_OFF_W3 = F_OFF_W2 + 16 * 64 * 2;
 constexpr int F_OFF_W4 = F_OFF_W3 + 64 * 32 * 2;
 constexpr int F_OFF_W5 = F_OFF_W4 + 64 * 64 * 2;
 constexpr int F_OFF_WH2 = F_OFF_W5 + 16 * 64 * 2;   // network 1: third hidden layer (64 x 64)
+// activations alias: a layer's output may overwrite its input once its MMA has
+// completed (the epilogue runs after the wait), so two buffers carry the chain:
+// R1 = X0, then CIN (SH after L1, raw after L2); R2 = H1, G1, G2 (network 1:
+// every hidden layer).  53 KB per CTA -> 4 CTAs per SM hide each other's latency.
 constexpr int F_OFF_X0 = F_OFF_WH2 + 64 * 64 * 2;
+constexpr int F_OFF_CIN = F_OFF_X0;
 constexpr int F_OFF_H1 = F_OFF_X0 + QT * 32 * 2;
-constexpr int F_OFF_CIN = F_OFF_H1 + QT * 64 * 2;
-constexpr int F_OFF_G1 = F_OFF_CIN + QT * 32 * 2;
-constexpr int F_OFF_G2 = F_OFF_G1 + QT * 64 * 2;
-constexpr int F_OFF_MISC = F_OFF_G2 + QT * 64 * 2;
+constexpr int F_OFF_G1 = F_OFF_H1;
+constexpr int F_OFF_G2 = F_OFF_H1;
+constexpr int F_OFF_MISC = F_OFF_H1 + QT * 64 * 2;
+constexpr int F_CTAS_PER_SM = 4;
 constexpr int F_SMEM = F_OFF_MISC + (int)((sizeof(QMisc) + 127) / 128 * 128);
 
 __device__ __forceinline__ void f_sync_for_mma() {
@@ -299,11 +310,6 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
             encode_pair_fp16(tab, u, P, off, hmask, active, fq);
             *reinterpret_cast<uint2*>(X0 + tc::il_offset(t, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
         }
-        {
-            float sh[16];
-            sh4(rr.d, sh);
-            tc::st16(CIN, t, 16, 32, sh);
-        }
         f_sync_for_mma();
         if (t == 0) {
 #pragma unroll
@@ -316,6 +322,11 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
         float sigma, c[3];
         if (cfg.net == 0) {
         tc::epi_relu64(wk, H1, t);
+        {   // X0 is free now (L1 done): SH(4) of the view direction -> CIN[:, 16:32]
+            float sh[16];
+            sh4(rr.d, sh);
+            tc::st16(CIN, t, 16, 32, sh);
+        }
         f_sync_for_mma();
         if (t == 0) {
 #pragma unroll
@@ -425,7 +436,7 @@ void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj,
         attr = true;
     }
     const long long tiles = (S + QT - 1) / QT;
-    long long grid = (long long)lc.num_sms * 2;
+    long long grid = (long long)lc.num_sms * F_CTAS_PER_SM;
     if (grid > tiles) grid = tiles;
     if (cfg.L == 16)
         k_fwd_mixed<16><<<(unsigned)grid, QT, F_SMEM, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
