@@ -192,19 +192,27 @@ constexpr int F_OFF_W2 = F_OFF_W1 + 64 * 32 * 2;
 constexpr int F_OFF_W3 = F_OFF_W2 + 16 * 64 * 2;
 constexpr int F_OFF_W4 = F_OFF_W3 + 64 * 32 * 2;
 constexpr int F_OFF_W5 = F_OFF_W4 + 64 * 64 * 2;
-constexpr int F_OFF_WH2 = F_OFF_W5 + 16 * 64 * 2;   // network 1: third hidden layer (64 x 64)
 // activations alias: a layer's output may overwrite its input once its MMA has
 // completed (the epilogue runs after the wait), so two buffers carry the chain:
 // R1 = X0, then CIN (SH after L1, raw after L2); R2 = H1, G1, G2 (network 1:
-// every hidden layer).  53 KB per CTA -> 4 CTAs per SM hide each other's latency.
-constexpr int F_OFF_X0 = F_OFF_WH2 + 64 * 64 * 2;
+// every hidden layer).  Network 0 needs 44.4 KB per CTA -> 5 CTAs per SM hide
+// each other's gather latency; network 1's third hidden layer adds 8 KB (4 CTAs).
+constexpr int F_OFF_X0 = F_OFF_W5 + 16 * 64 * 2;
 constexpr int F_OFF_CIN = F_OFF_X0;
 constexpr int F_OFF_H1 = F_OFF_X0 + QT * 32 * 2;
 constexpr int F_OFF_G1 = F_OFF_H1;
 constexpr int F_OFF_G2 = F_OFF_H1;
 constexpr int F_OFF_MISC = F_OFF_H1 + QT * 64 * 2;
-constexpr int F_CTAS_PER_SM = 4;
-constexpr int F_SMEM = F_OFF_MISC + (int)((sizeof(QMisc) + 127) / 128 * 128);
+struct FMisc {
+    uint64_t mbar;
+    uint32_t tmem;
+    int pad;
+    int4 lv[ROMAP_MAX_LEVELS];
+    int lvoff[ROMAP_MAX_LEVELS];
+};
+constexpr int F_OFF_WH2 = F_OFF_MISC + (int)((sizeof(FMisc) + 127) / 128 * 128);   // network 1 only
+constexpr int F_SMEM0 = F_OFF_WH2;
+constexpr int F_SMEM1 = F_OFF_WH2 + 64 * 64 * 2;
 
 __device__ __forceinline__ void f_sync_for_mma() {
     tc::fence_async_smem();
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
                                                   float* __restrict__ dist_o, float* __restrict__ delta_o) {
     constexpr int LF = 2 * L;
     extern __shared__ __align__(1024) uint8_t smem[];
-    QMisc* misc = reinterpret_cast<QMisc*>(smem + F_OFF_MISC);
+    FMisc* misc = reinterpret_cast<FMisc*>(smem + F_OFF_MISC);
     const int t = threadIdx.x, warp = t >> 5;
     const ObjDev& ob = *obj;
     const int N = cfg.N;
@@ -431,15 +439,17 @@ void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj,
     if (S == 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_fwd_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
-        cudaFuncSetAttribute(k_fwd_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+        cudaFuncSetAttribute(k_fwd_mixed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM1);
+        cudaFuncSetAttribute(k_fwd_mixed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM1);
         attr = true;
     }
     const long long tiles = (S + QT - 1) / QT;
-    long long grid = (long long)lc.num_sms * F_CTAS_PER_SM;
+    const bool wh2 = cfg.net == 1 && cfg.hl == 3;
+    const int smem = wh2 ? F_SMEM1 : F_SMEM0;
+    long long grid = (long long)lc.num_sms * (wh2 ? 4 : 5);
     if (grid > tiles) grid = tiles;
     if (cfg.L == 16)
-        k_fwd_mixed<16><<<(unsigned)grid, QT, F_SMEM, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
+        k_fwd_mixed<16><<<(unsigned)grid, QT, smem, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
     else
-        k_fwd_mixed<8><<<(unsigned)grid, QT, F_SMEM, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
+        k_fwd_mixed<8><<<(unsigned)grid, QT, smem, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
 }
