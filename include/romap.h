@@ -193,6 +193,14 @@ romap_status romap_create_object(romap_ctx* ctx, const romap_box* box, const rom
 romap_status romap_create_object_with_id(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
                                          int32_t instance_id, int32_t obj_id);
 romap_status romap_destroy_object(romap_ctx* ctx, int32_t obj);
+/* replace the object's box (object SLAM refines pose and size
+ * over time).  Parameters, Adam state and keyframes are kept:
+ * the hash grid and the MLP stay defined over the normalized box coordinates
+ * u = (x + a) / (2a) of R6, so every later training iteration, render and
+ * density query maps world points through the new box (the learned field
+ * moves and stretches with it).  E_INVALID: non-finite centre / yaw or a
+ * non-positive half extent (nothing changes); E_NOT_FOUND: no such object. */
+romap_status romap_set_box(romap_ctx* ctx, int32_t obj, const romap_box* box);
 romap_status romap_get_object_info(romap_ctx* ctx, int32_t obj, romap_object_info* out);
 
 /* Add one keyframe: rgb uint8 [H][W][3], mask uint16 [H][W]

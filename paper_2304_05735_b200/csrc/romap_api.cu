@@ -516,13 +516,19 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     return ROMAP_OK;
 }
 
-static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
-                                int32_t instance_id, int32_t id) {
+static romap_status check_box(const romap_box* box) {
     if (!box) return fail(ROMAP_E_INVALID, "null box");
     for (int k = 0; k < 3; ++k)
         if (!(box->half_extents[k] > 0) || !std::isfinite(box->half_extents[k]) || !std::isfinite(box->t[k]))
             return fail(ROMAP_E_INVALID, "box must have finite centre and positive half extents");
     if (!std::isfinite(box->yaw)) return fail(ROMAP_E_INVALID, "non-finite yaw");
+    return ROMAP_OK;
+}
+
+static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
+                                int32_t instance_id, int32_t id) {
+    romap_status sb = check_box(box);
+    if (sb) return sb;
     if (id < 0) return fail(ROMAP_E_INVALID, "object id must be >= 0");
     if (find(ctx, id)) return fail(ROMAP_E_INVALID, "object id %d exists", id);
     CfgDev cd;
@@ -603,6 +609,20 @@ romap_status romap_destroy_object(romap_ctx* ctx, int32_t obj) {
     ctx->objs.erase(obj);
     free_object(ctx, ob);
     ctx->last_call = LAST_NONE;
+    return ROMAP_OK;
+}
+
+romap_status romap_set_box(romap_ctx* ctx, int32_t obj, const romap_box* box) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    romap_status s = check_box(box);
+    if (s) return s;
+    // descriptors are rebuilt from these fields by every later call (make_objdev)
+    ob->box = *box;
+    ob->c = (float)cos((double)box->yaw);   // R8: cos/sin in double, rounded
+    ob->s = (float)sin((double)box->yaw);
+    ctx->last_call = LAST_NONE;             // debug dumps describe the old box
     return ROMAP_OK;
 }
 

@@ -86,6 +86,7 @@ _SIGS = {
     "romap_create_object": [_P, C.POINTER(Box), C.POINTER(ModelConfig), _I, C.POINTER(_I)],
     "romap_create_object_with_id": [_P, C.POINTER(Box), C.POINTER(ModelConfig), _I, _I],
     "romap_destroy_object": [_P, _I],
+    "romap_set_box": [_P, _I, _P],
     "romap_get_object_info": [_P, _I, C.POINTER(ObjectInfo)],
     "romap_add_observation": [_P, _I, _P, _P, _P, C.POINTER(Intrinsics), _P, _I],
     "romap_set_rays_per_iter": [_P, _I, _I],
@@ -222,6 +223,11 @@ class Context:
 
     def destroy_object(self, obj: int):
         _check(_lib.romap_destroy_object(self._h, obj))
+
+    def set_box(self, obj: int, t, yaw: float, half_extents):
+        """f3: replace the object's box; parameters stay in normalized box coordinates."""
+        b = Box((C.c_float * 3)(*[float(v) for v in t]), float(yaw), (C.c_float * 3)(*[float(v) for v in half_extents]))
+        _check(_lib.romap_set_box(self._h, obj, C.byref(b)))
 
     def object_info(self, obj: int) -> dict:
         info = ObjectInfo()

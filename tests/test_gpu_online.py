@@ -64,3 +64,48 @@ def test_gate_budget_and_scheduler():
             acc, _ = c.offer_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
             assert c.pending_iters(h) == (300 if acc else 0)
     c.close()
+
+
+def test_set_box_matches_oracle():
+    """f3 box update: parameters stay in normalized box coordinates (R6), so after
+    romap_set_box the rays, samples and losses follow the new box exactly as the
+    oracle with the same box; bad boxes are rejected without side effects."""
+    from gpu_common import make_pair, norm_rel
+    c = R.Context(0)
+    sc = scenes.sphere_scene(0, n_views=8)
+    kw = dict(CFG, rays_per_iter=256)
+    h, st = make_pair(R, c, sc, kw)
+    for _ in range(3):
+        s = c.train_step([h], 1)[0]
+        o, _, _ = O.train_iteration(st)
+    ob = sc.objects[0]
+    t2 = np.asarray(ob.t, np.float64) + [0.05, -0.03, 0.02]
+    yaw2 = float(ob.yaw) + 0.2
+    a2 = np.asarray(ob.a, np.float64) * 1.15
+    with pytest.raises(R.RomapError):
+        c.set_box(h, t2, yaw2, [a2[0], -1.0, a2[2]])
+    c.set_box(h, t2, yaw2, a2)
+    st.box_t = np.asarray(t2, np.float32)
+    st.box_yaw = float(np.float32(yaw2))
+    st.box_a = np.asarray(a2, np.float32)
+    # gradients at identical parameters: the oracle takes the GPU's current ones
+    # (3 mixed-precision Adam steps leave them slightly apart)
+    W = c.get_params(h, R.BLOCK_MLP).astype(np.float64)
+    Ws, off = [], 0
+    for w in st.params["W"]:
+        Ws.append(W[off:off + w.size].reshape(w.shape))
+        off += w.size
+    st.params = {"table": c.get_params(h, R.BLOCK_TABLE).reshape(-1, 2).astype(np.float64), "W": Ws}
+    s = c.forward_backward([h])[0]
+    L, g, dbg = O.loss_and_grads(st, 4)              # the 4th iteration's rays (3 steps taken)
+    for k in ("l_total", "l_rgb", "l_rr", "l_density"):
+        assert abs(s[k] - L[k]) <= 1e-2 * max(abs(L[k]), 1e-4), (k, s[k], L[k])
+    assert s["hit_rays"] == L["hit_rays"] and s["samples"] == L["samples"]
+    gt = c.get_params(h, R.BLOCK_GRAD_TABLE).reshape(-1, 2)
+    assert norm_rel(gt, g["table"]) < 2e-2
+    # training continues on the new box and tracks the oracle
+    for _ in range(3):
+        s = c.train_step([h], 1)[0]
+        o, _, _ = O.train_iteration(st)
+        assert abs(s["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (s, o)
+    c.close()
