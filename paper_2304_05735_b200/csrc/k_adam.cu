@@ -133,15 +133,6 @@ void launch_adam(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int
     k_adam<<<grid, 256, 0, lc.st>>>(cfg, objs, nonfinite, write_half ? 1 : 0);
 }
 
-__global__ void k_step_inc(const ObjDev* __restrict__ objs, int n_objs) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n_objs) *objs[i].step += 1;
-}
-
-void launch_step_inc(const LaunchCtx& lc, const ObjDev* objs, int n_objs) {
-    if (n_objs > 0) k_step_inc<<<(n_objs + 127) / 128, 128, 0, lc.st>>>(objs, n_objs);
-}
-
 __global__ void __launch_bounds__(256) k_zero_grads(CfgDev cfg, const ObjDev* __restrict__ objs) {
     const ObjDev& ob = objs[blockIdx.y];
     const int total = cfg.n_table + cfg.n_mlp;

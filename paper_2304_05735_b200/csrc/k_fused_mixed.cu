@@ -26,7 +26,7 @@
 //   tile_done[b] M -> G   the tile's last MMAs completed: dfeat is in TMEM DF[b]
 //                         and X0[b] is free                           (tcgen05.commit)
 //   df_empty[b]  G -> M   DF[b] has been read                         (8 warp arrivals)
-// Per-sample geometry (u, dist, delta) comes from k_raygen_samples (bit-exact
+// Per-sample geometry (u, dist, delta) comes from k_raygen + k_samples (bit-exact
 // with the fp32 path), so neither role recomputes the RNG / IEEE divisions.
 // Loss scaling: every backward operand is multiplied by cfg.loss_scale (a power
 // of two, exact) and divided out before the fp32 atomics.
@@ -441,7 +441,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     for (int it = 0; it < n + NB; ++it) {
         const bool dg = it < n, ds = it >= NB;       // gather tile it, scatter tile it - NB
         const int b = it % NB;
-        const bool ag = u_next.x >= 0.f;              // sample of an active ray (k_raygen_samples)
+        const bool ag = u_next.x >= 0.f;              // sample of an active ray (k_raygen + k_samples)
         const float ug[3] = {u_next.x, u_next.y, u_next.z};
         const int slot_g = slot_next;
         if (it + 1 < n) {

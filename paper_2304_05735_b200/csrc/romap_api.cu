@@ -2,10 +2,12 @@
 //
 // Owns: the object registry, per-object parameter / gradient / Adam blocks,
 // per-object keyframe crops on the device, the segmented ray layout of a
-// train_step batch, and the launch sequence of one iteration
-// (raygen -> fwd -> render_loss -> bwd -> adam -> step_inc).  Everything is
-// enqueued on the context's stream; the host only crosses the boundary at
-// launch and at the final statistics read-back.
+// train_step batch, and the launch sequence of one iteration (mixed path:
+// raygen + samples of K iterations -> fused step -> Adam, chunks of K replayed
+// as one CUDA graph; fp32 path: raygen -> fwd -> render_loss -> bwd -> Adam; the
+// Adam launch advances the step counters).  Everything is enqueued on the
+// context's stream; the host only crosses the boundary at launch and at the
+// final statistics read-back.
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -149,7 +151,7 @@ struct romap_ctx {
     size_t rays_cap = 0;
     float* samp = nullptr;       // sigma | rgb(3) | dist | delta | dsigma | drgb(3) : 10 floats per sample
     size_t samp_cap = 0;
-    float* srec = nullptr;       // mixed path: K slices of (u, dist) float4, then K slices of delta (k_raygen_samples)
+    float* srec = nullptr;       // mixed path: K slices of (u, dist) float4, then K slices of delta (k_raygen + k_samples)
     size_t srec_cap = 0;
     size_t last_ray_base = 0;    // ray slot of slice holding the last iteration's rays
     float* act = nullptr;
@@ -835,7 +837,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     if (dirty) STAGE(ST_ZERO_GRADS, launch_zero_grads(lc, b.cfg, ctx->objdev_d, n));
     const size_t S = (size_t)b.total_slots * b.cfg.N;
     // mixed path: rays and sample records of up to K iterations are generated by
-    // one k_raygen_samples launch (slices k = it % K), ~64 MB of records at most
+    // one k_raygen + k_samples pair (slices k = it % K), ~64 MB of records at most
     int K = 1;
     if (b.mixed) {
         const size_t per_iter = (size_t)b.total_slots * sizeof(RayRec) + S * 5 * sizeof(float);

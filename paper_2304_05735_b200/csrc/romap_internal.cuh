@@ -331,7 +331,6 @@ void launch_bwd_fp32(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs,
                      long long act_stride);
 void launch_adam(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int* nonfinite,
                  bool write_half);
-void launch_step_inc(const LaunchCtx& lc, const ObjDev* objs, int n_objs);
 void launch_zero_grads(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs);
 void launch_render_rays(const LaunchCtx& lc, const ObjDev* obj, const KfDev* cam, int W, int H, RayRec* rays);
 void launch_composite(const LaunchCtx& lc, int N, const RayRec* rays, int n_rays, const float* sigma,
