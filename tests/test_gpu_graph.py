@@ -61,3 +61,39 @@ def test_graph_matches_plain_launches():
     d_gp = max(norm_rel(ta, tb), norm_rel(ma, mb))
     d_pp = max(norm_rel(tc_, tb), norm_rel(mc, mb))
     assert d_gp <= 2.0 * d_pp + 5e-3, (d_gp, d_pp)
+
+
+def test_graph_multi_object_with_keyframe_appends():
+    """Three objects batched, 20 iterations per call (one graph chunk of 16 + a
+    4-iteration tail), keyframes appended between calls: the cached graph is
+    replayed with the new descriptors, the geometry stays bit-exact (hit counts
+    summed over each call) and the losses track the oracle."""
+    import dataclasses
+    c = R.Context(0)
+    sc = scenes.room_scene(6, n_objects=3, n_frames=8, W=160, H=120, f=131.25, room_half=1.5)
+    half = sc.frames[: len(sc.frames) // 2]
+    sc_half = dataclasses.replace(sc, frames=half)
+    kw = dict(CFG0M, rays_per_iter=128, seed=6)
+    hs, sts = [], []
+    for k, ob in enumerate(sc.objects[:3]):
+        h, st = make_pair(R, c, sc_half, kw, param_seed=60 + k, inst=ob.instance_id, obj_id=400 + k,
+                          avoid_kinks=False)
+        hs.append(h)
+        sts.append(st)
+    for call in range(2):
+        if call == 1:
+            for k, ob in enumerate(sc.objects[:3]):
+                for fr in sc.frames[len(half):]:
+                    if (fr.mask == ob.instance_id).any():
+                        c.add_observation(hs[k], fr.rgb, fr.mask, fr.T_wc, fr.K)
+                        sts[k].kfs.append(O.ingest_observation(fr.rgb, fr.mask, fr.T_wc, fr.K, ob.instance_id))
+        s = c.train_step(hs, 20)
+        for k in range(3):
+            hits = 0
+            for _ in range(20):
+                o, _, _ = O.train_iteration(sts[k])
+                hits += o["hit_rays"]
+            assert s[k]["hit_rays"] == hits, (call, k, s[k]["hit_rays"], hits)
+            assert s[k]["step"] == 20 * (call + 1)
+            assert abs(s[k]["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (call, k, s[k], o)
+    c.close()
