@@ -109,3 +109,34 @@ def test_set_box_matches_oracle():
         o, _, _ = O.train_iteration(st)
         assert abs(s["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (s, o)
     c.close()
+
+
+def test_all_rays_miss_after_box_moves_away():
+    """Degenerate batch: the box moved behind every camera, so no ray hits it.
+    The fused step must see zero hit rays, produce zero losses and gradients
+    without non-finite values, and Adam must still apply the dense MLP update
+    with zero gradients (momentum) exactly like the oracle,
+    leaving the sparse table untouched."""
+    from gpu_common import make_pair, norm_rel
+    c = R.Context(0)
+    sc = scenes.sphere_scene(0, n_views=8)
+    kw = dict(CFG, rays_per_iter=256)
+    h, st = make_pair(R, c, sc, kw)
+    for _ in range(2):
+        c.train_step([h], 1)
+        O.train_iteration(st)
+    t_far = np.asarray(sc.objects[0].t, np.float64) + [0.0, 0.0, 50.0]
+    c.set_box(h, t_far, sc.objects[0].yaw, sc.objects[0].a)
+    st.box_t = np.asarray(t_far, np.float32)
+    table0 = c.get_params(h, R.BLOCK_TABLE).copy()
+    for _ in range(2):
+        s = c.train_step([h], 1)[0]
+        o, _, _ = O.train_iteration(st)
+        assert s["hit_rays"] == o["hit_rays"] == 0
+        assert s["samples"] == 0 and s["l_total"] == 0.0
+    assert s["step"] == 4
+    assert np.array_equal(c.get_params(h, R.BLOCK_TABLE), table0)    # sparse: untouched
+    W = c.get_params(h, R.BLOCK_MLP).astype(np.float64)
+    Wo = np.concatenate([w.reshape(-1) for w in st.params["W"]])
+    assert norm_rel(W, Wo) < 5e-2                                      # momentum steps as the oracle
+    c.close()
