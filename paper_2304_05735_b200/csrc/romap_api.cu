@@ -82,6 +82,10 @@ struct Object {
     bool grads_dirty = false;
     // last batch (debug dumps)
     int last_ray_begin = -1, last_n_rays = 0;
+    // keyframe crops / depth live in a bump arena of device chunks (one cudaMalloc
+    // per few MB instead of one per keyframe; freed with the object)
+    std::vector<void*> kf_chunks;
+    size_t kf_used = 0, kf_cap = 0;
     // f3 online policy (R25): camera centre of the last accepted keyframe, pending budget
     bool has_gate_ref = false;
     double gate_ref[3] = {0, 0, 0};
@@ -482,7 +486,7 @@ static void free_object(romap_ctx* ctx, Object* ob) {
     dfree(ctx, ob->v);
     dfree(ctx, ob->p16);
     dfree(ctx, ob->step_d);
-    for (auto& k : ob->kfs) { dfree(ctx, k.crop_d); dfree(ctx, k.depth_d); }
+    for (void* c : ob->kf_chunks) dfree(ctx, c);     // keyframe crops and depth (arena)
     dfree(ctx, ob->kfs_d);
     dfree(ctx, ob->prefix_d);
     delete ob;
@@ -647,6 +651,21 @@ romap_status romap_get_object_info(romap_ctx* ctx, int32_t obj, romap_object_inf
     return ROMAP_OK;
 }
 
+static void* kf_alloc(romap_ctx* ctx, Object* ob, size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (ob->kf_chunks.empty() || ob->kf_used + bytes > ob->kf_cap) {
+        const size_t cap = std::max<size_t>(bytes, (size_t)4 << 20);
+        void* p = dalloc(ctx, cap);
+        if (!p) return nullptr;
+        ob->kf_chunks.push_back(p);
+        ob->kf_used = 0;
+        ob->kf_cap = cap;
+    }
+    void* p = static_cast<char*>(ob->kf_chunks.back()) + ob->kf_used;
+    ob->kf_used += bytes;
+    return p;
+}
+
 romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
                                    const float T_wc[12], const romap_intrinsics* K,
                                    const romap_depth_sample* depth, int32_t n_depth) {
@@ -661,15 +680,29 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
         if (!std::isfinite(T_wc[k])) return fail(ROMAP_E_INVALID, "non-finite pose");
     const int W = K->width, H = K->height;
     const uint16_t id = (uint16_t)ob->instance_id;
+    // tight AABB of mask == id: per row a branch-free (vectorisable) test of 32-pixel
+    // blocks finds the first and last hit, rows without the object cost one pass
     int x0 = W, y0 = H, x1 = -1, y1 = -1;
-    for (int y = 0; y < H; ++y)
-        for (int x = 0; x < W; ++x)
-            if (mask[(size_t)y * W + x] == id) {
-                if (x < x0) x0 = x;
-                if (x > x1) x1 = x;
-                if (y < y0) y0 = y;
-                if (y > y1) y1 = y;
-            }
+    for (int y = 0; y < H; ++y) {
+        const uint16_t* row = mask + (size_t)y * W;
+        int first = -1, last = -1;
+        for (int b = 0; b < W; b += 32) {
+            const int e = std::min(W, b + 32);
+            int any = 0;
+            for (int x = b; x < e; ++x) any |= row[x] == id;
+            if (!any) continue;
+            if (first < 0)
+                for (int x = b; x < e; ++x)
+                    if (row[x] == id) { first = x; break; }
+            for (int x = e - 1; x >= b; --x)
+                if (row[x] == id) { last = x; break; }
+        }
+        if (first < 0) continue;
+        x0 = std::min(x0, first);
+        x1 = std::max(x1, last);
+        if (y0 == H) y0 = y;
+        y1 = y;
+    }
     if (x1 < 0) return fail(ROMAP_E_INVALID, "instance %d not visible in the mask", ob->instance_id);
     const int w = x1 - x0 + 1, h = y1 - y0 + 1;
     if (ob->total_area + (long long)w * h >= (1LL << 31)) return fail(ROMAP_E_INVALID, "too many keyframe pixels");
@@ -705,11 +738,11 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     kf.dev.w = w;
     kf.dev.h = h;
     kf.area = (long long)w * h;
-    kf.crop_d = (uchar4*)dalloc(ctx, crop.size() * sizeof(uchar4));
+    kf.crop_d = (uchar4*)kf_alloc(ctx, ob, crop.size() * sizeof(uchar4));
     if (!kf.crop_d) return fail(ROMAP_E_OOM, "crop allocation failed");
     if (any_depth) {
-        kf.depth_d = (float*)dalloc(ctx, dep.size() * 4);
-        if (!kf.depth_d) { dfree(ctx, kf.crop_d); return fail(ROMAP_E_OOM, "depth allocation failed"); }
+        kf.depth_d = (float*)kf_alloc(ctx, ob, dep.size() * 4);
+        if (!kf.depth_d) return fail(ROMAP_E_OOM, "depth allocation failed");
     }
     kf.dev.crop = kf.crop_d;
     kf.dev.depth = kf.depth_d;
@@ -719,7 +752,7 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
         KfDev* nk = (KfDev*)dalloc(ctx, nc * sizeof(KfDev));
         long long* np = (long long*)dalloc(ctx, nc * sizeof(long long));
         if (!nk || !np) {
-            dfree(ctx, nk); dfree(ctx, np); dfree(ctx, kf.crop_d); dfree(ctx, kf.depth_d);
+            dfree(ctx, nk); dfree(ctx, np);          // (arena space of the crop stays with the object)
             return fail(ROMAP_E_OOM, "keyframe table allocation failed");
         }
         CK(cudaStreamSynchronize(ctx->st));
@@ -744,7 +777,8 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     }
     CK(cudaMemcpyAsync(ob->kfs_d, descs.data(), descs.size() * sizeof(KfDev), cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemcpyAsync(ob->prefix_d, prefix.data(), prefix.size() * sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
+    // (copies from pageable memory return once the source is staged: the host
+    // vectors may go; the device sees the data in stream order)
     return ROMAP_OK;
 }
 
