@@ -7,6 +7,13 @@
 // fp16 w, g zero) -- see DESIGN.md "Kernels".
 #include "romap_internal.cuh"
 
+#include <cstdlib>
+
+bool pdl_enabled() {
+    static const bool on = getenv("ROMAP_NO_PDL") == nullptr;
+    return on;
+}
+
 // one Adam update of 4 consecutive parameters (i0 .. i0+3, all < total);
 // returns whether any of them changed (tables are sparse, R18)
 __device__ __forceinline__ bool adam4(float4& pp, float4& mm, float4& vv, const float4 gg, int i0, int n_table,
@@ -51,6 +58,8 @@ __device__ __forceinline__ float2 bias_corrections(double b1, double b2, long lo
 
 __global__ void __launch_bounds__(256, 3) k_adam(CfgDev cfg, const ObjDev* __restrict__ objs, int* __restrict__ nonfinite,
                                                  int write_half) {
+    pdl_trigger();
+    pdl_wait();                                   // gradients of the fused step (PDL launch)
     const ObjDev& ob = objs[blockIdx.y];
     const float2 bc = *reinterpret_cast<const float2*>(ob.step + 2);
     const float ibc1 = bc.x, ibc2 = bc.y;
@@ -129,8 +138,17 @@ void launch_adam(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int
     // every float4 group of the object covered: 256 threads x ADAM_G groups per block
     int bx = (int)((total / 4 + 256 * ADAM_G - 1) / (256 * ADAM_G));
     if (bx < 1) bx = 1;
-    dim3 grid(bx, n_objs);
-    k_adam<<<grid, 256, 0, lc.st>>>(cfg, objs, nonfinite, write_half ? 1 : 0);
+    cudaLaunchConfig_t lcfg = {};
+    lcfg.gridDim = dim3(bx, n_objs);
+    lcfg.blockDim = dim3(256);
+    lcfg.dynamicSmemBytes = 0;
+    lcfg.stream = lc.st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lcfg.attrs = attr;
+    lcfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&lcfg, k_adam, cfg, objs, nonfinite, write_half ? 1 : 0);
 }
 
 __global__ void __launch_bounds__(256) k_zero_grads(CfgDev cfg, const ObjDev* __restrict__ objs) {

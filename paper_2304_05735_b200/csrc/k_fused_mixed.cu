@@ -1134,6 +1134,10 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
         misc->lv[t] = level_params(cfg, t);
         misc->lvoff[t] = cfg.off[t];
     }
+    // PDL: let Adam launch now (its CTAs take SMs as ours leave) and wait for the
+    // previous grid (Adam: tables, weights, zeroed gradients) before any access
+    pdl_trigger();
+    pdl_wait();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -1177,5 +1181,15 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
     const int per = 0;   // unused: tiles are strided over the grid
     auto kern = cfg.net == 1 ? (cfg.L == 16 ? k_fused_mixed<16, 1> : k_fused_mixed<8, 1>)
                              : (cfg.L == 16 ? k_fused_mixed<16, 0> : k_fused_mixed<8, 0>);
-    kern<<<grid, NT, SMEM_BYTES, lc.st>>>(cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc, nonfinite, dbg);
+    cudaLaunchConfig_t lcfg = {};
+    lcfg.gridDim = dim3(grid);
+    lcfg.blockDim = dim3(NT);
+    lcfg.dynamicSmemBytes = SMEM_BYTES;
+    lcfg.stream = lc.st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    lcfg.attrs = la;
+    lcfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&lcfg, kern, cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc, nonfinite, dbg);
 }

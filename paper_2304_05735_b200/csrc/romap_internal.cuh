@@ -249,6 +249,14 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned v) {
     asm("mov.b32 %0, %0;" : "+r"(v));
     return v;
 }
+// programmatic dependent launch (the fused step and Adam are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets the next one
+// launch early (its CTAs take SMs as ours leave, no launch gap) and waits for the
+// previous grid's completion and memory before touching its outputs
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// host: whether launches use it (ROMAP_NO_PDL=1 turns it off)
+bool pdl_enabled();
 // a when p else b, as one SEL the compiler cannot turn into a branch
 __device__ __forceinline__ uint32_t selp_u32(bool p, uint32_t a, uint32_t b) {
     uint32_t r;
