@@ -14,7 +14,8 @@ lib = C.CDLL(R.LIB_PATH)
 fn = lib.romap_debug_fused_prof
 fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 ctx = R.Context(0)
-kw = bench.cfg1_kwargs(1)
+paper = "--paper" in sys.argv                  # the paper's workload (network 1, 4096 x 32)
+kw = bench.paper_kwargs() if paper else bench.cfg1_kwargs(1)
 sc = bench.load_scene()
 ob = sc.objects[0]
 h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id)
@@ -27,7 +28,7 @@ iters = 20
 ctx.train_step([h], iters)
 fn(buf, 1)
 v = list(buf)
-tiles = 4096 * 64 // 128 * iters
+tiles = 4096 * kw["samples_per_ray"] // 128 * iters
 ctas = 148 * iters
 names = {5: "CTA setup", 7: "CTA total", 15: "M final flush", 0: "M total", 1: "M wait x0_full", 2: "M fwd chain", 3: "M render", 4: "M bwd chain", 6: "M tile top", 12: "  render scans", 13: "  render loss",
          8: "G total (per WG)", 9: "G wait tile_done", 10: "G level loop"}
