@@ -63,6 +63,8 @@ def workload_kwargs(args, precision):
     kw = cfg1_kwargs(precision)
     if args.log2_T:
         kw["log2_T"] = args.log2_T
+    if args.rays_per_iter:
+        kw["rays_per_iter"] = args.rays_per_iter      # cfg3: 2048 rays per object
     return kw
 
 
@@ -444,11 +446,11 @@ def run_ours(args):
         paper_sps = paper_baseline_samples_per_s(kw)
         if args.network == "paper":
             desc = (f"paper network (PAPER.md:222, R24): L=16 F=2 T=2^{kw['log2_T']} res 16->2048, "
-                    f"{kw['hidden_layers']} hidden layer(s) of 64 on positions -> sigma, rgb, 4096 rays x 32 "
+                    f"{kw['hidden_layers']} hidden layer(s) of 64 on positions -> sigma, rgb, {kw['rays_per_iter']} rays x 32 "
                     f"stratified samples per object, Adam")
         else:
-            desc = ("L=16 F=2 T=2^16 res 16->512, density 32->64->16 + SH4 colour 32->64->64->3, "
-                    "4096 rays x 64 stratified samples per object, Adam")
+            desc = (f"L=16 F=2 T=2^{kw['log2_T']} res 16->512, density 32->64->16 + SH4 colour 32->64->64->3, "
+                    f"{kw['rays_per_iter']} rays x 64 stratified samples per object, Adam")
         cpu = None if args.no_cpu_baseline else cpu_baseline(scene, kw)
         per_obj_ms = t_max_ms / args.steps / len(objs)
         line = {
@@ -548,6 +550,7 @@ def main():
     ap.add_argument("--objects", type=int, default=0,
                     help="total objects over all ranks, LPT-partitioned (0: objects-per-gpu x ranks)")
     ap.add_argument("--keyframes", type=int, default=20)
+    ap.add_argument("--rays-per-iter", type=int, default=0, help="rays per object and iteration (0: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
