@@ -114,7 +114,7 @@ constexpr int NM = 128;                        // MLP/render threads (M)
 constexpr int NT = NG + NM;
 constexpr int BAR_M = 1;                       // named barrier of M
 #ifndef ROMAP_MERGE_RES
-#define ROMAP_MERGE_RES 64
+#define ROMAP_MERGE_RES 41
 #endif
 #ifndef ROMAP_MERGE8_RES
 #define ROMAP_MERGE8_RES 0
@@ -643,6 +643,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
         gm[0] = g_cur;
         FP_MARK(g_w2);
         FP_ACC(10, g_w1, g_w2);
+        if (WG == 1) FP_ACC(11, g_w1, g_w2);         // warpgroup G1 alone (G0 = slot 10 - slot 11)
     }
     FP_MARK(g_end);
     FP_ACC(8, g_start, g_end);

@@ -32,6 +32,8 @@ tiles = 4096 * kw["samples_per_ray"] // 128 * iters
 ctas = 148 * iters
 names = {5: "CTA setup", 7: "CTA total", 15: "M final flush", 0: "M total", 1: "M wait x0_full", 2: "M fwd chain", 3: "M render", 4: "M bwd chain", 6: "M tile top", 12: "  render scans", 13: "  render loss",
          8: "G total (per WG)", 9: "G wait tile_done", 10: "G level loop"}
+G1 = v[11] / tiles
+print(f"G level loop per warpgroup: G0 {(v[10] - v[11]) / tiles:.0f}, G1 {G1:.0f} cycles/tile")
 for k, n in names.items():
     per = v[k] / (2 * tiles if 8 <= k <= 10 else tiles)
     print(f"{n:20s} {per:10.0f} cycles/tile   ({v[k] / ctas / 1965:.1f} us per CTA-iteration{' per WG' if 8 <= k <= 10 else ''})")
