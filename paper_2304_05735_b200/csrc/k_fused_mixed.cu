@@ -471,15 +471,24 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             unsigned fl;
             asm volatile("mov.b32 %0, %1;" : "=r"(fl) : "r"(flags_it));
             const bool dg_ = fl & 1u, ds_ = fl & 2u, ag_ = fl & 4u, as_ = fl & 8u;
-            const int l = LPT * pp;
+            // levels of this trip: with 2 per trip, pair pp = (pp, L - 1 - pp), a coarse
+            // level with a fine one, so the two warpgroups carry the same mix of
+            // merged (coarse) and plain (fine) scatters
+            int lv_[LPT];
+            if constexpr (LPT == 2) {
+                lv_[0] = pp;
+                lv_[1] = L - 1 - pp;
+            } else {
+                lv_[0] = pp;
+            }
             int4 P[LPT];
             unsigned off[LPT];
 #pragma unroll
             for (int q = 0; q < LPT; ++q) {
-                P[q] = misc->lv[l + q];
-                off[q] = (unsigned)misc->lvoff[l + q];
+                P[q] = misc->lv[lv_[q]];
+                off[q] = (unsigned)misc->lvoff[lv_[q]];
             }
-            // (1) gathers of levels l, l+1 of tile it.  x-neighbour corners (b, b|1)
+            // (1) gathers of the trip's levels of tile it.  x-neighbour corners (b, b|1)
             // share a 16-byte chunk of the fp16 table in 3 of 4 cases (dense:
             // entries e, e+1; hashed: e ^ (x ^ (x+1)) with the x prime = 1), so each
             // corner pair is one 16-B gather (+ a 4-B one otherwise); level blocks
@@ -510,7 +519,10 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
             // (RED requests, not bytes, bound this kernel).
             if (ds_) {
                 float g[4];
-                tc::tmem_ld4_sync(df_lane + 32 * b + 2 * l, g);
+                if constexpr (LPT == 2)
+                    tc::tmem_ld2x2_sync(df_lane + 32 * b + 2 * lv_[0], df_lane + 32 * b + 2 * lv_[1], g);
+                else
+                    tc::tmem_ld4_sync(df_lane + 32 * b + 2 * lv_[0], g);
 #pragma unroll
                 for (int q = 0; q < LPT; ++q) {
                     Cell cs;
@@ -616,10 +628,9 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                     fq[q] = __hfma2(fz, __hsub2(vy1, vy0), vy0);
 #endif
                 }
-                if constexpr (LPT == 2)
-                    *reinterpret_cast<uint2*>(X0 + tc::il_offset(r, 2 * l, LF)) = *reinterpret_cast<uint2*>(fq);
-                else
-                    *reinterpret_cast<__half2*>(X0 + tc::il_offset(r, 2 * l, LF)) = fq[0];
+#pragma unroll
+                for (int q = 0; q < LPT; ++q)
+                    *reinterpret_cast<__half2*>(X0 + tc::il_offset(r, 2 * lv_[q], LF)) = fq[q];
             }
         }
         if (ds) {                                     // DF[b] read: M may overwrite it (tile it)
