@@ -128,18 +128,20 @@ constexpr int OFF_W2 = OFF_W1 + 64 * 32 * 2;   // 16 x 64
 constexpr int OFF_W3 = OFF_W2 + 16 * 64 * 2;   // 64 x 32
 constexpr int OFF_W4 = OFF_W3 + 64 * 32 * 2;   // 64 x 64
 constexpr int OFF_W5 = OFF_W4 + 64 * 64 * 2;   // 16 x 64 (rows 3..15 zero)
-constexpr int OFF_WH2 = OFF_W5 + 16 * 64 * 2;  // network 1: second 64 x 64 hidden layer
 constexpr int X0_BYTES = TILE * 32 * 2;
-constexpr int OFF_X0 = OFF_WH2 + 64 * 64 * 2;  // NB slots x 128 x LF
+constexpr int OFF_X0 = OFF_W5 + 16 * 64 * 2;   // NB slots x 128 x LF
 constexpr int OFF_H1 = OFF_X0 + NB * X0_BYTES; // 128 x 64
 constexpr int OFF_CIN = OFF_H1 + TILE * 64 * 2;
+constexpr int OFF_WH2 = OFF_CIN;               // network 1 (no CIN): third 64 x 64 hidden layer
 constexpr int OFF_G1 = OFF_CIN + TILE * 32 * 2;
 constexpr int OFF_G2 = OFF_G1 + TILE * 64 * 2;
 constexpr int OFF_DC = OFF_G2 + TILE * 64 * 2;  // 128 x 16
 constexpr int OFF_DR = OFF_DC + TILE * 16 * 2;  // 128 x 16
 constexpr int OFF_DB = OFF_DR + TILE * 16 * 2;  // 128 x 64 (dg2, dh1)
-constexpr int OFF_DB2 = OFF_DB + TILE * 64 * 2; // 128 x 64 (dg1): its producer overlaps the dW MMAs reading DB
-constexpr int OFF_MISC = OFF_DB2 + TILE * 64 * 2;
+// dg1 (its producer overlaps the dW MMAs reading DB): G2's space, dead by then
+// (B5's dW5 MMAs are covered by B4's commit; network 1 likewise after W_out)
+constexpr int OFF_DB2 = OFF_G2;
+constexpr int OFF_MISC = OFF_DB + TILE * 64 * 2;
 constexpr int SMEM_BYTES = OFF_MISC + 1024;
 
 // TMEM columns (one CTA per SM, so the whole 512-column allocation is free)
@@ -755,7 +757,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             dw_fresh = true;
             invB = 1.0f / (float)ob.n_rays;
         }
-        {
+        if constexpr (NET == 0) {    // SH(4) of the view direction (network 1 has no colour net; WH2 aliases CIN)
             float sh[16];
             sh4(rr.d, sh);
             tc::st16(CIN, m, 16, 32, sh);
