@@ -678,6 +678,8 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     if (n_depth < 0 || (n_depth > 0 && !depth)) return fail(ROMAP_E_INVALID, "bad depth samples");
     for (int k = 0; k < 12; ++k)
         if (!std::isfinite(T_wc[k])) return fail(ROMAP_E_INVALID, "non-finite pose");
+    static const bool host_prof = getenv("ROMAP_HOST_PROF") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     const int W = K->width, H = K->height;
     const uint16_t id = (uint16_t)ob->instance_id;
     // tight AABB of mask == id: per row a branch-free (vectorisable) test of 32-pixel
@@ -704,16 +706,21 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
         y1 = y;
     }
     if (x1 < 0) return fail(ROMAP_E_INVALID, "instance %d not visible in the mask", ob->instance_id);
+    const auto t1 = std::chrono::steady_clock::now();
     const int w = x1 - x0 + 1, h = y1 - y0 + 1;
     if (ob->total_area + (long long)w * h >= (1LL << 31)) return fail(ROMAP_E_INVALID, "too many keyframe pixels");
     std::vector<uchar4> crop((size_t)w * h);
-    for (int y = 0; y < h; ++y)
+    for (int y = 0; y < h; ++y) {
+        const uint16_t* mrow = mask + (size_t)(y0 + y) * W + x0;
+        const uint8_t* crow = rgb + 3 * ((size_t)(y0 + y) * W + x0);
+        uchar4* out = crop.data() + (size_t)y * w;
         for (int x = 0; x < w; ++x) {
-            size_t src = (size_t)(y0 + y) * W + (x0 + x);
-            uint16_t mv = mask[src];
-            unsigned char cls = mv == id ? CLS_OBJ : (mv == 0 ? CLS_BG : CLS_OCC);
-            crop[(size_t)y * w + x] = make_uchar4(rgb[3 * src], rgb[3 * src + 1], rgb[3 * src + 2], cls);
+            const uint16_t mv = mrow[x];
+            const unsigned char cls = mv == id ? CLS_OBJ : (mv == 0 ? CLS_BG : CLS_OCC);
+            out[x] = make_uchar4(crow[3 * x], crow[3 * x + 1], crow[3 * x + 2], cls);
         }
+    }
+    const auto t2 = std::chrono::steady_clock::now();
     std::vector<float> dep;
     bool any_depth = false;
     if (n_depth > 0) {
@@ -762,6 +769,7 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
         ob->prefix_d = np;
         ob->kfs_cap = nc;
     }
+    const auto t3 = std::chrono::steady_clock::now();
     CK(cudaMemcpyAsync(kf.crop_d, crop.data(), crop.size() * sizeof(uchar4), cudaMemcpyHostToDevice, ctx->st));
     if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep.data(), dep.size() * 4, cudaMemcpyHostToDevice, ctx->st));
     ob->kfs.push_back(kf);
@@ -779,6 +787,14 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     CK(cudaMemcpyAsync(ob->prefix_d, prefix.data(), prefix.size() * sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
     // (copies from pageable memory return once the source is staged: the host
     // vectors may go; the device sees the data in stream order)
+    if (host_prof) {
+        const auto t4 = std::chrono::steady_clock::now();
+        auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        fprintf(stderr, "[romap host] add_observation: aabb %.3f ms, crop %.3f ms, alloc+desc %.3f ms, copies %.3f ms\n",
+                ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+    }
     return ROMAP_OK;
 }
 
