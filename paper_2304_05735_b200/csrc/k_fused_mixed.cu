@@ -15,9 +15,10 @@
 //          the object (flushed once per CTA and object with fp32 REDs)   [M]
 //   a7     hash-grid backward: recomputed cells, fp32 vector REDs      [G0, G1]
 //
-// Pipeline.  G0 / G1 (threads 0-255) own hash levels [0, L/2) / [L/2, L) of
-// sample t % 128; M (threads 256-383) owns the whole MLP / render chain of
-// sample t - 256.  In G iteration `it` the gathers of tile `it` are interleaved,
+// Pipeline.  G0 / G1 (threads 0-255) own the level pairs (p, L-1-p) with p even /
+// odd of sample t % 128 (each pair a coarse and a fine level, so both carry the
+// same mix); M (threads 256-383) owns the whole MLP / render chain of sample
+// t - 256.  In G iteration `it` the gathers of tile `it` are interleaved,
 // level pair by level pair, with the fire-and-forget scatter of tile `it - NB`
 // (NB = 3), so the REDs fill the gathers' L2 latency; meanwhile M runs one of the
 // tiles in between (three slots absorb the tile-to-tile variation of either role).
