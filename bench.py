@@ -175,12 +175,17 @@ def ncu_traffic(kernel):
 REQ_CEILING = 0.828
 
 
-def request_roofline(samples_per_launch, ms, sm_clk, n_sm):
+def request_roofline(kw, samples_per_launch, ms, sm_clk, n_sm):
     """L1 sector requests of the gathers + REDs per SM-cycle against the measured
-    random-access ceiling; sectors per hit sample from the committed ncu capture."""
+    random-access ceiling; sectors per hit sample from the committed ncu capture of
+    the same model (profiles/ncu_requests.json), else None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_requests.json")))
+        entries = json.load(open(os.path.join(ROOT, "profiles", "ncu_requests.json")))["entries"]
     except Exception:
+        return None
+    mine = {k: v for k, v in kw.items() if not k.startswith("_")}
+    d = next((e for e in entries if e["kw"] == mine), None)
+    if d is None:
         return None
     req = d["sectors_per_hit_sample"] * samples_per_launch
     achieved = req / (ms * 1e-3 * sm_clk * n_sm)
@@ -205,9 +210,8 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
         achieved = bytes_ / (ms * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
         out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s"}
-        # sectors per hit sample were captured on cfg1's model (any number of objects)
-        rq = request_roofline(samples_per_launch, ms, sm_clk, 148) if \
-            {k: v for k, v in kw.items() if not k.startswith("_")} == cfg1_kwargs(1) else None
+        # sectors per hit sample captured on the same model (any number of objects)
+        rq = request_roofline(kw, samples_per_launch, ms, sm_clk, 148)
         if rq:
             out["request_roofline"] = rq
     elif dom in ("fwd_fp32", "bwd_fp32"):

@@ -98,7 +98,17 @@ def main(tag, launch_csv, rep, hit_samples=None):
         req = {"kernel": "k_fused_mixed", "profile": f"profiles/{tag}_ncu.json",
                "sectors_per_launch": sum(sec) / len(sec), "hit_samples_per_launch": float(hit_samples),
                "sectors_per_hit_sample": sum(sec) / len(sec) / float(hit_samples)}
-        json.dump(req, open(os.path.join(ROOT, "profiles", "ncu_requests.json"), "w"), indent=1)
+        # (cfg1 entry of profiles/ncu_requests.json; other workloads are added by hand)
+        path = os.path.join(ROOT, "profiles", "ncu_requests.json")
+        try:
+            allreq = json.load(open(path))
+        except Exception:
+            allreq = {"entries": []}
+        req["workload"] = "cfg1"
+        req["kw"] = {"levels": 16, "log2_T": 16, "base_res": 16, "finest_res": 512.0, "res_cap": 0,
+                     "samples_per_ray": 64, "rays_per_iter": 4096, "precision": 1, "seed": 1}
+        allreq["entries"] = [e for e in allreq.get("entries", []) if e.get("workload") != "cfg1"] + [req]
+        json.dump(allreq, open(path, "w"), indent=1)
         md += ["## request rate", "", f"- L1 sector requests (global ld + red) per hit ray-sample: "
                f"{req['sectors_per_hit_sample']:.1f}", ""]
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu.md"), "w").write("\n".join(md) + "\n")
