@@ -259,9 +259,15 @@ def measure_inference(ctx, h, ob, frame, torch):
     t0 = time.perf_counter()
     ctx.render(h, frame.T_wc, frame.K, 640, 480, 128)
     r_s = time.perf_counter() - t0
+    peaks, src = load_measured_peaks()
+    q_gbs = P.shape[0] * 16 * 8 * 4 / (q_ms * 1e-3) / 1e9   # 16 levels x 8 corners x 4 B (fp16 F=2) per point
     return {"query_density": {"points_per_s": P.shape[0] / (q_ms * 1e-3), "ms_per_lattice": q_ms,
                               "points": int(P.shape[0]), "what": "128^3 vertex lattice of the trained object, "
-                              "device buffers, CUDA events (mixed path: fp16 tables + tcgen05 first layer)"},
+                              "device buffers, CUDA events (mixed path: fp16 tables + tcgen05 first layer)",
+                              "roofline": {"bound": "hbm", "achieved": q_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                           "frac": q_gbs / peaks["hbm_gbs"], "peak_source": src,
+                                           "note": "algorithmic gather bytes; the 3.4 MB table is L2-resident, so the "
+                                                   "random-request rate, not HBM, binds it"}},
             "render": {"rays_per_s": 640 * 480 / r_s, "ms_per_frame": r_s * 1e3, "samples_per_ray": 128,
                        "what": "one 640x480 frame, host outputs, wall clock (mixed path: tensor-core forward of midpoint samples + compositing)"}}
 
