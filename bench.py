@@ -451,6 +451,19 @@ def run_ours(args):
     e2e_max_ms, tot_e2e, e2e_value = reduce_throughput(e2e_s * 1e3, e2e_samples, pg, device="cuda")
 
     infer = measure_inference(ctx, objs[0], ob, scene.frames[0], torch) if rank == 0 else None
+    if infer is not None:
+        # cfg4 (ii): render_scene of every object on this GPU from 10 poses (640x480,
+        # <= 128 samples per segment, host outputs)
+        poses = scene.frames[:10]
+        ctx.render_scene(objs, poses[0].T_wc, poses[0].K, 640, 480, 128)
+        t0 = time.perf_counter()
+        for fr in poses:
+            ctx.render_scene(objs, fr.T_wc, fr.K, 640, 480, 128)
+        rs_s = (time.perf_counter() - t0) / len(poses)
+        infer["render_scene"] = {"objects": len(objs), "poses": len(poses), "ms_per_frame": rs_s * 1e3,
+                                 "rays_per_s": 640 * 480 / rs_s,
+                                 "what": "romap_render_scene of all objects, 640x480, 128 samples per segment, "
+                                         "host outputs, wall clock"}
     if rank == 0:
         rf = roofline(prof, kw, precision, samples / args.steps, len(objs))
         paper_sps = paper_baseline_samples_per_s(kw)
