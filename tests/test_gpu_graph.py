@@ -97,3 +97,27 @@ def test_graph_multi_object_with_keyframe_appends():
             assert s[k]["step"] == 20 * (call + 1)
             assert abs(s[k]["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (call, k, s[k], o)
     c.close()
+
+
+def test_graph_rebuilt_when_the_batch_changes():
+    """The cached graph is keyed by the batch (objects, slots, buffers): one object,
+    then two (the ray buffers grow), then the other alone -- every call replays a
+    graph built for its own batch, with geometry bit-exact against the oracle."""
+    c = R.Context(0)
+    sc = scenes.room_scene(7, n_objects=2, n_frames=6, W=160, H=120, f=131.25, room_half=1.5)
+    kw = dict(CFG0M, rays_per_iter=128, seed=7)
+    pairs = [make_pair(R, c, sc, kw, param_seed=70 + k, inst=ob.instance_id, obj_id=500 + k, avoid_kinks=False)
+             for k, ob in enumerate(sc.objects[:2])]
+    (h1, s1), (h2, s2) = pairs
+    for batch in ([0], [0, 1], [1]):
+        hs = [pairs[k][0] for k in batch]
+        out = c.train_step(hs, 18)                 # one 16-iteration chunk + 2
+        for k, st in zip(batch, out):
+            hits = 0
+            for _ in range(18):
+                o, _, _ = O.train_iteration(pairs[k][1])
+                hits += o["hit_rays"]
+            assert st["hit_rays"] == hits, (batch, k, st["hit_rays"], hits)
+            assert abs(st["l_total"] - o["l_total"]) <= 5e-2 * o["l_total"], (batch, k, st, o)
+    assert c.object_info(h1)["step"] == 36 and c.object_info(h2)["step"] == 36
+    c.close()
