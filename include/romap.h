@@ -176,9 +176,14 @@ typedef struct {
 typedef void* (*romap_alloc_fn)(size_t bytes, void* user);
 typedef void (*romap_free_fn)(void* ptr, void* user);
 
-/* Create a context on CUDA device `device`, enqueueing on `cuda_stream`
- * (a cudaStream_t; NULL = the legacy default stream).  alloc/free: optional
- * device allocator callbacks (e.g. torch's caching allocator); NULL -> cudaMalloc. */
+/* Create a context on CUDA device `device`, enqueueing on `cuda_stream` (a
+ * cudaStream_t).  NULL: the context creates and owns a stream of its own (a
+ * blocking stream, so it stays ordered with work on the legacy default stream;
+ * the a9 CUDA graph cannot be captured on the legacy stream itself).  alloc/free: optional device allocator callbacks
+ * (e.g. torch's caching allocator, "PyTorch only for device memory",
+ * BASELINE north_star): every device buffer of the context and its objects is
+ * taken from alloc(bytes, user) and returned with free(ptr, user); both NULL ->
+ * cudaMalloc / cudaFree.  E_INVALID if exactly one of them is NULL. */
 romap_status romap_ctx_create(int32_t device, void* cuda_stream, romap_alloc_fn alloc, romap_free_fn free_fn,
                               void* user, romap_ctx** out);
 romap_status romap_ctx_destroy(romap_ctx* ctx);
@@ -269,10 +274,14 @@ romap_status romap_train_pending(romap_ctx* ctx, int32_t chunk, int32_t max_iter
  * pose, intrinsics) into a queue of queue_cap frames and returns at once: *queued =
  * 1, or 0 when the queue is full (the frame is dropped, the producer never waits).
  * While the worker runs every other call on the context returns E_STATE.
- * async_stop joins the worker after draining the queue, and first trains every
- * pending budget when finish_pending; it returns the worker's first error, if any. */
+ * A queued frame that fails validation (unknown object, instance not visible in
+ * the mask: E_NOT_FOUND / E_INVALID of romap_offer_observation) is counted as
+ * rejected and the worker goes on; any other error (CUDA, non-finite) stops the
+ * worker, after which async_offer returns E_STATE.  async_stop joins the worker
+ * after draining the queue, and first trains every pending budget when
+ * finish_pending; it returns the worker's first error, if any. */
 typedef struct {
-    int64_t offered, dropped, accepted, iterations, max_queue_depth;
+    int64_t offered, dropped, accepted, iterations, max_queue_depth, rejected;
 } romap_async_stats;
 romap_status romap_async_start(romap_ctx* ctx, int32_t chunk, float alpha_deg, int32_t iters_per_update,
                                int32_t queue_cap);
@@ -342,6 +351,17 @@ romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes);
  * inputs (host pointers, row-major fp32). */
 romap_status romap_selftest_mma(const float* X, const float* W, const float* Dl, float* out1, float* out2,
                                 float* out3);
+
+/* Deterministic-reduction mode (tests; SURVEY.md 8(c) "bitwise in a
+ * deterministic-reduction debug mode").  on = 1: every
+ * later train_step / forward_backward writes each table-gradient, weight-gradient
+ * and loss contribution to a record instead of an fp32 atomic, and fixed-order
+ * reductions (k_det.cu) apply them: within an object in sample / tile / ray
+ * order.  Results are then bitwise reproducible run to run, equal between graph
+ * replays and plain launches, and equal for an object trained in a batch or
+ * alone.  Costs ~16 B of records per (sample, level, corner) and a radix sort per
+ * iteration (not for timing).  on = 0 (default): fp32 atomics. */
+romap_status romap_set_deterministic(romap_ctx* ctx, int32_t on);
 
 /* Wait for all work on the context's stream. */
 romap_status romap_sync(romap_ctx* ctx);

@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(256) k_render_loss(CfgDev cfg, const ObjDev* _
                                                      const float* __restrict__ sigma, const float* __restrict__ rgb,
                                                      const float* __restrict__ dist, const float* __restrict__ delta,
                                                      float* __restrict__ dsigma, float* __restrict__ drgb,
-                                                     double* __restrict__ loss_acc, int* __restrict__ nonfinite) {
+                                                     double* __restrict__ loss_acc, int* __restrict__ nonfinite,
+                                                     DetBufs det) {
     __shared__ float sm_loss[8][4];
     __shared__ int sm_slot[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -318,6 +319,12 @@ __global__ void __launch_bounds__(256) k_render_loss(CfgDev cfg, const ObjDev* _
             }
         }
     }
+    // deterministic mode: per-ray loss sums, reduced in ray order by k_det.cu
+    if (det.ray_loss) {
+        if (lane == 0 && ray < n_rays)
+            *reinterpret_cast<float4*>(det.ray_loss + 4LL * ray) = make_float4(lossv[0], lossv[1], lossv[2], lossv[3]);
+        return;
+    }
     // per-object loss sums: block reduction when all warps share one slot
     if (lane == 0) {
 #pragma unroll
@@ -343,10 +350,10 @@ __global__ void __launch_bounds__(256) k_render_loss(CfgDev cfg, const ObjDev* _
 
 void launch_render_loss(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
                         const float* sigma, const float* rgb, const float* dist, const float* delta, float* dsigma,
-                        float* drgb, double* loss_acc, int* nonfinite) {
+                        float* drgb, double* loss_acc, int* nonfinite, const DetBufs& det) {
     if (n_rays == 0) return;
     k_render_loss<<<(n_rays + 7) / 8, 256, 0, lc.st>>>(cfg, objs, rays, n_rays, sigma, rgb, dist, delta, dsigma, drgb,
-                                                       loss_acc, nonfinite);
+                                                       loss_acc, nonfinite, det);
 }
 
 // ---------------------------------------------------------------------------
@@ -354,13 +361,16 @@ void launch_render_loss(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
 #define SM_LD 65
 
 // dW[j][k] += sum_s delta[s][j] * in[s][k] over the tile, one atomic per weight
-__device__ __forceinline__ void tile_dw(const float* sm_d, const float* sm_i, int OUT, int IN, float* gW) {
+// (store: the deterministic mode's per-tile partial, plain stores)
+__device__ __forceinline__ void tile_dw(const float* sm_d, const float* sm_i, int OUT, int IN, float* gW,
+                                        bool store = false) {
     for (int e = threadIdx.x; e < OUT * IN; e += blockDim.x) {
         int j = e / IN, k = e - j * IN;
         float acc = 0.f;
 #pragma unroll 8
         for (int s = 0; s < ROMAP_TILE; ++s) acc += sm_d[s * SM_LD + j] * sm_i[s * SM_LD + k];
-        if (acc != 0.f) atomicAdd(gW + e, acc);
+        if (store) gW[e] = acc;
+        else if (acc != 0.f) atomicAdd(gW + e, acc);
     }
 }
 
@@ -368,7 +378,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
                                                   const RayRec* __restrict__ rays, int n_rays,
                                                   const float* __restrict__ sigma, const float* __restrict__ rgb,
                                                   const float* __restrict__ dsigma, const float* __restrict__ drgb,
-                                                  const float* __restrict__ act, long long stride) {
+                                                  const float* __restrict__ act, long long stride, DetBufs det) {
     extern __shared__ float smem[];
     float* sm_d = smem;                       // [128][65]
     float* sm_i = smem + ROMAP_TILE * SM_LD;  // [128][65]
@@ -382,7 +392,8 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
     const ObjDev& ob = objs[slot];
     const bool active = (rr.flags & RF_ACTIVE) != 0;
     const float* mlp = ob.p32 + cfg.n_table;
-    float* gm = ob.g32 + cfg.n_table;
+    const bool dst = det.dw != nullptr;            // deterministic mode: per-tile partials, records
+    float* gm = dst ? det.dw + (long long)blockIdx.x * cfg.n_mlp : ob.g32 + cfg.n_table;
     const int LF = cfg.LF;
     const float* a_feat = act + s;
     const float* a_h1 = a_feat + (long long)LF * stride;
@@ -409,7 +420,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
 #pragma unroll
     for (int k = 0; k < ROMAP_WIDTH; ++k) { v64[k] = active ? a_g2[(long long)k * stride] : 0.f; si[k] = v64[k]; }
     __syncthreads();
-    tile_dw(sm_d, sm_i, 3, ROMAP_WIDTH, gm + cfg.w_off[4]);
+    tile_dw(sm_d, sm_i, 3, ROMAP_WIDTH, gm + cfg.w_off[4], dst);
     __syncthreads();
     // dg2 = W5^T dc . (g2 > 0)
     float dg[ROMAP_WIDTH];
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
 #pragma unroll
     for (int k = 0; k < ROMAP_WIDTH; ++k) { v64[k] = active ? a_g1[(long long)k * stride] : 0.f; si[k] = v64[k]; }
     __syncthreads();
-    tile_dw(sm_d, sm_i, ROMAP_WIDTH, ROMAP_WIDTH, gm + cfg.w_off[3]);
+    tile_dw(sm_d, sm_i, ROMAP_WIDTH, ROMAP_WIDTH, gm + cfg.w_off[3], dst);
     __syncthreads();
     // dg1 = W4^T dg2 . (g1 > 0)
     float dg1[ROMAP_WIDTH];
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
 #pragma unroll
     for (int k = 0; k < ROMAP_SH; ++k) si[ROMAP_DOUT + k] = active ? sh[k] : 0.f;
     __syncthreads();
-    tile_dw(sm_d, sm_i, ROMAP_WIDTH, ROMAP_CIN, gm + cfg.w_off[2]);
+    tile_dw(sm_d, sm_i, ROMAP_WIDTH, ROMAP_CIN, gm + cfg.w_off[2], dst);
     __syncthreads();
     // dr = (W3^T dg1)[:16]; dr0 += dsigma * act'(r0)
     float dr[ROMAP_DOUT];
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
 #pragma unroll
     for (int k = 0; k < ROMAP_WIDTH; ++k) { v64[k] = active ? a_h1[(long long)k * stride] : 0.f; si[k] = v64[k]; }
     __syncthreads();
-    tile_dw(sm_d, sm_i, ROMAP_DOUT, ROMAP_WIDTH, gm + cfg.w_off[1]);
+    tile_dw(sm_d, sm_i, ROMAP_DOUT, ROMAP_WIDTH, gm + cfg.w_off[1], dst);
     __syncthreads();
     // dh1 = W2^T dr . (h1 > 0)
 #pragma unroll
@@ -484,9 +495,13 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
         if (k < LF) si[k] = feat[k];
     }
     __syncthreads();
-    tile_dw(sm_d, sm_i, ROMAP_WIDTH, LF, gm + cfg.w_off[0]);
+    tile_dw(sm_d, sm_i, ROMAP_WIDTH, LF, gm + cfg.w_off[0], dst);
     // dfeat = W1^T dh1
-    if (!active) return;
+    if (!active) {
+        if (dst)
+            for (int r8 = 0; r8 < cfg.L * 8; ++r8) det.key[s * cfg.L * 8 + r8] = DET_NO_KEY;
+        return;
+    }
     float dfeat[ROMAP_MAX_LF];
 #pragma unroll
     for (int k = 0; k < ROMAP_MAX_LF; ++k) {
@@ -511,7 +526,13 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
             for (int b = 0; b < 8; ++b) {
                 int e = corner_entry(cl, b, res, cfg.dense[l], cfg.T);
                 float w = corner_weight(cl, b);
-                red_add_f2(gt + cfg.off[l] + e, w * dfeat[2 * l], w * dfeat[2 * l + 1]);
+                if (dst) {
+                    const long long rec = (s * cfg.L + l) * 8 + b;
+                    det.key[rec] = ((unsigned long long)slot << 32) | (unsigned long long)(cfg.off[l] + e);
+                    det.val[rec] = make_float2(w * dfeat[2 * l], w * dfeat[2 * l + 1]);
+                } else {
+                    red_add_f2(gt + cfg.off[l] + e, w * dfeat[2 * l], w * dfeat[2 * l + 1]);
+                }
             }
         }
     }
@@ -519,7 +540,7 @@ __global__ void __launch_bounds__(128) k_bwd_fp32(CfgDev cfg, const ObjDev* __re
 
 void launch_bwd_fp32(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
                      const float* sigma, const float* rgb, const float* dsigma, const float* drgb, const float* act,
-                     long long act_stride) {
+                     long long act_stride, const DetBufs& det) {
     long long S = (long long)n_rays * cfg.N;
     if (S == 0) return;
     size_t smem = 2 * ROMAP_TILE * SM_LD * sizeof(float);
@@ -529,7 +550,7 @@ void launch_bwd_fp32(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs,
         attr = true;
     }
     k_bwd_fp32<<<(unsigned)(S / ROMAP_TILE), ROMAP_TILE, smem, lc.st>>>(cfg, objs, rays, n_rays, sigma, rgb, dsigma,
-                                                                         drgb, act, act_stride);
+                                                                         drgb, act, act_stride, det);
 }
 
 // ---------------------------------------------------------------------------

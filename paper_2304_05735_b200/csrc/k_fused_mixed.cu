@@ -35,7 +35,20 @@
 #include "tc_sm100.cuh"
 #include "hash_fp16.cuh"
 
+// deterministic-reduction build (-DROMAP_DET, k_fused_mixed_det.o; k_det.cu):
+// the same kernel writing per-record gradient / loss contributions instead of
+// atomics (DetBufs, romap_internal.cuh); tests only
+#ifdef ROMAP_DET
+#define DET_PARAM , DetBufs det
+#define DET_ARG , det
+#define FUSED_LAUNCH launch_fused_mixed_det
+#define k_fused_mixed k_fused_mixed_det
+#else
+#define DET_PARAM
+#define DET_ARG
+#define FUSED_LAUNCH launch_fused_mixed
 bool fused_mixed_available() { return true; }
+#endif
 
 // optional phase timing (build with -DROMAP_FUSED_PROF): clock64 cycles per
 // phase summed over CTAs, read back with romap_debug_fused_prof
@@ -319,12 +332,21 @@ __device__ void load_weights(uint8_t* smem, const __half* __restrict__ mlp16, co
 
 // flush the dW accumulators (TMEM) and loss sums of one object (M threads).
 // M=64 accumulators: row i lives in TMEM lane 32 (i / 16) + i % 16.
-template <int LF>
-__device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* misc, double* loss_acc, int slot,
+// (STORE: plain stores into a per-tile buffer laid out like the MLP block, the
+// deterministic mode's per-tile partials; else fp32 REDs into the gradients)
+__device__ __forceinline__ void emit4(bool store, float* p, float a, float b, float c, float d) {
+    if (store) *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+    else red_add_f4(reinterpret_cast<float4*>(p), a, b, c, d);
+}
+__device__ __forceinline__ void emit1(bool store, float* p, float a) {
+    if (store) *p = a;
+    else red_add_f1(p, a);
+}
+template <int LF, bool STORE = false>
+__device__ void m_flush(const CfgDev& cfg, float* gm, uint32_t tm, Misc* misc, double* loss_acc, int slot,
                         bool have_dw) {
     const int m = threadIdx.x - NG, mw = m >> 5, lane = m & 31;
     const float inv = 1.0f / cfg.loss_scale;
-    float* gm = ob.g32 + cfg.n_table;
     if (have_dw) {
         const int row = mw * 16 + lane;
         const bool on = lane < 16;
@@ -334,8 +356,7 @@ __device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* 
             if (on)
 #pragma unroll
                 for (int k = 0; k < 16; k += 4)
-                    red_add_f4(reinterpret_cast<float4*>(dst + k), v[k] * inv, v[k + 1] * inv, v[k + 2] * inv,
-                               v[k + 3] * inv);
+                    emit4(STORE, dst + k, v[k] * inv, v[k + 1] * inv, v[k + 2] * inv, v[k + 3] * inv);
         };
 #pragma unroll
         for (int c0 = 0; c0 < LF; c0 += 16) rows4(TM_DW1 + c0, gm + cfg.w_off[0] + row * LF + c0);
@@ -349,7 +370,7 @@ __device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* 
             tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, TM_DW2), v);
             if (on)
 #pragma unroll
-                for (int o = 0; o < 4; ++o) red_add_f1(gm + cfg.w_off[hl] + o * 64 + row, v[o] * inv);
+                for (int o = 0; o < 4; ++o) emit1(STORE, gm + cfg.w_off[hl] + o * 64 + row, v[o] * inv);
         } else {
 #pragma unroll
         for (int c0 = 0; c0 < 32; c0 += 16) rows4(TM_DW3 + c0, gm + cfg.w_off[2] + row * 32 + c0);
@@ -359,11 +380,11 @@ __device__ void m_flush(const CfgDev& cfg, const ObjDev& ob, uint32_t tm, Misc* 
         tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, TM_DW2), v);
         if (on)
 #pragma unroll
-            for (int o = 0; o < 16; ++o) red_add_f1(gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
+            for (int o = 0; o < 16; ++o) emit1(STORE, gm + cfg.w_off[1] + o * 64 + row, v[o] * inv);
         tc::tmem_ld16_sync(tc::taddr(tm, mw * 32, TM_DW5), v);
         if (on)
 #pragma unroll
-            for (int o = 0; o < 3; ++o) red_add_f1(gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
+            for (int o = 0; o < 3; ++o) emit1(STORE, gm + cfg.w_off[4] + o * 64 + row, v[o] * inv);
         }
     }
     tc::bar_sync(BAR_M, NM);
@@ -412,7 +433,7 @@ __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint
 template <int L>
 __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
                                        const RayRec* __restrict__ rays, const float4* __restrict__ srec, int tile0,
-                                       int tstride, int n, uint8_t* smem, Misc* misc, uint32_t tm) {
+                                       int tstride, int n, uint8_t* smem, Misc* misc, uint32_t tm DET_PARAM) {
     constexpr int LF = 2 * L;
     const int t = threadIdx.x, r = t & (TILE - 1), lane = t & 31, q4 = (t >> 5) & 3, WG = t >> 7;
     const int N = cfg.N;
@@ -431,10 +452,16 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
     float2* g_cur = nullptr;
     float um[NB][3];                              // positions of tiles it-1 .. it-NB (-1: inactive)
     float2* gm[NB];                               // their gradient tables
+#ifdef ROMAP_DET
+    int sl[NB];                                   // their object slots (record keys)
+#endif
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         um[k][0] = um[k][1] = um[k][2] = -1.f;
         gm[k] = nullptr;
+#ifdef ROMAP_DET
+        sl[k] = 0;
+#endif
     }
 
 #ifdef ROMAP_FUSED_PROF
@@ -542,6 +569,23 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         v[4 * p + 2] = wb * g0;
                         v[4 * p + 3] = wb * g1;
                     }
+#ifdef ROMAP_DET
+                    {
+                        // one record per corner (sample, level, corner order); k_det.cu sums
+                        // each entry's records in that order
+                        const long long s_sc = ((long long)tile0 + (long long)(it - NB) * tstride) * TILE + r;
+                        const long long rec = (s_sc * L + lv_[q]) * 8;
+                        const unsigned long long kb = (unsigned long long)sl[NB - 1] << 32;
+#pragma unroll
+                        for (int c8 = 0; c8 < 8; ++c8) {
+                            det.key[rec + c8] = as_ ? (kb | (unsigned long long)(off[q] + es[c8])) : DET_NO_KEY;
+                            det.val[rec + c8] = make_float2(v[2 * c8], v[2 * c8 + 1]);
+                        }
+                    }
+                    if (false) {
+#else
+                    {
+#endif
                     // fine levels: every lane issues (an inactive sample adds zeros: one
                     // request, no branch); coarse levels: the run leaders of active samples
                     bool issue = true;
@@ -586,6 +630,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                                                : make_float4(n0, n1, v[4 * p], v[4 * p + 1]);
                         xred4(reinterpret_cast<float4*>(gl + opaque_u32(ea & ~1u)), w4.x, w4.y, w4.z, w4.w);
                         if (!pair) xred2(gl + eb, v[4 * p + 2], v[4 * p + 3]);
+                    }
                     }
                     }
                 }
@@ -651,10 +696,16 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
 #pragma unroll
             for (int k = 0; k < 3; ++k) um[q][k] = um[q - 1][k];
             gm[q] = gm[q - 1];
+#ifdef ROMAP_DET
+            sl[q] = sl[q - 1];
+#endif
         }
 #pragma unroll
         for (int k = 0; k < 3; ++k) um[0][k] = (dg && ag) ? ug[k] : -1.f;
         gm[0] = g_cur;
+#ifdef ROMAP_DET
+        sl[0] = slot_tab;
+#endif
         FP_MARK(g_w2);
         FP_ACC(10, g_w1, g_w2);
         if (WG == 1) FP_ACC(11, g_w1, g_w2);         // warpgroup G1 alone (G0 = slot 10 - slot 11)
@@ -695,7 +746,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
                                        const float* __restrict__ sdelta, int tile0, int tstride, int n, uint8_t* smem,
                                        Misc* misc,
                                        uint32_t tm, double* __restrict__ loss_acc, int* __restrict__ nonfinite,
-                                       float* __restrict__ dbg) {
+                                       float* __restrict__ dbg DET_PARAM) {
     constexpr int LF = 2 * L;
     const int m = threadIdx.x - NG, mw = m >> 5;
     const bool leader = m == 0;
@@ -750,7 +801,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
                 // every MMA of the previous tile (they read W and write dW) has completed
                 tc::mbar_wait(&misc->tile_done[(j - 1) % NB], ((j - 1) / NB) & 1);
                 tc::fence_after();
-                m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
+                m_flush<LF>(cfg, objs[cur].g32 + cfg.n_table, tm, misc, loss_acc, cur, !dw_fresh);
             }
             const ObjDev& ob = objs[rr.slot];
             load_weights(smem, ob.p16 + cfg.n_table, cfg, LF);
@@ -926,12 +977,23 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
             }
             gCb = gC[0] * bgc[0] + gC[1] * bgc[1] + gC[2] * bgc[2];
             if (i == 0) {
+#ifdef ROMAP_DET
+                *reinterpret_cast<float4*>(det.ray_loss + 4 * (s >> lgN)) =
+                    make_float4(cls == CLS_OBJ ? ne : 0.f, cls == CLS_OBJ ? 0.f : ne, has_depth ? fabsf(ed) : 0.f,
+                                cls == CLS_BG ? sums[4] : 0.f);
+#else
                 atomicAdd(&misc->loss[cls == CLS_OBJ ? 0 : 1], ne);
                 if (has_depth) atomicAdd(&misc->loss[2], fabsf(ed));
                 if (cls == CLS_BG) atomicAdd(&misc->loss[3], sums[4]);
+#endif
                 if (!isfinite(ne) || !isfinite(sums[4])) atomicOr(nonfinite, 1);
             }
         }
+#ifdef ROMAP_DET
+        else if (i == 0) {
+            *reinterpret_cast<float4*>(det.ray_loss + 4 * (s >> lgN)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#endif
         const float gc = gC[0] * c[0] + gC[1] * c[1] + gC[2] * c[2];
         // S = sum_{j>i} w_j gc_j = gC . suf(c), Sd = sum_{j>i} w_j dist_j (gC is per ray)
         const float S = gC[0] * R.suf[0] + gC[1] * R.suf[1] + gC[2] * R.suf[2], Sd = R.suf[3];
@@ -1093,7 +1155,16 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
                             tc::idesc_f16(64, LF, true, true), (dw_fresh && ks == 0) ? 0 : 1);
             tc::commit(&misc->tile_done[b]);
         }
+#ifdef ROMAP_DET
+        // this tile's dW alone (every tile starts its accumulators fresh) into its
+        // per-tile partial; k_det.cu sums an object's tiles in tile order
+        tc::mbar_wait(&misc->tile_done[b], (j / NB) & 1);
+        tc::fence_after();
+        m_flush<LF, true>(cfg, det.dw + tile * (long long)cfg.n_mlp, tm, misc, loss_acc, cur, true);
+        dw_fresh = true;
+#else
         dw_fresh = false;
+#endif
         FP_MARK(m_t5);
         FP_ACC(6, m_t0, m_t1);
         FP_ACC(1, m_t1, m_t2);
@@ -1105,7 +1176,7 @@ __device__ __forceinline__ void m_loop(const CfgDev& cfg, const ObjDev* __restri
     if (cur >= 0) {
         tc::mbar_wait(&misc->tile_done[(n - 1) % NB], ((n - 1) / NB) & 1);
         tc::fence_after();
-        m_flush<LF>(cfg, objs[cur], tm, misc, loss_acc, cur, !dw_fresh);
+        m_flush<LF>(cfg, objs[cur].g32 + cfg.n_table, tm, misc, loss_acc, cur, !dw_fresh);
     }
     FP_MARK(m_end);
     FP_ACC(0, m_start, m_end);
@@ -1120,7 +1191,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
                                                        const float4* __restrict__ srec,
                                                        const float* __restrict__ sdelta, int n_tiles,
                                                        int tiles_per_cta, double* __restrict__ loss_acc,
-                                                       int* __restrict__ nonfinite, float* __restrict__ dbg) {
+                                                       int* __restrict__ nonfinite, float* __restrict__ dbg DET_PARAM) {
     extern __shared__ __align__(1024) uint8_t smem[];
     Misc* misc = reinterpret_cast<Misc*>(smem + OFF_MISC);
     const int t = threadIdx.x, warp = t >> 5;
@@ -1163,9 +1234,10 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     const int n = tile0 < n_tiles ? (n_tiles - 1 - tile0) / tstride + 1 : 0;
     if (n > 0) {
         if (warp < NG / 32)
-            g_loop<L>(cfg, objs, rays, srec, tile0, tstride, n, smem, misc, tm);
+            g_loop<L>(cfg, objs, rays, srec, tile0, tstride, n, smem, misc, tm DET_ARG);
         else
-            m_loop<L, NET>(cfg, objs, rays, srec, sdelta, tile0, tstride, n, smem, misc, tm, loss_acc, nonfinite, dbg);
+            m_loop<L, NET>(cfg, objs, rays, srec, sdelta, tile0, tstride, n, smem, misc, tm, loss_acc, nonfinite, dbg
+                           DET_ARG);
     }
     tc::fence_before();
     __syncthreads();
@@ -1177,9 +1249,9 @@ __global__ void __launch_bounds__(NT, 1) k_fused_mixed(CfgDev cfg, const ObjDev*
     if (warp == 0) tc::tmem_dealloc(tm, TM_COLS);
 }
 
-void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
-                        const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
-                        float* dbg) {
+void FUSED_LAUNCH(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
+                  const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
+                  float* dbg DET_PARAM) {
     const long long S = (long long)n_rays * cfg.N;
     const int n_tiles = (int)(S / TILE);
     if (n_tiles == 0) return;
@@ -1206,5 +1278,5 @@ void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* ob
     la[0].val.programmaticStreamSerializationAllowed = 1;
     lcfg.attrs = la;
     lcfg.numAttrs = pdl_enabled() ? 1 : 0;
-    cudaLaunchKernelEx(&lcfg, kern, cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc, nonfinite, dbg);
+    cudaLaunchKernelEx(&lcfg, kern, cfg, objs, rays, srec, sdelta, n_tiles, per, loss_acc, nonfinite, dbg DET_ARG);
 }

@@ -30,6 +30,9 @@
 void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
                         const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
                         float* dbg_ray_grads);
+void launch_fused_mixed_det(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
+                            const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
+                            float* dbg_ray_grads, DetBufs det);
 bool fused_mixed_available();
 void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const RayRec* rays, int n_rays,
                       float* sigma, float* rgb, float* dist, float* delta);
@@ -95,9 +98,13 @@ struct Object {
 enum LastCall { LAST_NONE = 0, LAST_TRAIN = 1, LAST_FWDBWD = 2 };
 
 enum Stage { ST_RAYGEN = 0, ST_FWD, ST_RENDER_LOSS, ST_BWD, ST_FUSED, ST_ADAM, ST_STEP_INC, ST_ZERO_GRADS, ST_FLUSH,
-             ST_COUNT };
+             ST_DET, ST_GRAPH, ST_COUNT };
+// (det_reduce: the deterministic mode's fixed-order reductions; graph_replay:
+// cudaGraphLaunch calls of a captured K-iteration chunk, its kernels are counted
+// under their own stages)
 static const char* kStageNames[ST_COUNT] = {"raygen", "fwd_fp32", "render_loss", "bwd_fp32", "fused_mixed",
-                                             "adam", "step_inc", "zero_grads", "l2_flush"};
+                                             "adam", "step_inc", "zero_grads", "l2_flush", "det_reduce",
+                                             "graph_replay"};
 
 // per-stage launch counters and (optional) CUDA-event timing on the ctx stream
 struct Profiler {
@@ -135,7 +142,7 @@ struct AsyncState {
     bool stop = false, finish = false;
     int chunk = 100, iters_per_update = 300, cap = 64;
     float alpha_deg = 25.f;
-    long long offered = 0, dropped = 0, accepted = 0, iterations = 0, max_depth = 0;
+    long long offered = 0, dropped = 0, accepted = 0, iterations = 0, max_depth = 0, rejected = 0;
     romap_status error = 0;
     std::string error_msg;
 };
@@ -143,6 +150,7 @@ struct AsyncState {
 struct romap_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
+    bool own_stream = false;     // created by romap_ctx_create (the caller passed NULL)
     romap_alloc_fn alloc = nullptr;
     romap_free_fn free_fn = nullptr;
     void* user = nullptr;
@@ -189,6 +197,16 @@ struct romap_ctx {
     AsyncState* async = nullptr;    // non-null while the async worker runs
     void* flush_buf = nullptr;
     size_t flush_bytes = 0;
+    // deterministic-reduction mode (romap_set_deterministic; DetBufs, k_det.cu)
+    bool det_on = false;
+    void* det_mem = nullptr;
+    size_t det_cap = 0;          // bytes
+    DetBufs det{};
+    unsigned long long* det_key_sorted = nullptr;
+    unsigned* det_iota = nullptr;
+    unsigned* det_perm = nullptr;
+    void* det_temp = nullptr;
+    size_t det_temp_bytes = 0;
     // a9: CUDA graph of one chunk of K training iterations of the mixed path
     // (raygen of K slices, then K x [flush], fused, Adam), replayed while the batch,
     // its config and every buffer it touches stay the same
@@ -196,6 +214,7 @@ struct romap_ctx {
         cudaGraphExec_t exec = nullptr;
         CfgDev cfg;
         int n = 0, total_slots = 0, K = 0;
+        bool det = false;
         const void* ptrs[8] = {};
         size_t flush_bytes = 0;
     } tg;
@@ -465,6 +484,17 @@ romap_status romap_ctx_create(int32_t device, void* cuda_stream, romap_alloc_fn 
     romap_ctx* ctx = new romap_ctx();
     ctx->device = device;
     ctx->st = (cudaStream_t)cuda_stream;
+    if (!ctx->st) {
+        // no stream given: a stream of our own (a CUDA graph cannot be captured on
+        // the legacy NULL stream, a9).  A blocking stream: it stays ordered with work
+        // the caller enqueues on the legacy default stream (e.g. torch's)
+        if (cudaStreamCreate(&ctx->st) != cudaSuccess) {
+            cudaGetLastError();
+            delete ctx;
+            return fail(ROMAP_E_CUDA, "cudaStreamCreate failed");
+        }
+        ctx->own_stream = true;
+    }
     ctx->alloc = alloc;
     ctx->free_fn = free_fn;
     ctx->user = user;
@@ -472,6 +502,7 @@ romap_status romap_ctx_create(int32_t device, void* cuda_stream, romap_alloc_fn 
     ctx->single_d = (ObjDev*)dalloc(ctx, sizeof(ObjDev));
     ctx->cam_d = (KfDev*)dalloc(ctx, sizeof(KfDev));
     if (!ctx->single_d || !ctx->cam_d) {
+        if (ctx->own_stream) cudaStreamDestroy(ctx->st);
         delete ctx;
         return fail(ROMAP_E_OOM, "context allocation failed");
     }
@@ -515,9 +546,11 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->nonfinite_d);
     dfree(ctx, ctx->io_d);
     dfree(ctx, ctx->flush_buf);
+    dfree(ctx, ctx->det_mem);
     if (ctx->tg.exec) cudaGraphExecDestroy(ctx->tg.exec);
     prof_collect(ctx);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->st);
     delete ctx;
     return ROMAP_OK;
 }
@@ -877,6 +910,40 @@ static romap_status upload_batch(romap_ctx* ctx, Batch& b, bool train_scratch) {
     return ROMAP_OK;
 }
 
+// deterministic mode: record / partial buffers of one iteration of batch b (DetBufs)
+static romap_status ensure_det(romap_ctx* ctx, const Batch& b) {
+    const long long S = (long long)b.total_slots * b.cfg.N;
+    const long long n_rec = S * b.cfg.L * 8, tiles = S / ROMAP_TILE;
+    if (n_rec >= (1LL << 31)) return fail(ROMAP_E_INVALID, "deterministic mode: batch too large (%lld records)", n_rec);
+    const size_t temp = det_sort_temp_bytes(n_rec, (int)b.dev.size());
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t sz[7] = {al(8 * n_rec), al(8 * n_rec), al(4 * tiles * (size_t)b.cfg.n_mlp), al(16 * (size_t)b.total_slots),
+                          al(8 * n_rec), al(4 * n_rec), al(4 * n_rec)};
+    size_t need = al(temp);
+    for (size_t x : sz) need += x;
+    if (need > ctx->det_cap || !ctx->det_mem) {
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(ctx, ctx->det_mem);
+        ctx->det_mem = dalloc(ctx, need);
+        ctx->det_cap = ctx->det_mem ? need : 0;
+        if (!ctx->det_mem) return fail(ROMAP_E_OOM, "deterministic-mode buffers (%zu bytes)", need);
+    }
+    char* p = static_cast<char*>(ctx->det_mem);
+    ctx->det.key = reinterpret_cast<unsigned long long*>(p); p += sz[0];
+    ctx->det.val = reinterpret_cast<float2*>(p); p += sz[1];
+    ctx->det.dw = reinterpret_cast<float*>(p); p += sz[2];
+    ctx->det.ray_loss = reinterpret_cast<float*>(p); p += sz[3];
+    ctx->det_key_sorted = reinterpret_cast<unsigned long long*>(p); p += sz[4];
+    ctx->det_iota = reinterpret_cast<unsigned*>(p); p += sz[5];
+    ctx->det_perm = reinterpret_cast<unsigned*>(p); p += sz[6];
+    ctx->det_temp = p;
+    ctx->det_temp_bytes = temp;
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    launch_det_iota(lc, ctx->det_iota, n_rec);
+    CK(cudaGetLastError());
+    return ROMAP_OK;
+}
+
 static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool adam, romap_train_stats* out) {
     const int n = (int)b.dev.size();
     LaunchCtx lc{ctx->st, ctx->num_sms};
@@ -901,6 +968,16 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
         K = std::min(Kmax, n_iters);
     }
     ctx->last_ray_base = (size_t)((n_iters - 1) % K) * b.total_slots;
+    DetBufs det{};                   // all null: atomics (the default)
+    if (ctx->det_on) {
+        romap_status ds = ensure_det(ctx, b);
+        if (ds) return ds;
+        det = ctx->det;
+    }
+    auto det_reduce = [&]() {
+        STAGE(ST_DET, launch_det_reduce(lc, b.cfg, ctx->objdev_d, n, b.total_slots, det, ctx->det_key_sorted,
+                                        ctx->det_iota, ctx->det_perm, ctx->det_temp, ctx->det_temp_bytes, ctx->loss_d));
+    };
     float* sigma = ctx->samp;
     float* rgb = sigma + S;
     float* dist = rgb + 3 * S;
@@ -937,17 +1014,25 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
                                                        srec, sdelta, ctx->hits_d));
                 ctx->prof.launches[ST_RAYGEN]++;      // two kernels: k_raygen + k_samples
             }
-            STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays + (size_t)k * b.total_slots,
-                                               srec + (size_t)k * S, sdelta + (size_t)k * S, b.total_slots,
-                                               ctx->loss_d, ctx->nonfinite_d, adam ? nullptr : ctx->samp));
+            if (ctx->det_on) {
+                STAGE(ST_FUSED, launch_fused_mixed_det(lc, b.cfg, ctx->objdev_d, ctx->rays + (size_t)k * b.total_slots,
+                                                       srec + (size_t)k * S, sdelta + (size_t)k * S, b.total_slots,
+                                                       ctx->loss_d, ctx->nonfinite_d, adam ? nullptr : ctx->samp, det));
+                det_reduce();
+            } else {
+                STAGE(ST_FUSED, launch_fused_mixed(lc, b.cfg, ctx->objdev_d, ctx->rays + (size_t)k * b.total_slots,
+                                                   srec + (size_t)k * S, sdelta + (size_t)k * S, b.total_slots,
+                                                   ctx->loss_d, ctx->nonfinite_d, adam ? nullptr : ctx->samp));
+            }
         } else {
             STAGE(ST_RAYGEN, launch_raygen(lc, b.cfg, ctx->objdev_d, n, b.total_slots, ctx->rays, ctx->hits_d));
             STAGE(ST_FWD, launch_fwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, true, false, sigma, rgb,
                                           dist, delta, ctx->act, (long long)S));
             STAGE(ST_RENDER_LOSS, launch_render_loss(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb,
-                                                     dist, delta, dsigma, drgb, ctx->loss_d, ctx->nonfinite_d));
+                                                     dist, delta, dsigma, drgb, ctx->loss_d, ctx->nonfinite_d, det));
             STAGE(ST_BWD, launch_bwd_fp32(lc, b.cfg, ctx->objdev_d, ctx->rays, b.total_slots, sigma, rgb, dsigma, drgb,
-                                          ctx->act, (long long)S));
+                                          ctx->act, (long long)S, det));
+            if (ctx->det_on) det_reduce();
         }
         auto h2 = hnow();
         hp[1] += hms(h1, h2);
@@ -962,8 +1047,8 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     if (n_chunks > 0) {
         auto& g = ctx->tg;
         const void* ptrs[8] = {ctx->objdev_d, ctx->rays, ctx->srec, ctx->loss_d, ctx->hits_d, ctx->nonfinite_d,
-                               ctx->flush_buf, nullptr};
-        const bool same = g.exec && g.n == n && g.total_slots == b.total_slots && g.K == K &&
+                               ctx->flush_buf, ctx->det_on ? ctx->det_mem : nullptr};
+        const bool same = g.exec && g.n == n && g.total_slots == b.total_slots && g.K == K && g.det == ctx->det_on &&
                           g.flush_bytes == ctx->flush_bytes && !memcmp(g.ptrs, ptrs, sizeof ptrs) &&
                           !memcmp(&g.cfg, &b.cfg, sizeof(CfgDev));
         if (!same) {
@@ -972,32 +1057,45 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             cudaGraph_t graph = nullptr;
             long long saved[ST_COUNT];                  // capturing is not launching
             memcpy(saved, ctx->prof.launches, sizeof saved);
-            if (cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            cudaError_t ec = cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal);
+            const char* what = "cudaStreamBeginCapture";
+            if (ec == cudaSuccess) {
                 // the loss partials of a call are those of its last iteration: the
                 // chunk resets them before its last iteration
                 for (int k = 0; k < K; ++k) enqueue_iter(k, k, K, k == K - 1);
-                const cudaError_t ec = cudaStreamEndCapture(ctx->st, &graph);
-                if (ec == cudaSuccess && graph && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) g.exec = nullptr;
+                ec = cudaStreamEndCapture(ctx->st, &graph);
+                what = "cudaStreamEndCapture";
+                if (ec == cudaSuccess && graph) {
+                    ec = cudaGraphInstantiate(&g.exec, graph, 0);
+                    what = "cudaGraphInstantiate";
+                    if (ec != cudaSuccess) g.exec = nullptr;
+                }
                 if (graph) cudaGraphDestroy(graph);
             }
-            cudaGetLastError();                       // a failed capture falls back to plain launches
             memcpy(ctx->prof.launches, saved, sizeof saved);
-            if (g.exec) {
-                g.cfg = b.cfg;
-                g.n = n;
-                g.total_slots = b.total_slots;
-                g.K = K;
-                g.flush_bytes = ctx->flush_bytes;
-                memcpy(g.ptrs, ptrs, sizeof ptrs);
+            if (ec != cudaSuccess || !g.exec) {
+                // nothing was launched: report instead of silently running without the graph
+                cudaGetLastError();
+                return fail(ROMAP_E_CUDA, "a9 graph capture failed at %s: %s (ROMAP_NO_GRAPH=1 runs plain launches)",
+                            what, cudaGetErrorString(ec));
             }
+            g.cfg = b.cfg;
+            g.n = n;
+            g.total_slots = b.total_slots;
+            g.K = K;
+            g.det = ctx->det_on;
+            g.flush_bytes = ctx->flush_bytes;
+            memcpy(g.ptrs, ptrs, sizeof ptrs);
         }
         if (g.exec) {
             for (int c = 0; c < n_chunks; ++c) CK(cudaGraphLaunch(g.exec, ctx->st));
+            ctx->prof.launches[ST_GRAPH] += n_chunks;
             it0 = n_chunks * K;
             ctx->prof.launches[ST_RAYGEN] += 2LL * n_chunks;   // (capture counted one chunk already)
             ctx->prof.launches[ST_FUSED] += (long long)K * n_chunks;
             ctx->prof.launches[ST_ADAM] += (long long)K * n_chunks;
             if (ctx->flush_bytes) ctx->prof.launches[ST_FLUSH] += (long long)K * n_chunks;
+            if (ctx->det_on) ctx->prof.launches[ST_DET] += (long long)K * n_chunks;
         }
     }
     for (int it = it0; it < n_iters; ++it) {
@@ -1202,6 +1300,13 @@ static void async_worker(romap_ctx* ctx) {
                                          as->alpha_deg, as->iters_per_update, &acc, nullptr);
             std::lock_guard<std::mutex> lk(as->mu);
             as->accepted += acc;
+            // a bad frame (unknown object, instance not in the mask, bad intrinsics)
+            // is rejected, nothing changed (validation precedes device work): the
+            // worker keeps going.  Only CUDA / non-finite / state errors stop it.
+            if (st == ROMAP_E_INVALID || st == ROMAP_E_NOT_FOUND) {
+                as->rejected++;
+                st = ROMAP_OK;
+            }
         } else if (train) {
             std::vector<int32_t> ids(ctx->objs.size() + 1), its(ctx->objs.size() + 1);
             int32_t n = 0;
@@ -1237,6 +1342,14 @@ romap_status romap_async_start(romap_ctx* ctx, int32_t chunk, float alpha_deg, i
 romap_status romap_async_offer(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
                                const float T_wc[12], const romap_intrinsics* K, int32_t* queued) {
     if (!ctx || !ctx->async) return fail(ROMAP_E_STATE, "async worker not running");
+    {
+        // a worker that stopped on an error takes no more frames (the producer must
+        // not mistake a dead trainer for backpressure)
+        std::lock_guard<std::mutex> lk(ctx->async->mu);
+        if (ctx->async->error)
+            return fail(ROMAP_E_STATE, "async worker stopped: %s (romap_async_stop returns the error)",
+                        ctx->async->error_msg.c_str());
+    }
     if (!rgb || !mask || !T_wc || !K || !queued || K->width < 1 || K->height < 1)
         return fail(ROMAP_E_INVALID, "bad frame");
     AsyncState* as = ctx->async;
@@ -1278,6 +1391,7 @@ romap_status romap_async_stop(romap_ctx* ctx, int32_t finish_pending, romap_asyn
         out->accepted = as->accepted;
         out->iterations = as->iterations;
         out->max_queue_depth = as->max_depth;
+        out->rejected = as->rejected;
     }
     romap_status err = as->error;
     std::string msg = as->error_msg;
@@ -1731,6 +1845,13 @@ romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes) {
         if (!ctx->flush_buf) return fail(ROMAP_E_OOM, "flush buffer");
         ctx->flush_bytes = (size_t)bytes;
     }
+    return ROMAP_OK;
+}
+
+romap_status romap_set_deterministic(romap_ctx* ctx, int32_t on) {
+    CHECK_CTX();
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->det_on = on != 0;                       // the cached graph is keyed by the mode
     return ROMAP_OK;
 }
 

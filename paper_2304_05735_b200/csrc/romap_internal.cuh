@@ -318,6 +318,25 @@ __device__ __forceinline__ void sample_geometry(const RayRec& rr, int i, int N, 
 }
 
 // ---------------------------------------------------------------------------
+// deterministic-reduction mode (romap_set_deterministic; tests only): instead of
+// fp32 atomics, the training kernels write every gradient / loss contribution
+// to a record, and k_det.cu reduces the records in a fixed order (sample order
+// within an object), so the result does not depend on scheduling, on the other
+// objects of the batch or on graph vs plain launches.
+//   key/val: one record per (sample s, level l, corner b) of the launch, index
+//            (s * L + l) * 8 + b; key = (object slot << 32) | table entry, or
+//            DET_NO_KEY for a sample of an inactive ray
+//   dw:      per 128-sample tile the tile's MLP weight gradient [n_mlp]
+//   ray_loss:per ray slot of the launch the four loss sums (rgb, rr, depth, density)
+#define DET_NO_KEY 0xffffffffffffffffULL
+struct DetBufs {
+    unsigned long long* key;
+    float2* val;
+    float* dw;
+    float* ray_loss;
+};
+
+// ---------------------------------------------------------------------------
 // launchers (defined in the kernel .cu files; all enqueue on `st`)
 struct LaunchCtx {
     cudaStream_t st;
@@ -333,10 +352,16 @@ void launch_fwd_fp32(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs,
                      long long act_stride);
 void launch_render_loss(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
                         const float* sigma, const float* rgb, const float* dist, const float* delta, float* dsigma,
-                        float* drgb, double* loss_acc, int* nonfinite);
+                        float* drgb, double* loss_acc, int* nonfinite, const DetBufs& det);
 void launch_bwd_fp32(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays, int n_rays,
                      const float* sigma, const float* rgb, const float* dsigma, const float* drgb, const float* act,
-                     long long act_stride);
+                     long long act_stride, const DetBufs& det);
+// k_det.cu: the fixed-order reductions of the deterministic mode
+size_t det_sort_temp_bytes(long long n_records, int n_objs);
+void launch_det_reduce(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int total_slots,
+                       const DetBufs& det, unsigned long long* key_sorted, const unsigned* iota, unsigned* perm,
+                       void* temp, size_t temp_bytes, double* loss_acc);
+void launch_det_iota(const LaunchCtx& lc, unsigned* v, long long n);
 void launch_adam(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs, int* nonfinite,
                  bool write_half);
 void launch_zero_grads(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, int n_objs);

@@ -114,7 +114,12 @@ _SIGS = {
     "romap_pending_iters": [_P, _I, C.POINTER(C.c_int64)],
     "romap_train_pending": [_P, _I, _I, _P, _P, _I, C.POINTER(_I)],
     "romap_set_l2_flush": [_P, C.c_int64],
+    "romap_set_deterministic": [_P, _I],
 }
+
+# device allocator callbacks of romap_ctx_create (romap.h): void* alloc(size_t, void*), void free(void*, void*)
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
 
 def load_library(path: str = LIB_PATH):
@@ -184,20 +189,48 @@ def _ids(objs):
     return arr, len(arr)
 
 
-class Context:
-    """One context per device (romap_ctx); enqueues on torch's current stream."""
+def _torch_allocator(device):
+    """romap_ctx_create callbacks backed by torch's caching allocator (north_star:
+    "PyTorch only for device memory").  The library frees a buffer only after
+    synchronizing its stream, so a block handed back may be reused on any stream."""
+    import torch
 
-    def __init__(self, device: int = 0, stream=None):
+    def _alloc(nbytes, _user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device)
+        except Exception:
+            return None
+
+    def _free(ptr, _user):
+        try:
+            torch.cuda.caching_allocator_delete(ptr)
+        except Exception:
+            pass
+    return ALLOC_FN(_alloc), FREE_FN(_free)
+
+
+class Context:
+    """One context per device (romap_ctx).  Enqueues on torch's current stream when
+    that is a side stream; on the default stream the library uses a (blocking)
+    stream of its own, so the a9 CUDA graph can be captured.  Device memory comes
+    from torch's caching allocator (torch_alloc=True) or cudaMalloc."""
+
+    def __init__(self, device: int = 0, stream=None, torch_alloc: bool = True):
+        self._cb = (None, None)
         if stream is None:
             try:
                 import torch
                 if torch.cuda.is_available():
                     torch.cuda.set_device(device)
                     stream = torch.cuda.current_stream(device).cuda_stream
+                    if torch_alloc:
+                        self._cb = _torch_allocator(device)
             except Exception:
                 stream = None
         self._h = C.c_void_p()
-        _check(_lib.romap_ctx_create(device, C.c_void_p(stream or 0), None, None, None, C.byref(self._h)))
+        a, f = self._cb
+        _check(_lib.romap_ctx_create(device, C.c_void_p(stream or 0), C.cast(a, C.c_void_p) if a else None,
+                                     C.cast(f, C.c_void_p) if f else None, None, C.byref(self._h)))
         self.device = device
 
     def close(self):
@@ -281,9 +314,9 @@ class Context:
         return bool(q.value)
 
     def async_stop(self, finish_pending: bool = True) -> dict:
-        st = (C.c_int64 * 5)()
+        st = (C.c_int64 * 6)()
         _check(_lib.romap_async_stop(self._h, 1 if finish_pending else 0, C.cast(st, C.c_void_p)))
-        return dict(zip(["offered", "dropped", "accepted", "iterations", "max_queue_depth"], list(st)))
+        return dict(zip(["offered", "dropped", "accepted", "iterations", "max_queue_depth", "rejected"], list(st)))
 
     def pending_iters(self, obj: int) -> int:
         p = C.c_int64()
@@ -399,6 +432,10 @@ class Context:
 
     def set_l2_flush(self, nbytes: int):
         _check(_lib.romap_set_l2_flush(self._h, int(nbytes)))
+
+    def set_deterministic(self, on: bool = True):
+        """Deterministic-reduction mode (romap.h): fixed-order gradient / loss sums."""
+        _check(_lib.romap_set_deterministic(self._h, 1 if on else 0))
 
     def profile_enable(self, on: bool = True, stages=None):
         """Per-stage event timing; `stages` (names) restricts the events to those stages."""

@@ -64,3 +64,24 @@ def test_async_queue_full_drops_without_blocking():
     st = c.async_stop(finish_pending=False)
     assert st["offered"] == len(res) and st["dropped"] == res.count(False)
     c.close()
+
+
+def test_async_bad_frames_are_rejected_and_the_worker_goes_on():
+    """a frame for an unknown object, or one whose mask does not contain the
+    instance, is rejected (counted) and changes nothing; the worker keeps taking
+    and training the good frames"""
+    c = R.Context(0)
+    sc = scenes.sphere_scene(0, n_views=8)
+    ob = sc.objects[0]
+    h = c.create_object(ob.t, ob.yaw, ob.a, R.model_config(**CFG), ob.instance_id)
+    c.async_start(chunk=50, queue_cap=64)
+    fr0 = sc.frames[0]
+    assert c.async_offer(h + 77, fr0.rgb, fr0.mask, fr0.T_wc, fr0.K)             # unknown object
+    assert c.async_offer(h, fr0.rgb, np.zeros_like(fr0.mask), fr0.T_wc, fr0.K)   # instance not visible
+    for fr in sc.frames:
+        assert c.async_offer(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
+    st = c.async_stop(finish_pending=True)
+    assert st["rejected"] == 2 and st["accepted"] >= 1
+    assert c.object_info(h)["n_keyframes"] == st["accepted"]
+    assert int(c.get_params(h, R.BLOCK_STEP)[0]) == 300 * st["accepted"]
+    c.close()
