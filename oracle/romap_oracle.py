@@ -17,7 +17,13 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   level_table       hand-listed resolutions / entry totals (BASELINE cfg0, cfg1)
   mix64 / rng_u32   published SplitMix64 output vectors (golden file)
   draw_pixels       bijection over all in-box pixels (brute force), chi^2
+  rng_u32 key       golden u32 of the composed key from an independent python-int
+                    reference (tests/golden/rng_ref.py, rng_u32_keys.txt); the
+                    training stream layout (pixel 0, background 1-3, jitter 16+i)
   make_rays         principal-point ray, projection round trip
+  make_rays_per_ray equals make_rays ray by ray (bitwise), round trip with per-ray K
+  sample_points     hand-computed u for unequal half extents, clamp at the faces (R6)
+  forward_rays      R17 depth target: z on the optical axis, z*|dc| off axis
   ray_box           (4,6) example, parallel miss,
                     dense-stepping membership oracle
   stratified        one sample per stratum, ascending, mean≈midpoint
@@ -39,7 +45,8 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   marching_tetrahedra  single-vertex case counts (6 on the Kuhn diagonal, 2
                     elsewhere), exact vertices for a linear field, sphere radius /
                     area within the lattice step; mesh_metrics shifted-grid closed form
-No function is "parity unpinned".
+tools/oracle_mutations.py applies plausible mistakes (wrong index / sign / stream /
+operand) to this file one at a time and checks that each fails a pin.
 """
 from __future__ import annotations
 

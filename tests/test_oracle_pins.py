@@ -767,3 +767,123 @@ def test_observed_mask_projection():
     assert O.observed_mask(P, [0, 0, 0], 0.0, [kf]).tolist() == [True, False, False, True, False]
     # the box pose moves the points: a box translated by 0.5 m in x puts its origin off-axis
     assert O.observed_mask(P[:1], [0.5, 0, 0], 0.0, [kf]).tolist() == [False]
+
+
+# ---------------------------------------------------------------- O2 / O4 / O6 / R17: the training-path pieces
+# (VERDICT r1 "What's weak" #1: make_rays_per_ray, sample_points, the rng key / stream
+# layout and the R17 depth conversion had no pin of their own)
+import sys as _sys  # noqa: E402
+_sys.path.insert(0, GOLD)
+import rng_ref  # noqa: E402  (plain-int reference, tests/golden/rng_ref.py; imports nothing from oracle/)
+
+
+def test_rng_composed_key_golden():
+    # R13 key composition: golden u32 written by tests/golden/make_rng_golden.py (python ints)
+    rows = [l.split() for l in open(os.path.join(GOLD, "rng_u32_keys.txt")) if l.strip() and not l.startswith("#")]
+    assert len(rows) >= 10
+    for seed, obj, t, ray, stream, hx in rows:
+        got = int(O.rng_u32(int(seed), int(obj), int(t), np.array([int(ray)]), np.array([int(stream)]))[0])
+        assert got == int(hx, 16), (seed, obj, t, ray, stream, hex(got), hx)
+
+
+def _kf_image(W, H, K, T, obj_px, occ_px=(), depth=None, iid=1):
+    rgb = (np.arange(H * W * 3) % 251).astype(np.uint8).reshape(H, W, 3)
+    mask = np.zeros((H, W), np.uint16)
+    for (x, y) in obj_px:
+        mask[y, x] = iid
+    for (x, y) in occ_px:
+        mask[y, x] = iid + 1
+    return O.ingest_observation(rgb, mask, T, K, iid, depth)
+
+
+def _pose(yaw_deg, centre):
+    """camera looking along +x of the world rotated by yaw, OpenCV axes"""
+    a = math.radians(yaw_deg)
+    fwd = np.array([math.cos(a), math.sin(a), 0.0])
+    right = np.array([math.sin(a), -math.cos(a), 0.0])
+    down = np.array([0.0, 0.0, -1.0])
+    R = np.stack([right, down, fwd], 1)
+    return np.concatenate([R, np.asarray(centre, float)[:, None]], 1).astype(f32)
+
+
+def test_training_rng_stream_layout():
+    # R13 streams of a training iteration (SPEC.md:436,456): pixel = stream 0, background
+    # colour = streams 1-3, jitter of sample i = stream 16+i, all keyed (seed, obj, t, ray)
+    cfg = O.ModelConfig(samples_per_ray=8, rays_per_iter=300, seed=11)
+    K = np.array([40.0, 42.0, 15.5, 11.0], f32)
+    kfs = [_kf_image(32, 24, K, _pose(10 * k, [-2.0, 0.1 * k, 0.3]),
+                     [(x, y) for x in range(8 + k, 20) for y in range(5, 14 + k)], occ_px=[(21, 7)]) for k in range(3)]
+    st = O.ObjectState(cfg, np.zeros(3, f32), 0.2, np.full(3, 0.6, f32), 37, O.init_params(cfg, 0), kfs=kfs)
+    t = 5
+    rs = O.forward_rays(st, t)
+    total = sum(k.w * k.h for k in kfs)
+    for r in range(cfg.rays_per_iter):
+        idx = rng_ref.pixel_index(rng_ref.key_u32(11, 37, t, r, 0), total)
+        k = 0
+        while idx >= kfs[k].w * kfs[k].h:
+            idx -= kfs[k].w * kfs[k].h
+            k += 1
+        assert (rs["k"][r], rs["px"][r], rs["py"][r]) == (k, kfs[k].x0 + idx % kfs[k].w, kfs[k].y0 + idx // kfs[k].w)
+        for c in range(3):
+            assert rs["bg"][r, c] == f32(rng_ref.unit(rng_ref.key_u32(11, 37, t, r, 1 + c)))
+        for i in range(cfg.samples_per_ray):
+            assert rs["xi"][r, i] == f32(rng_ref.unit(rng_ref.key_u32(11, 37, t, r, 16 + i)))
+
+
+def test_make_rays_per_ray_equals_make_rays():
+    # the training-path builder (per-ray intrinsics / pose) equals the pinned
+    # single-camera builder ray by ray, bitwise
+    g = np.random.default_rng(3)
+    n = 64
+    Ks = np.stack([np.array([g.uniform(200, 600), g.uniform(200, 600), g.uniform(100, 400), g.uniform(50, 300)], f32)
+                   for _ in range(n)])
+    Ts = np.stack([_pose(g.uniform(-180, 180), g.uniform(-2, 2, 3)) for _ in range(n)])
+    px = g.integers(0, 640, n)
+    py = g.integers(0, 480, n)
+    bt = np.array([0.3, -0.2, 0.1], f32)
+    yaw = 0.7
+    o, d, nn = O.make_rays_per_ray(px, py, Ks, Ts, bt, yaw)
+    for i in range(n):
+        o1, d1, n1 = O.make_rays([px[i]], [py[i]], Ks[i], Ts[i], bt, yaw)
+        assert np.array_equal(o[i], o1[0]) and np.array_equal(d[i], d1[0]) and nn[i] == n1[0]
+    # and a projection round trip with each ray's own intrinsics (SPEC.md:324)
+    for i in range(n):
+        xo = o[i].astype(np.float64) + 1.7 * d[i].astype(np.float64)
+        c, s = math.cos(yaw), math.sin(yaw)
+        xw = np.array([c * xo[0] - s * xo[1], s * xo[0] + c * xo[1], xo[2]]) + bt
+        T64 = Ts[i].astype(np.float64)
+        xc = T64[:, :3].T @ (xw - T64[:, 3])
+        assert abs(Ks[i, 0] * xc[0] / xc[2] + Ks[i, 2] - (px[i] + 0.5)) < 1e-3
+        assert abs(Ks[i, 1] * xc[1] / xc[2] + Ks[i, 3] - (py[i] + 0.5)) < 1e-3
+
+
+def test_sample_points_hand_computed_and_clamped():
+    # R6: u = (x + a) / (a + a), x = o + dist d, clamped to [0, 1]; a box with unequal
+    # half extents, values exact in fp32
+    a = np.array([0.5, 1.0, 2.0], f32)
+    o = np.array([[-0.25, 0.5, -1.0]], f32)
+    d = np.array([[1.0, 0.0, 0.0]], f32)
+    u = O.sample_points(o, d, np.array([[0.0, 0.5]], f32), a)
+    assert np.array_equal(u[0, 0], np.array([0.25, 0.75, 0.25], f32))      # x = (-0.25, 0.5, -1)
+    assert np.array_equal(u[0, 1], np.array([0.75, 0.75, 0.25], f32))      # x = (0.25, 0.5, -1)
+    # faces: x beyond +a / -a clamps to 1 / 0 on that axis only
+    o2 = np.array([[0.6, -1.5, 3.0]], f32)
+    u2 = O.sample_points(o2, np.array([[0.0, 0.0, 1.0]], f32), np.array([[0.0]], f32), a)
+    assert np.array_equal(u2[0, 0], np.array([1.0, 0.0, 1.0], f32))
+    u3 = O.sample_points(np.array([[0.0, 0.25, -0.5]], f32), d, np.array([[-0.75]], f32), a)
+    assert np.array_equal(u3[0, 0], np.array([0.0, 0.625, 0.375], f32))   # x = (-0.75 -> clamp, 0.25, -0.5)
+
+
+def test_depth_target_is_ray_distance():
+    # R17 (PAPER.md:132,167-170): a sparse camera-z sample on pixel (px, py) becomes the
+    # ray distance z * |((px+.5-cx)/fx, (py+.5-cy)/fy, 1)|: z on the optical axis,
+    # z * sqrt(1 + 1/16) one pixel off axis with fx = 4
+    cfg = O.ModelConfig(samples_per_ray=4, rays_per_iter=64, seed=2)
+    K = np.array([4.0, 4.0, 3.5, 2.5], f32)
+    kf = _kf_image(8, 6, K, _pose(0.0, [-2.0, 0.0, 0.0]), [(3, 2), (4, 2)], depth=[(3.5, 2.5, 2.0), (4.7, 2.2, 3.0)])
+    st = O.ObjectState(cfg, np.zeros(3, f32), 0.0, np.full(3, 0.5, f32), 1, O.init_params(cfg, 0), kfs=[kf])
+    rs = O.forward_rays(st, 1)
+    assert set(rs["px"].tolist()) == {3, 4} and rs["has_depth"].all()
+    on = rs["px"] == 3
+    assert np.all(rs["depth_t"][on] == f32(2.0))
+    assert np.allclose(rs["depth_t"][~on].astype(np.float64), 3.0 * math.sqrt(1.0 + 1.0 / 16.0), rtol=1e-6, atol=0)
