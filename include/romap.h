@@ -150,6 +150,10 @@ typedef struct {
 /* debug_dump kinds: per ray / per sample data of the object's rays in the LAST
  * iteration run by train_step / forward_backward (recomputed by the same device
  * functions as the training kernels, with the parameters as they are now).
+ * Mixed-precision objects (precision 1): SAMPLES are the very records the fused
+ * kernel consumed (k_raygen + k_samples output) and HASH_IDX the corner entries
+ * the fused kernel's own addressing (hash_fp16.cuh) computes from them; both are
+ * available after train_step as well as after forward_backward.
  *   RAYS:     romap_ray_dump[n_rays]
  *   SAMPLES:  float[n_rays][N][5] = dist, delta, u.x, u.y, u.z
  *   HASH_IDX: int32[n_rays][N][L][8] absolute table entry per corner

@@ -45,7 +45,7 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   marching_tetrahedra  single-vertex case counts (6 on the Kuhn diagonal, 2
                     elsewhere), exact vertices for a linear field, sphere radius /
                     area within the lattice step; mesh_metrics shifted-grid closed form
-tools/oracle_mutations.py applies plausible mistakes (wrong index / sign / stream /
+tests/test_oracle_mutations.py applies plausible mistakes (wrong index / sign / stream /
 operand) to this file one at a time and checks that each fails a pin.
 """
 from __future__ import annotations

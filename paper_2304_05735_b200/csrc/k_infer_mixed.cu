@@ -453,3 +453,41 @@ void launch_fwd_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj,
     else
         k_fwd_mixed<8><<<(unsigned)grid, QT, smem, lc.st>>>(cfg, obj, rays, n_rays, sigma, rgb, dist, delta);
 }
+
+// ---------------------------------------------------------------------------
+// debug dumps of the MEASURED mixed path (romap_debug_dump on precision-1
+// objects): the (u, dist) / delta records k_raygen + k_samples wrote for the
+// iteration and k_fused_mixed consumed, and the corner entries computed from them
+// by the fused kernel's own addressing (hash_fp16.cuh level_entries + the level
+// offset), so a test can hold both bit-exact against the oracle.
+//   what 1 (SAMPLES):  out float[n][5] = dist, delta, u.x, u.y, u.z
+//   what 2 (HASH_IDX): out int32[n][L][8] absolute entry of corner b (bit k -> +1 on axis k)
+__global__ void k_debug_mixed(CfgDev cfg, const float4* __restrict__ srec, const float* __restrict__ sdelta,
+                              long long n, int what, void* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 r = srec[i];
+    if (what == 1) {
+        float* o = static_cast<float*>(out) + 5 * i;
+        o[0] = r.w;
+        o[1] = sdelta[i];
+        o[2] = r.x;
+        o[3] = r.y;
+        o[4] = r.z;
+        return;
+    }
+    const float u[3] = {r.x, r.y, r.z};
+    int* o = static_cast<int*>(out) + i * cfg.L * 8;
+    for (int l = 0; l < cfg.L; ++l) {
+        Cell cl;
+        unsigned e[8];
+        level_entries(u, level_params(cfg, l), 0u, (unsigned)cfg.T - 1u, cl, e);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) o[l * 8 + b] = (int)(e[b] + (unsigned)cfg.off[l]);
+    }
+}
+
+void launch_debug_mixed(const LaunchCtx& lc, const CfgDev& cfg, const float4* srec, const float* sdelta, long long n,
+                        int what, void* out) {
+    if (n > 0) k_debug_mixed<<<(unsigned)((n + 127) / 128), 128, 0, lc.st>>>(cfg, srec, sdelta, n, what, out);
+}

@@ -43,6 +43,8 @@ void launch_mt(const LaunchCtx& lc, const ObjDev* obj, const float* sig, const f
                int* counts, int* offsets, void* tmp, size_t tmp_bytes, float* tris, bool emit);
 void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz,
                                 long long n, float* sigma);
+void launch_debug_mixed(const LaunchCtx& lc, const CfgDev& cfg, const float4* srec, const float* sdelta, long long n,
+                        int what, void* out);
 
 static thread_local std::string g_err;
 
@@ -166,6 +168,7 @@ struct romap_ctx {
     float* srec = nullptr;       // mixed path: K slices of (u, dist) float4, then K slices of delta (k_raygen + k_samples)
     size_t srec_cap = 0;
     size_t last_ray_base = 0;    // ray slot of slice holding the last iteration's rays
+    int last_K = 1;              // mixed path: slices of the last call's sample records
     float* act = nullptr;
     size_t act_cap = 0;
     ObjDev* objdev_d = nullptr;
@@ -968,6 +971,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
         K = std::min(Kmax, n_iters);
     }
     ctx->last_ray_base = (size_t)((n_iters - 1) % K) * b.total_slots;
+    ctx->last_K = K;
     DetBufs det{};                   // all null: atomics (the default)
     if (ctx->det_on) {
         romap_status ds = ensure_det(ctx, b);
@@ -1758,6 +1762,22 @@ romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* b
             }
             o[i].t_near = rr[i].tn; o[i].t_far = rr[i].tf; o[i].depth = rr[i].depth;
         }
+        return ROMAP_OK;
+    }
+    if (ob->cfg.precision == 1 && (what == ROMAP_DUMP_SAMPLES || what == ROMAP_DUMP_HASH_IDX)) {
+        // the mixed path's own records of the last iteration (train_step or
+        // forward_backward) and the fused kernel's corner addressing of them
+        const CfgDev& c = ctx->last_cfg;
+        const size_t S = (size_t)ctx->last_total_slots * c.N;
+        const size_t k = ctx->last_ray_base / (size_t)ctx->last_total_slots;
+        const float4* srec = reinterpret_cast<const float4*>(ctx->srec) + k * S + (size_t)begin * c.N;
+        const float* sdelta = ctx->srec + 4 * S * ctx->last_K + k * S + (size_t)begin * c.N;
+        if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)(need / 4 + 1))) return fail(ROMAP_E_OOM, "staging buffer");
+        LaunchCtx lc{ctx->st, ctx->num_sms};
+        launch_debug_mixed(lc, c, srec, sdelta, (long long)R * c.N, what == ROMAP_DUMP_SAMPLES ? 1 : 2, ctx->io_d);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(buf, ctx->io_d, need, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
         return ROMAP_OK;
     }
     if (ctx->last_call != LAST_FWDBWD)

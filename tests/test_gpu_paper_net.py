@@ -1,6 +1,8 @@
 """The paper's network (R24: hash encoding + 1..3
 hidden layers of 64 -> sigma, rgb; positions only) on the mixed GPU path vs the
-oracle: per-block gradients within 2e-2 norm-relative (BASELINE, fp16 path),
+oracle: per-block gradients within 2e-2 norm-relative of fp64 (BASELINE, fp16
+path; the 2- and 3-layer Table 4 variants: see GRAD_TOL), every block and every
+hash level within 1e-2 of the fp16 precision model (tests/mixed_model.py),
 losses within 1e-2, a few training steps, density query and render."""
 import numpy as np
 import pytest
@@ -27,26 +29,44 @@ def ctx():
     c.close()
 
 
+# GPU vs the fp16 model: both round at the same points, but fp32 (GPU) and fp64
+# (model) accumulation still move a few pre-activations across a ReLU kink or an
+# fp16 rounding boundary, and one flipped unit of one sample shifts a coarse level's
+# cancelling sum by up to ~0.7 % (measured, N = 16); a wrong corner index or
+# scatter on a level moves that level by O(1)
+MODEL_TOL = 1e-2
+
+
 def _grads(ctx, h, st, tol=2e-2):
+    import mixed_model
     stats = ctx.forward_backward([h])[0]
     L, g, dbg = O.loss_and_grads(st, 1)
     assert stats["hit_rays"] == L["hit_rays"] and stats["samples"] == L["samples"]
     assert abs(stats["l_total"] - L["l_total"]) <= 1e-2 * L["l_total"]
-    e_tab = norm_rel(ctx.get_params(h, R.BLOCK_GRAD_TABLE), g["table"].reshape(-1))
+    gt = ctx.get_params(h, R.BLOCK_GRAD_TABLE).reshape(-1, 2)
+    e_tab = norm_rel(gt, g["table"])
     gm = ctx.get_params(h, R.BLOCK_GRAD_MLP)
-    errs, off = [], 0
-    for w in g["W"]:
+    _, gmod = mixed_model.mixed_loss_and_grads(st, 1)
+    errs, e_mod, off = [], [], 0
+    for w, wm in zip(g["W"], gmod["W"]):
         errs.append(norm_rel(gm[off:off + w.size], w))
+        e_mod.append(norm_rel(gm[off:off + w.size], wm))
         off += w.size
     assert off == gm.size
+    e_mod += [norm_rel(gt[l.offset:l.offset + l.size], gmod["table"][l.offset:l.offset + l.size])
+              for l in O.level_table(st.cfg)]
     assert e_tab < tol and max(errs) < tol, (e_tab, errs)
+    assert max(e_mod) < MODEL_TOL, e_mod
 
 
-# gradient tolerance per hidden-layer count: 2e-2 (BASELINE, fp16 path) for the
-# paper's single layer; every further fp16 backward layer rounds delta once more
-# and the table-gradient sums cancel, measured 1.4 / 2.9 / 3.8 % (tools/
-# diag_paper_net.py), so the Table 4 variants get 2e-2 + 1.5e-2 per extra layer
-#
+# gradient tolerance against fp64 per hidden-layer count: 2e-2 (BASELINE, fp16
+# path) for the paper's single layer.  The Table 4 variants with 2 / 3 hidden
+# layers are an explicit deviation from north_star's 2e-2:
+# the fp16 precision model (tests/mixed_model.py) puts the fp64 gap of the table
+# gradient at 1.0-1.1 % / 2.0-2.1 % / 2.5-2.7 % for 1 / 2 / 3 layers with the
+# backward deltas exact (rounding the deltas adds < 0.05 %): it comes from the fp16
+# FORWARD operands (features, weights, activations) through the deeper ReLU chain,
+# so fp32 deltas cannot close it.  The kernel itself is held to the model (1e-2).
 GRAD_TOL = {1: 2e-2, 2: 3.5e-2, 3: 5e-2}
 
 

@@ -1,7 +1,10 @@
 """GPU mixed path (fp16 tensor-core MLP, fp16 tables, fp32 master / atomics) vs
 the CPU oracle.  BASELINE north_star: parameter gradients within 2e-2 relative
-(norm-relative per block); geometry stays bit-exact (same raygen / sampling).
-Losses: 1e-2 relative (fp16 operands)."""
+(norm-relative per block: every hash level's table block and every weight matrix
+separately); geometry bit-exact: the sample records the fused kernel consumed
+(dist, delta, u) and the corner entries its own addressing computes from them
+(hash_fp16.cuh) equal the oracle's bit for bit.  Losses: 1e-2 relative (fp16
+operands)."""
 import numpy as np
 import pytest
 
@@ -27,23 +30,67 @@ def ctx():
     c.close()
 
 
-def _check_grads(ctx, h, L, g, dbg, stats, N, loss_tol=1e-2):
+def _check_geometry(ctx, h, rs, idx, N, L):
+    """bit-exact: the fused kernel's sample records and corner entries vs the oracle
+    (rs: oracle forward_rays, idx: oracle hash_encode corner entries of the hit samples)"""
+    hit = rs["hit"]
+    R_ = rs["R"]
+    sm = ctx.debug_dump(h, R.DUMP_SAMPLES).reshape(R_, N, 5)[hit]
+    u32 = lambda a: np.ascontiguousarray(a, np.float32).view(np.uint32)
+    assert np.array_equal(u32(sm[..., 0]), u32(rs["dist"][hit]))
+    assert np.array_equal(u32(sm[..., 1]), u32(rs["delta"][hit]))
+    assert np.array_equal(u32(sm[..., 2:5]), u32(rs["u"][hit]))
+    gi = ctx.debug_dump(h, R.DUMP_HASH_IDX).reshape(R_, N, L, 8)[hit].reshape(-1, L, 8)
+    assert np.array_equal(gi.astype(np.int64), idx)
+
+
+# GPU vs the fp16 model: both round at the same points, but fp32 (GPU) and fp64
+# (model) accumulation still move a few pre-activations across a ReLU kink or an
+# fp16 rounding boundary, and one flipped unit of one sample shifts a coarse level's
+# cancelling sum by up to ~0.7 % (measured, N = 16); a wrong corner index or
+# scatter on a level moves that level by O(1)
+MODEL_TOL = 1e-2
+
+
+def _check_grads(ctx, h, L, g, dbg, stats, N, st, loss_tol=1e-2, levels_vs_fp64=True):
+    """Every weight block and every hash level's table block against the fp64
+    oracle within 2e-2 (north_star), and against the fp16 precision model of the
+    mixed path (tests/mixed_model.py) within MODEL_TOL.  levels_vs_fp64=False: for
+    shapes where the fp16 forward perturbation alone moves coarse levels past 2e-2
+    of fp64 (N = 8 / 16 / 128 extremes), the whole table block
+    is held to 2e-2 and each level to the model."""
+    cfg = st.cfg
     for k in ("l_total", "l_rgb", "l_rr", "l_density"):
         assert abs(stats[k] - L[k]) <= loss_tol * max(abs(L[k]), 1e-4), (k, stats[k], L[k])
+    _check_geometry(ctx, h, dbg["rays"], dbg["idx"], N, cfg.levels)
     hit = dbg["rays"]["hit"]
     rg = ctx.debug_dump(h, R.DUMP_RAY_GRADS).reshape(dbg["rays"]["R"], N, 4)[hit]
     assert norm_rel(rg[..., 0], dbg["dsigma"]) < GRAD_TOL
     assert norm_rel(rg[..., 1:], dbg["drgb"]) < GRAD_TOL
     gt = ctx.get_params(h, R.BLOCK_GRAD_TABLE).reshape(-1, 2)
-    e_tab = norm_rel(gt, g["table"])
+    # per hash level (a wrong index on a fine level must not hide under the coarse
+    # levels' larger gradients)
+    lv = O.level_table(cfg)
+    e_lv = [norm_rel(gt[l.offset:l.offset + l.size], g["table"][l.offset:l.offset + l.size]) for l in lv]
     gm = ctx.get_params(h, R.BLOCK_GRAD_MLP)
     errs, off = [], 0
     for w in g["W"]:
         errs.append(norm_rel(gm[off:off + w.size], w))
         off += w.size
-    assert e_tab < GRAD_TOL, (e_tab, errs)
-    assert max(errs) < GRAD_TOL, (e_tab, errs)
-    return e_tab, errs
+    assert max(errs) < GRAD_TOL, (e_lv, errs)
+    if levels_vs_fp64:
+        assert max(e_lv) < GRAD_TOL, (e_lv, errs)
+    import mixed_model
+    _, gmod = mixed_model.mixed_loss_and_grads(st, 1)
+    e_mod = [norm_rel(gt[l.offset:l.offset + l.size], gmod["table"][l.offset:l.offset + l.size]) for l in lv]
+    e_modw = [norm_rel(gm[o:o + w.size], wm) for o, w, wm in
+              zip(np.cumsum([0] + [w.size for w in g["W"]])[:-1], g["W"], gmod["W"])]
+    print("per-level vs fp64 oracle", np.round(e_lv, 4), "vs fp16 model", np.round(e_mod, 4), "W vs model",
+          np.round(e_modw, 4))
+    assert norm_rel(gt, g["table"]) < GRAD_TOL, e_lv
+    assert max(e_mod) < MODEL_TOL, (e_mod, e_lv)
+    assert max(e_modw) < MODEL_TOL, (e_modw, errs)
+    return e_lv, errs
 
 
 def test_mixed_cfg0_grads(ctx):
@@ -53,7 +100,7 @@ def test_mixed_cfg0_grads(ctx):
     L, g, dbg = O.loss_and_grads(st, 1)
     rd = ctx.debug_dump(h, R.DUMP_RAYS)
     assert np.array_equal(rd["t_near"].view(np.uint32), dbg["rays"]["tn"].view(np.uint32))
-    _check_grads(ctx, h, L, g, dbg, stats, 32)
+    _check_grads(ctx, h, L, g, dbg, stats, 32, st)
     ctx.destroy_object(h)
 
 
@@ -63,7 +110,7 @@ def test_mixed_cfg1_shape_small(ctx):
     h, st = make_pair(R, ctx, sc, kw)
     stats = ctx.forward_backward([h])[0]
     L, g, dbg = O.loss_and_grads(st, 1)
-    _check_grads(ctx, h, L, g, dbg, stats, 64)
+    _check_grads(ctx, h, L, g, dbg, stats, 64, st)
     ctx.destroy_object(h)
 
 
@@ -75,7 +122,24 @@ def test_mixed_cfg1_full_size(ctx):
     stats = ctx.forward_backward([h])[0]
     L, g, dbg = O.loss_and_grads(st, 1)
     assert stats["hit_rays"] == L["hit_rays"] and stats["samples"] == L["samples"]
-    _check_grads(ctx, h, L, g, dbg, stats, 64)
+    _check_grads(ctx, h, L, g, dbg, stats, 64, st)
+    ctx.destroy_object(h)
+
+
+def test_mixed_cfg1_full_size_train_step_geometry(ctx):
+    # the timed configuration itself: train_step of 20 iterations at full cfg1 (one
+    # 16-iteration graph chunk + 4 plain iterations, K sample-record slices); the
+    # records of iteration 20 and their corner entries are the oracle's bit for bit
+    sc = scenes.object_scene(1, n_views=20)
+    h, st = make_pair(R, ctx, sc, CFG1M, avoid_kinks=False)
+    s = ctx.train_step([h], 20)[0]
+    assert s["step"] == 20
+    rs = O.forward_rays(st, 20)
+    _, idx, _ = O.hash_encode(rs["u"][rs["hit"]].reshape(-1, 3), st.params["table"], st.cfg)
+    _check_geometry(ctx, h, rs, idx, 64, 16)
+    rd = ctx.debug_dump(h, R.DUMP_RAYS)
+    for k_gpu, k_or in (("t_near", "tn"), ("t_far", "tf")):
+        assert np.array_equal(rd[k_gpu][rs["hit"]].view(np.uint32), rs[k_or][rs["hit"]].view(np.uint32))
     ctx.destroy_object(h)
 
 
@@ -90,7 +154,7 @@ def test_mixed_multi_object_and_training(ctx):
     stats = ctx.forward_backward(hs)
     for k in range(2):
         L, g, dbg = O.loss_and_grads(sts[k], 1)
-        _check_grads(ctx, hs[k], L, g, dbg, stats[k], 32)
+        _check_grads(ctx, hs[k], L, g, dbg, stats[k], 32, sts[k])
     # 10 mixed training steps track the oracle's losses
     for it in range(10):
         s = ctx.train_step(hs, 1)
@@ -169,5 +233,5 @@ def test_mixed_samples_per_ray_extremes(ctx, N, rays):
     stats = ctx.forward_backward([h])[0]
     L, g, dbg = O.loss_and_grads(st, 1)
     assert stats["samples"] == L["samples"]
-    _check_grads(ctx, h, L, g, dbg, stats, N)
+    _check_grads(ctx, h, L, g, dbg, stats, N, st, levels_vs_fp64=False)
     ctx.destroy_object(h)
