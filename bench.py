@@ -1,26 +1,40 @@
 #!/usr/bin/env python
 """bench.py -- RO-MAP multi-object NeRF training throughput on B200.
 
-Metric (BASELINE.json): NeRF train ray-samples/s (and seconds to the paper's
-~2 s per-object budget).  A step = one training iteration of every object on
-the rank: ray sampling -> hash encode -> MLP -> volume render + loss -> backward
--> Adam, run through the C ABI (libromap.so).
+Metric (BASELINE.json): NeRF train ray-samples/s and seconds-to-budget per object.
+A step = one training iteration of every object on the rank: ray sampling ->
+hash encode -> MLP -> volume render + loss -> backward -> Adam (SURVEY.md 8(a)
+a1..a8), run through the C ABI (libromap.so).
 
-Workload (default, N=1): BASELINE cfg1 -- one object, L=16, F=2, T=2^16,
-resolutions 16->512, density + SH colour MLP, 4096 rays x 64 stratified samples
-per iteration, 20 keyframes of 640x480 of a seeded box-union-torus SDF object.
-With --gpus N each rank trains its own cfg1-family object (weak scaling: objects
-are independent, no data-path collective; one NCCL all_reduce of the timings at
-the end).
+Workloads (--workload; BASELINE.json configs, synthetic stand-ins of the paper's
+640x480 sequences):
+  cfg1  one object per rank: L=16, F=2, T=2^16, resolutions 16->512, density +
+        SH colour MLP, 4096 rays x 64 stratified samples, 20 keyframes 640x480
+        (the N=1 default: BASELINE's metric is quoted on it)
+  cfg3  64 objects of the cfg1 family (seeded shapes, edges U(0.2, 1.5) m), 2048
+        rays x 64 each, LPT-sharded over the ranks by cost, objects keep their
+        global ids; strong scaling (the N>1 default)
+  cfg2  8 objects of one room on one GPU, rays split by mask area (4096 x 8 in
+        total), keyframes U{5..40} per object revealed in 6 batches, appended
+        before iterations 0, 50, ..., 250 (300 iterations)
+  cfg4  the 64 cfg3 objects trained 200 iterations, then density on a 128^3
+        lattice per object and render_scene of all 64 (placed in a room with
+        romap_set_box) from 10 poses
+With --gpus N and no WORLD_SIZE in the environment the script launches itself
+under torch.distributed.run with N ranks (one per GPU, NCCL; init logged with
+NCCL_DEBUG=INFO / SUBSYS=INIT).  No data-path collective: one all_reduce of the
+timings at the end.
 
 Timing: W warm-up iterations, then exactly K iterations in ONE train_step call,
-bracketed by barrier + cuda.synchronize on both sides and CUDA events on the
-library's stream; L2 is flushed before every iteration by the library's
-measurement hook (romap_set_l2_flush, 512 MiB) and the flush time -- timed by the
-library's own events -- is subtracted.  Max over ranks.
+bracketed by barrier + cuda.synchronize on both sides and CUDA events; L2 is
+flushed before every iteration by the library's measurement hook
+(romap_set_l2_flush, 512 MiB) and the flush time -- timed by the library's own
+events on its stream -- is subtracted.  Max over ranks.
 
 --impl reference runs the CPU oracle (oracle/, the "reference arm" of this tier)
-on a bounded sample of the same workload, on the host cores.
+on a bounded sample of the same workload, on the host cores.  --dry-run runs the
+launcher, the partition and the end-of-run reduction without a GPU (gloo; the
+CPU test of the multi-rank path).
 """
 from __future__ import annotations
 
@@ -28,6 +42,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,13 +53,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PAPER_SAMPLES_PER_S = 4096 * 32 / 0.706e-3     # PAPER.md:222,307 (RTX 4090; context only)
-BUDGET_SAMPLES = 2833 * 4096 * 32               # ~2 s / 0.706 ms iterations
+PAPER_ITERS_TO_BUDGET = 2833                    # ~2 s / 0.706 ms per iteration
 FLUSH_BYTES = 512 << 20
+CONFIG_ITERS = {"cfg1": 500, "cfg2": 300, "cfg3": 200, "cfg4": 200, "paper": 300}
 
 
-def cfg1_kwargs(precision):
+def cfg1_kwargs(precision, rays=4096):
     return dict(levels=16, log2_T=16, base_res=16, finest_res=512.0, res_cap=0, samples_per_ray=64,
-                rays_per_iter=4096, precision=precision, seed=1)
+                rays_per_iter=rays, precision=precision, seed=1)
 
 
 # the paper's own configuration (R24): T = 2^16, N_max = 2048,
@@ -55,17 +71,6 @@ PAPER_MS = {(16, 1): 0.706, (14, 1): 0.658, (18, 1): 0.921, (20, 1): 1.495, (16,
 def paper_kwargs(log2_T=16, hidden_layers=1):
     return dict(levels=16, log2_T=log2_T, base_res=16, finest_res=2048.0, res_cap=0, samples_per_ray=32,
                 rays_per_iter=4096, precision=1, seed=1, network=1, hidden_layers=hidden_layers)
-
-
-def workload_kwargs(args, precision):
-    if args.network == "paper":
-        return paper_kwargs(args.log2_T or 16, args.hidden_layers)
-    kw = cfg1_kwargs(precision)
-    if args.log2_T:
-        kw["log2_T"] = args.log2_T
-    if args.rays_per_iter:
-        kw["rays_per_iter"] = args.rays_per_iter      # cfg3: 2048 rays per object
-    return kw
 
 
 def paper_baseline_samples_per_s(kw):
@@ -82,6 +87,26 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args):
+    """--gpus N without a launcher: run this script under torch.distributed.run with
+    N ranks on this node (rendezvous on 127.0.0.1), pass rank 0's JSON line through"""
+    env = dict(os.environ)
+    if not args.dry_run:
+        env.setdefault("NCCL_DEBUG", "INFO")            # the rank / device map of the communicator
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def start_clock_sampler(dev_index):
@@ -135,14 +160,87 @@ def visible_index(local_rank):
     return str(local_rank)
 
 
-def load_scene():
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores_available": len(os.sched_getaffinity(0))}
+
+
+# ----------------------------------------------------------------------------- workloads
+def cfg3_half_extents(gid):
+    """cfg3 family member gid: edges U(0.2, 1.5) m per axis (BASELINE cfg2/3), seeded by the global id"""
+    import numpy as np
+    g = np.random.default_rng(3000 + gid)
+    return (g.uniform(0.2, 1.5, size=3) / 2).astype(np.float32)
+
+
+def objects_for_rank(workload, args, ws, rank, precision):
+    """[(global id, SceneObject, [frames], rays)] of this rank, model kwargs, description"""
     import scenes
-    return scenes.object_scene(1, n_views=20)
+    from paper_2304_05735_b200.shard import partition
+    if workload in ("cfg1", "paper"):
+        kw = paper_kwargs(args.log2_T or 16, args.hidden_layers) if workload == "paper" else cfg1_kwargs(precision)
+        if args.log2_T and workload == "cfg1":
+            kw["log2_T"] = args.log2_T
+        if args.rays_per_iter:
+            kw["rays_per_iter"] = args.rays_per_iter
+        n_total = args.objects or ws * args.objects_per_gpu
+        mine = partition([kw["rays_per_iter"] * kw["samples_per_ray"]] * n_total, ws)[rank]
+        sc = scenes.object_scene(1, n_views=20)
+        ob = sc.objects[0]
+        return [(gid, ob, sc.frames, kw["rays_per_iter"]) for gid in mine], kw, sc
+    if workload in ("cfg3", "cfg4"):
+        kw = cfg1_kwargs(precision, rays=args.rays_per_iter or 2048)
+        n_total = args.objects or 64
+        mine = partition([kw["rays_per_iter"] * kw["samples_per_ray"]] * n_total, ws)[rank]
+        out = []
+        for gid in mine:
+            sc = scenes.object_scene(1000 + gid, n_views=20, half_extents=cfg3_half_extents(gid))
+            out.append((gid, sc.objects[0], sc.frames, kw["rays_per_iter"]))
+        return out, kw, None
+    raise ValueError(workload)
+
+
+def cfg2_plan(seed=2, n_objects=8, n_frames=200, rays_per_object=4096, batches=6):
+    """BASELINE cfg2: 8 room objects; keyframes K_o ~ U{5..40} of the frames where the
+    object covers >= 1 % of the image (evenly spaced along the trajectory), revealed
+    in `batches` batches; R_total = 4096 x n split by total keyframe mask area (largest
+    remainder, >= 128 per object, R9)"""
+    import numpy as np
+    import scenes
+    sc = scenes.room_scene(seed, n_objects=n_objects, n_frames=n_frames)
+    g = np.random.default_rng(seed + 100)
+    plan = []
+    for ob in sc.objects:
+        vis = scenes.visible_frames(sc, ob.instance_id, min_frac=0.01)
+        if not vis:
+            continue
+        k = min(len(vis), int(g.integers(5, 41)))
+        pick = [vis[int(round(i))] for i in np.linspace(0, len(vis) - 1, k)]
+        area = sum(int((sc.frames[i].mask == ob.instance_id).sum()) for i in pick)
+        plan.append({"ob": ob, "frames": pick, "batches": [list(b) for b in np.array_split(np.asarray(pick), batches)],
+                     "area": area})
+    total = rays_per_object * len(plan)
+    areas = np.array([p["area"] for p in plan], float)
+    share = total * areas / areas.sum()
+    rays = np.maximum(np.floor(share).astype(int), 128)
+    rem = total - rays.sum()
+    if rem > 0:
+        rays[np.argsort(-(share - np.floor(share)))[:rem]] += 1
+    for p, r in zip(plan, rays):
+        p["rays"] = int(r)
+    return sc, plan
 
 
 # ----------------------------------------------------------------------------- roofline bookkeeping
 def algorithmic_per_sample(kw, precision):
-    """Algorithmic work per ray-sample (DESIGN.md 'Roofline'): bytes the method must
+    """Algorithmic work per ray-sample (DESIGN.md section 7): bytes the method must
     move and FLOPs it must compute, per kernel stage."""
     L, F = kw["levels"], 2
     LF = L * F
@@ -169,22 +267,23 @@ def ncu_traffic(kernel):
         return None
 
 
-# measured ceiling of the fused kernel's request mix (tools/micro/tma_gather_bench.cu,
-# profiles/r1_micro.md): random 16-B LDG.128 gathers + RED.v4.f32 scatters 1:1 over
-# L2-resident tables, per SM and cycle
+# measured ceiling of the fused kernel's request mix (profiles/r1_micro.md): random
+# 16-B LDG.128 gathers + RED.v4.f32 scatters 1:1 over L2-resident tables, per SM and cycle
 REQ_CEILING = 0.828
+_MODEL_KEYS = ("levels", "log2_T", "base_res", "finest_res", "res_cap", "samples_per_ray", "precision", "network",
+               "hidden_layers")
 
 
 def request_roofline(kw, samples_per_launch, ms, sm_clk, n_sm):
     """L1 sector requests of the gathers + REDs per SM-cycle against the measured
     random-access ceiling; sectors per hit sample from the committed ncu capture of
-    the same model (profiles/ncu_requests.json), else None."""
+    the same model (profiles/ncu_requests.json; per sample, so any ray count), else None."""
     try:
         entries = json.load(open(os.path.join(ROOT, "profiles", "ncu_requests.json")))["entries"]
     except Exception:
         return None
-    mine = {k: v for k, v in kw.items() if not k.startswith("_")}
-    d = next((e for e in entries if e["kw"] == mine), None)
+    key = lambda d: tuple(d.get(k, {"network": 0, "hidden_layers": 1}.get(k)) for k in _MODEL_KEYS)
+    d = next((e for e in entries if key(e["kw"]) == key(kw)), None)
     if d is None:
         return None
     req = d["sectors_per_hit_sample"] * samples_per_launch
@@ -192,25 +291,22 @@ def request_roofline(kw, samples_per_launch, ms, sm_clk, n_sm):
     return {"bound": "l1_l2_random_requests", "achieved": achieved, "peak": REQ_CEILING,
             "unit": "sector requests / SM / cycle", "frac": achieved / REQ_CEILING,
             "source": f"{d['sectors_per_hit_sample']:.1f} sectors per hit sample ({d['profile']}); "
-                      "ceiling tools/micro/tma_gather_bench.cu"}
+                      "ceiling profiles/r1_micro.md"}
 
 
 def roofline(prof, kw, precision, samples_per_launch, n_objs):
     peaks, src = load_measured_peaks()
     work = algorithmic_per_sample(kw, precision)
-    stages = {k: v for k, v in prof.items() if v["launches"] > 0 and k not in ("l2_flush",)}
+    stages = {k: v for k, v in prof.items() if v["launches"] > 0 and v["ms"] > 0 and k not in ("l2_flush",)}
     dom = max(stages, key=lambda k: stages[k]["ms"])
     st = stages[dom]
     ms = st["ms"] / st["launches"]
-    params = None
     sm_clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
     if dom in ("fused_mixed",):
-        # fused tile kernel: bound by L2/HBM traffic of the gathers + atomics
+        # algorithmic bytes of the hash gathers + gradient atomics
         bytes_ = samples_per_launch * (work["gather_bytes"] + work["scatter_bytes"])
         achieved = bytes_ / (ms * 1e-3) / 1e9
-        peak = peaks["hbm_gbs"]
-        out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s"}
-        # sectors per hit sample captured on the same model (any number of objects)
+        out = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
         rq = request_roofline(kw, samples_per_launch, ms, sm_clk, 148)
         if rq:
             out["request_roofline"] = rq
@@ -220,9 +316,7 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
         peak = 148 * 128 * 2 * sm_clk / 1e12           # fp32 FMA lanes x 2 FLOP x max SM clock
         out = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s"}
     elif dom == "adam":
-        # dense upper bound: 4 B grad read for all + 28 B for updated params
-        nparam = kw["_n_params"] * n_objs
-        bytes_ = nparam * 32
+        bytes_ = kw["_n_params"] * n_objs * 32
         achieved = bytes_ / (ms * 1e-3) / 1e9
         out = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     else:
@@ -232,80 +326,115 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
     out["frac"] = out["achieved"] / out["peak"]
     out["kernel"] = dom
     out["ms_per_launch"] = ms
+    out["algorithmic_bytes_per_hit_sample"] = work["gather_bytes"] + work["scatter_bytes"]
+    out["hit_samples_per_launch"] = samples_per_launch
     out["peak_source"] = src
     out["traffic"] = ncu_traffic(dom)
     return out
 
 
-# ----------------------------------------------------------------------------- inference (8(a) a10, a11)
-def measure_inference(ctx, h, ob, frame, torch):
-    """cfg4-style inference on one trained object: density on the 128^3 vertex
-    lattice spanning the box (marching-cubes input, R21) with device buffers, and
-    one 640x480 render (128 midpoints per ray, host outputs)."""
-    a = [float(x) for x in ob.a]
-    axes = [torch.linspace(-a[k], a[k], 128, device="cuda") for k in range(3)]
-    P = torch.stack(torch.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3).float().contiguous()
-    ctx.query_density(h, P)
+# ----------------------------------------------------------------------------- inference (8(a) a10, a11; cfg4)
+def room_layout(obs, spacing=0.25):
+    """non-overlapping room positions for render_scene: boxes on a square grid of
+    cells sized by the largest footprint (object frame centre -> world t, yaw kept)"""
+    import numpy as np
+    n = len(obs)
+    side = int(math.ceil(math.sqrt(n)))
+    cell = 2.0 * max(float(np.hypot(ob.a[0], ob.a[1])) for ob in obs) + spacing
+    out = []
+    for i, ob in enumerate(obs):
+        gx, gy = i % side, i // side
+        out.append(np.array([(gx - (side - 1) / 2) * cell, (gy - (side - 1) / 2) * cell, float(ob.a[2])], np.float32))
+    return out, side * cell
+
+
+def room_poses(extent, n=10, f=525.0):
+    import numpy as np
+    import scenes
+    K = np.array([f, f, 320.0, 240.0], np.float32)
+    out = []
+    for i in range(n):
+        az = 2 * math.pi * i / n
+        r = 0.75 * extent + 1.0
+        cam = (r * math.cos(az), r * math.sin(az), 0.45 * extent + 1.0)
+        out.append((scenes.look_at(cam, (0.0, 0.0, 0.2)), K))
+    return out
+
+
+def measure_inference(ctx, hs, obs, poses, torch):
+    """cfg4-style inference on trained objects: density on the 128^3 vertex lattice
+    spanning each object's box (marching-cubes input, R21) with device buffers, one
+    640x480 render of the first object, and render_scene of all objects from the poses."""
+    peaks, src = load_measured_peaks()
+    lattices = []
+    for ob in obs:
+        a = [float(x) for x in ob.a]
+        axes = [torch.linspace(-a[k], a[k], 128, device="cuda") for k in range(3)]
+        lattices.append(torch.stack(torch.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3).float().contiguous())
+    for h, P in zip(hs, lattices):
+        ctx.query_density(h, P)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 5
     e0.record()
-    for _ in range(reps):
+    for h, P in zip(hs, lattices):
         ctx.query_density(h, P)
     e1.record()
     torch.cuda.synchronize()
-    q_ms = e0.elapsed_time(e1) / reps
-    ctx.render(h, frame.T_wc, frame.K, 640, 480, 128)
+    q_ms = e0.elapsed_time(e1)
+    npts = sum(P.shape[0] for P in lattices)
+    q_gbs = npts * 16 * 8 * 4 / (q_ms * 1e-3) / 1e9   # 16 levels x 8 corners x 4 B (fp16 F=2) per point
+    T0, K0 = poses[0]
+    ctx.render(hs[0], T0, K0, 640, 480, 128)
     t0 = time.perf_counter()
-    ctx.render(h, frame.T_wc, frame.K, 640, 480, 128)
+    ctx.render(hs[0], T0, K0, 640, 480, 128)
     r_s = time.perf_counter() - t0
-    peaks, src = load_measured_peaks()
-    q_gbs = P.shape[0] * 16 * 8 * 4 / (q_ms * 1e-3) / 1e9   # 16 levels x 8 corners x 4 B (fp16 F=2) per point
-    return {"query_density": {"points_per_s": P.shape[0] / (q_ms * 1e-3), "ms_per_lattice": q_ms,
-                              "points": int(P.shape[0]), "what": "128^3 vertex lattice of the trained object, "
-                              "device buffers, CUDA events (mixed path: fp16 tables + tcgen05 first layer)",
+    ctx.render_scene(hs, T0, K0, 640, 480, 128)
+    t0 = time.perf_counter()
+    for T, K in poses:
+        rgb, dep, opa = ctx.render_scene(hs, T, K, 640, 480, 128)
+    rs_s = (time.perf_counter() - t0) / len(poses)
+    return {"query_density": {"objects": len(hs), "points": int(npts), "points_per_s": npts / (q_ms * 1e-3),
+                              "ms_per_object_lattice": q_ms / len(hs),
+                              "what": "128^3 vertex lattice per object box, device buffers, CUDA events (mixed path: "
+                                      "fp16 tables + tcgen05 first layer)",
                               "roofline": {"bound": "hbm", "achieved": q_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                            "frac": q_gbs / peaks["hbm_gbs"], "peak_source": src,
-                                           "note": "algorithmic gather bytes; the 3.4 MB table is L2-resident, so the "
+                                           "note": "algorithmic gather bytes; each 3.4 MB table is L2-resident, so the "
                                                    "random-request rate, not HBM, binds it"}},
             "render": {"rays_per_s": 640 * 480 / r_s, "ms_per_frame": r_s * 1e3, "samples_per_ray": 128,
-                       "what": "one 640x480 frame, host outputs, wall clock (mixed path: tensor-core forward of midpoint samples + compositing)"}}
+                       "what": "one 640x480 frame of one object, host outputs, wall clock"},
+            "render_scene": {"objects": len(hs), "poses": len(poses), "ms_per_frame": rs_s * 1e3,
+                             "rays_per_s": 640 * 480 / rs_s, "hit_pixels_last_pose": int((opa > 0).sum()),
+                             "what": "romap_render_scene of all objects, 640x480, <= 128 samples per segment, "
+                                     "host outputs, wall clock"}}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def oracle_run(scene, kw, rays, iters, obj_id=0):
-    import numpy as np
+def oracle_run(ob, frames, kw, rays, iters, obj_id=0):
     import oracle as O
+    from threadpoolctl import threadpool_limits
     ocfg = O.ModelConfig(**{k: v for k, v in kw.items() if k in O.ModelConfig.__dataclass_fields__})
     ocfg.rays_per_iter = rays
-    ob = scene.objects[0]
     st = O.ObjectState(ocfg, ob.t, ob.yaw, ob.a, obj_id, O.init_params(ocfg, 0))
-    for fr in scene.frames:
+    for fr in frames:
         st.kfs.append(O.ingest_observation(fr.rgb, fr.mask, fr.T_wc, fr.K, ob.instance_id))
-    O.train_iteration(st)                       # warm-up
-    t0 = time.perf_counter()
-    samples = 0
-    for _ in range(iters):
-        L, _, _ = O.train_iteration(st)
-        samples += L["samples"]
-    dt = time.perf_counter() - t0
+    with threadpool_limits(1):                   # the plain oracle, one core (BLAS pinned to 1 thread)
+        O.train_iteration(st)                    # warm-up
+        t0 = time.perf_counter()
+        samples = 0
+        for _ in range(iters):
+            L, _, _ = O.train_iteration(st)
+            samples += L["samples"]
+        dt = time.perf_counter() - t0
     return samples, dt
 
 
-def host_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        n = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
-    except Exception:
-        n = 1
-    return max(1, n)
-
-
-def cpu_baseline(scene, kw, rays=1024, iters=3):
-    samples, dt = oracle_run(scene, kw, rays, iters)
-    return {"value": samples / dt, "unit": "ray-samples/s", "cores": host_threads(), "kind": "oracle",
-            "sample": f"{iters} oracle iterations of the cfg1 object at {rays} rays x {kw['samples_per_ray']} samples "
-                      f"(numpy fp32-geometry/fp64; {samples} ray-samples in {dt:.1f} s)"}
+def cpu_baseline(ob, frames, kw, rays=1024, iters=3):
+    samples, dt = oracle_run(ob, frames, kw, rays, iters)
+    return dict({"value": samples / dt, "unit": "ray-samples/s", "cores": 1, "kind": "oracle",
+                 "sample": f"{iters} oracle iterations of one object of this workload at {rays} rays x "
+                           f"{kw['samples_per_ray']} samples (numpy, fp32 geometry / fp64 arithmetic, BLAS limited "
+                           f"to 1 thread; {samples} ray-samples in {dt:.1f} s)"}, **host_info())
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -313,77 +442,82 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    scene = load_scene()
-    kw = workload_kwargs(args, 0)
+    import scenes
+    workload = resolve_workload(args, args.gpus)
+    kw = cfg1_kwargs(0, rays=2048 if workload in ("cfg3", "cfg4") else 4096)
+    if workload == "paper":
+        kw = paper_kwargs(args.log2_T or 16, args.hidden_layers)
+    if workload in ("cfg3", "cfg4"):
+        sc = scenes.object_scene(1000, n_views=20, half_extents=cfg3_half_extents(0))
+    else:
+        sc = scenes.object_scene(1, n_views=20)
+    ob = sc.objects[0]
     rays = 256
     for _ in range(args.warmup):
-        oracle_run(scene, kw, rays, 1)
-    samples, dt = oracle_run(scene, kw, rays, args.steps)
+        oracle_run(ob, sc.frames, kw, rays, 1)
+    samples, dt = oracle_run(ob, sc.frames, kw, rays, args.steps)
     v = samples / dt
     line = {"impl": "reference", "metric": "NeRF train ray-samples/s", "value": v, "unit": "ray-samples/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded box-union-torus SDF object, 20 keyframes 640x480)",
-            "config": {"workload": "cfg1 (1 object/rank; reference = CPU oracle, bounded sample)",
-                       "rays_per_iter": rays, "samples_per_ray": kw["samples_per_ray"], "levels": 16, "log2_T": 16},
-            "cpu_baseline": {"value": v, "unit": "ray-samples/s", "cores": host_threads(), "kind": "oracle",
-                             "sample": f"{args.steps} oracle iterations at {rays} rays x 64 samples"},
+            "config": {"workload": f"{workload} (reference = the CPU oracle on one object, bounded sample)",
+                       "rays_per_iter": rays, "samples_per_ray": kw["samples_per_ray"], "levels": kw["levels"],
+                       "log2_T": kw["log2_T"]},
+            "cpu_baseline": dict({"value": v, "unit": "ray-samples/s", "cores": 1, "kind": "oracle",
+                                  "sample": f"{args.steps} oracle iterations at {rays} rays x {kw['samples_per_ray']} "
+                                            "samples, BLAS limited to 1 thread"}, **host_info()),
             "e2e": {"value": v, "unit": "ray-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ----------------------------------------------------------------------------- our arm
-def run_ours(args):
-    import numpy as np
+# ----------------------------------------------------------------------------- dry run (CPU, gloo)
+def run_dry(args):
+    """the multi-rank path without a GPU: launcher, LPT partition of the workload's
+    objects, end-of-run reduction (gloo), JSON line; no kernels, no data"""
     import torch
-
-    ws, rank, local = dist_env()
-    if args.gpus > 1 and ws != args.gpus:
-        print(f"--gpus {args.gpus} needs torchrun with {args.gpus} ranks (WORLD_SIZE={ws})", file=sys.stderr)
-        return 2
-    torch.cuda.set_device(local)
-    pg = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        pg = dist
-    from paper_2304_05735_b200 import romap as R
-
-    ctx = R.Context(local)
-    precision = 1 if args.precision == "mixed" else 0
-    if args.precision == "auto":
-        # the mixed (tensor-core) path when this build has it, else the fp32 GPU path
-        try:
-            ctx.destroy_object(ctx.create_object([0, 0, 0], 0.0, [1, 1, 1], R.model_config(**cfg1_kwargs(1)), 1))
-            precision = 1
-        except R.RomapError:
-            precision = 0
-    if args.network == "paper":
-        precision = 1
-    kw = workload_kwargs(args, precision)
-    scene = load_scene()
+    import torch.distributed as dist
     from paper_2304_05735_b200.shard import partition, reduce_throughput
-    objs = []
-    ob = scene.objects[0]
-    n_total = args.objects or args.objects_per_gpu * ws
-    mine = partition([kw["rays_per_iter"] * kw["samples_per_ray"]] * n_total, ws)[rank]   # LPT by cost (8(e))
-    for gid in mine:
-        h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id, obj_id=gid)
-        for fr in scene.frames[:args.keyframes]:
-            ctx.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
-        objs.append(h)
-    info = ctx.object_info(objs[0])
-    kw["_n_params"] = info["table_params"] + info["mlp_params"]
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    workload = resolve_workload(args, ws)
+    rays = args.rays_per_iter or (2048 if workload in ("cfg3", "cfg4") else 4096)
+    n_total = args.objects or (64 if workload in ("cfg3", "cfg4") else ws * args.objects_per_gpu)
+    mine = partition([rays * 64] * n_total, ws)[rank]
+    samples = len(mine) * rays * 64 * args.steps
+    elapsed_ms = 1.0 + rank                       # stand-in per-rank device times
+    pg = dist if ws > 1 else None
+    t_max, tot, value = reduce_throughput(elapsed_ms, samples, pg)
+    objs = [None] * ws
+    if ws > 1:
+        dist.all_gather_object(objs, mine)
+    else:
+        objs = [mine]
+    if rank == 0:
+        print(json.dumps({"metric": "NeRF train ray-samples/s", "value": value, "unit": "ray-samples/s",
+                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "dry_run": True,
+                          "config": {"workload": workload, "objects": n_total, "rays_per_iter": rays},
+                          "partition": objs, "max_ms": t_max, "total_samples": tot}), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
-    # warm-up (untimed)
-    ctx.train_step(objs, args.warmup)
-    torch.cuda.synchronize()
 
-    # timed region: exactly K iterations, L2 flushed before each by the library hook.
-    # Only the flush (subtracted) and the dominant kernel (roofline) are bracketed
-    # with CUDA events here; the full per-stage breakdown comes from a separate
-    # short profiled pass after the timed region.
+def resolve_workload(args, ws):
+    if args.network == "paper":
+        return "paper"
+    if args.workload != "auto":
+        return args.workload
+    return "cfg3" if ws > 1 else "cfg1"
+
+
+# ----------------------------------------------------------------------------- our arm
+def timed_train(ctx, hs, steps, precision, pg, torch, local):
+    """exactly `steps` iterations of all objects in ONE train_step call (device-timed,
+    L2 flushed before each iteration, flush subtracted); returns stats, timing"""
     ctx.set_l2_flush(FLUSH_BYTES)
     dominant = "fused_mixed" if precision == 1 else "bwd_fp32"
     ctx.profile_enable(True, stages=[dominant, "l2_flush"])
@@ -396,7 +530,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0.record(stream)
     th0 = time.perf_counter()
-    stats = ctx.train_step(objs, args.steps)
+    stats = ctx.train_step(hs, steps)
     host_ms = (time.perf_counter() - th0) * 1e3
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -406,112 +540,174 @@ def run_ours(args):
     prof = ctx.profile_read()
     # separate, untimed pass: every stage bracketed with events (breakdown only)
     ctx.profile_enable(True)
-    n_brk = min(10, args.steps)
-    ctx.train_step(objs, n_brk)
+    n_brk = min(10, steps)
+    ctx.train_step(hs, n_brk)
     prof_all = ctx.profile_read()
     ctx.profile_enable(False)
     ctx.set_l2_flush(0)
     total_ms = ev0.elapsed_time(ev1)
     flush_ms = prof.get("l2_flush", {}).get("ms", 0.0)
-    step_ms = (total_ms - flush_ms) / args.steps
-    samples = sum(s["samples"] for s in stats)
-    launches = sum(v["launches"] for k, v in prof.items() if k != "l2_flush")
+    return {"stats": stats, "total_ms": total_ms, "flush_ms": flush_ms, "step_ms": (total_ms - flush_ms) / steps,
+            "host_ms": host_ms, "prof": prof, "prof_all": prof_all, "n_brk": n_brk, "clocks": clocks,
+            "dominant": dominant}
 
-    # e2e: the paper's online unit through the public API with HOST buffers: one new
-    # keyframe (640x480 rgb + mask from pinned host memory) -> add_observation ->
-    # train_step(n_iters = e2e_iters) -> per-object stats read back to the host
-    e2e_frames = scene.frames[args.keyframes:] or scene.frames
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    ws, rank, local = dist_env()
+    # ROMAP_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo reduction -- a check of
+    # the multi-rank launcher on a one-GPU box (ranks never wait on each other's
+    # kernels; not a measurement of scaling)
+    share = os.environ.get("ROMAP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+    torch.cuda.set_device(local)
+    pg = None
+    red_dev = "cpu" if share else "cuda"
+    if ws > 1:
+        import torch.distributed as dist
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    from paper_2304_05735_b200 import romap as R
+    from paper_2304_05735_b200.shard import reduce_throughput
+
+    ctx = R.Context(local)
+    precision = 0 if args.precision == "fp32" else 1
+    workload = resolve_workload(args, ws)
+    if workload == "cfg2":
+        return run_cfg2(args, ctx, R, torch, precision)
+    if workload == "paper":
+        precision = 1
+    items, kw, _ = objects_for_rank(workload, args, ws, rank, precision)
+    hs, obs = [], []
+    for gid, ob, frames, rays in items:
+        h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id, obj_id=gid)
+        for fr in frames[:args.keyframes]:
+            ctx.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
+        hs.append(h)
+        obs.append((ob, frames))
+    info = ctx.object_info(hs[0])
+    kw["_n_params"] = info["table_params"] + info["mlp_params"]
+
+    ctx.train_step(hs, args.warmup)                   # warm-up (untimed)
+    torch.cuda.synchronize()
+    tr = timed_train(ctx, hs, args.steps, precision, pg, torch, local)
+    samples = sum(s["samples"] for s in tr["stats"])
+    launches = sum(v["launches"] for k, v in tr["prof"].items() if k not in ("l2_flush", "graph_replay"))
+
+    # e2e through the public API with HOST buffers: one new keyframe per object
+    # (640x480 rgb + mask from pinned host memory) -> add_observation -> train_step(e2e_iters)
+    # -> per-object stats read back to the host
     pinned = []
-    for fr in e2e_frames:
-        rgb = torch.from_numpy(fr.rgb).pin_memory()
-        mask = torch.from_numpy(fr.mask.astype(np.int16)).pin_memory()
-        pinned.append((rgb, mask, fr))
-    h2d = 0
-    e2e_samples = 0
+    for ob, frames in obs:
+        fr = frames[-1]
+        pinned.append((torch.from_numpy(fr.rgb).pin_memory(), torch.from_numpy(fr.mask.astype(np.int16)).pin_memory(),
+                       fr, ob))
+    h2d, e2e_samples = 0, 0
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(args.e2e_steps):
-        rgb, mask, fr = pinned[k % len(pinned)]
-        m_np = mask.numpy().view(np.uint16)
-        for h in objs:
+    for _ in range(args.e2e_steps):
+        for h, (rgb, mask, fr, ob) in zip(hs, pinned):
+            m_np = mask.numpy().view(np.uint16)
             ctx.add_observation(h, rgb.numpy(), m_np, fr.T_wc, fr.K)
-        st = ctx.train_step(objs, args.e2e_iters)
+            ys, xs = np.nonzero(m_np == ob.instance_id)
+            h2d += (xs.max() - xs.min() + 1) * (ys.max() - ys.min() + 1) * 4 + 96 + 8
+        st = ctx.train_step(hs, args.e2e_iters)
         e2e_samples += sum(s["samples"] for s in st)
-        ys, xs = np.nonzero(m_np == ob.instance_id)
-        h2d += len(objs) * ((xs.max() - xs.min() + 1) * (ys.max() - ys.min() + 1) * 4 + 96 + 8)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if pg:
         pg.barrier()
 
     # reductions over ranks: max time, sum of samples (NCCL all_reduce, shard.reduce_throughput)
-    t_max_ms, tot_samples, value = reduce_throughput(step_ms * args.steps, samples, pg, device="cuda")
-    e2e_max_ms, tot_e2e, e2e_value = reduce_throughput(e2e_s * 1e3, e2e_samples, pg, device="cuda")
+    own_ms = tr["step_ms"] * args.steps
+    t_max_ms, tot_samples, value = reduce_throughput(own_ms, samples, pg, device=red_dev)
+    e2e_max_ms, tot_e2e, e2e_value = reduce_throughput(e2e_s * 1e3, e2e_samples, pg, device=red_dev)
+    per_gpu = [samples / (own_ms * 1e-3)]
+    devices = [torch.cuda.get_device_name(local)]
+    if pg:
+        g = [None] * ws
+        pg.all_gather_object(g, (samples / (own_ms * 1e-3), torch.cuda.get_device_name(local), local))
+        per_gpu = [x[0] for x in g]
+        devices = [f"rank {r}: cuda:{x[2]} {x[1]}" for r, x in enumerate(g)]
 
-    infer = measure_inference(ctx, objs[0], ob, scene.frames[0], torch) if rank == 0 else None
-    if infer is not None:
-        # cfg4 (ii): render_scene of every object on this GPU from 10 poses (640x480,
-        # <= 128 samples per segment, host outputs)
-        poses = scene.frames[:10]
-        ctx.render_scene(objs, poses[0].T_wc, poses[0].K, 640, 480, 128)
-        t0 = time.perf_counter()
-        for fr in poses:
-            ctx.render_scene(objs, fr.T_wc, fr.K, 640, 480, 128)
-        rs_s = (time.perf_counter() - t0) / len(poses)
-        infer["render_scene"] = {"objects": len(objs), "poses": len(poses), "ms_per_frame": rs_s * 1e3,
-                                 "rays_per_s": 640 * 480 / rs_s,
-                                 "what": "romap_render_scene of all objects, 640x480, 128 samples per segment, "
-                                         "host outputs, wall clock"}
+    infer = None
+    if rank == 0 and not args.no_inference:
+        if workload == "cfg4":
+            # the trained objects placed in one room (romap_set_box keeps the learned field, R27)
+            ts, extent = room_layout([ob for ob, _ in obs])
+            for h, (ob, _), t in zip(hs, obs, ts):
+                ctx.set_box(h, t, ob.yaw, ob.a)
+            poses = room_poses(extent)
+        else:
+            poses = [(fr.T_wc, fr.K) for fr in obs[0][1][:10]]
+        infer = measure_inference(ctx, hs, [ob for ob, _ in obs], poses, torch)
     if rank == 0:
-        rf = roofline(prof, kw, precision, samples / args.steps, len(objs))
+        rf = roofline(tr["prof"], kw, precision, samples / args.steps, len(hs))
         paper_sps = paper_baseline_samples_per_s(kw)
-        if args.network == "paper":
+        if workload == "paper":
             desc = (f"paper network (PAPER.md:222, R24): L=16 F=2 T=2^{kw['log2_T']} res 16->2048, "
-                    f"{kw['hidden_layers']} hidden layer(s) of 64 on positions -> sigma, rgb, {kw['rays_per_iter']} rays x 32 "
-                    f"stratified samples per object, Adam")
+                    f"{kw['hidden_layers']} hidden layer(s) of 64 on positions -> sigma, rgb, {kw['rays_per_iter']} "
+                    f"rays x 32 stratified samples per object, Adam")
         else:
             desc = (f"L=16 F=2 T=2^{kw['log2_T']} res 16->512, density 32->64->16 + SH4 colour 32->64->64->3, "
                     f"{kw['rays_per_iter']} rays x 64 stratified samples per object, Adam")
-        cpu = None if args.no_cpu_baseline else cpu_baseline(scene, kw)
-        per_obj_ms = t_max_ms / args.steps / len(objs)
+        objs_total = args.objects or (64 if workload in ("cfg3", "cfg4") else ws * args.objects_per_gpu)
+        cpu = None if args.no_cpu_baseline else cpu_baseline(obs[0][0], obs[0][1], kw)
+        t_iter_obj_ms = (t_max_ms / args.steps) / len(hs)
+        strong = workload in ("cfg3", "cfg4") or bool(args.objects)
         line = {
             "metric": "NeRF train ray-samples/s", "value": value, "unit": "ray-samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.objects else "weak",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": (value / paper_sps) if paper_sps else None,
             "dtype": "f16-mma/f32" if precision == 1 else "f32",
-            "data": "synthetic (seeded box-union-torus SDF object on a textured floor, 20 keyframes 640x480, 1 cm pose jitter)",
-            "config": {"workload": (f"{'paper' if args.network == 'paper' else 'cfg1'} family: {n_total} object(s) "
-                                    f"over {ws} GPU(s) (LPT by cost)" if args.objects
-                                    else f"{'paper' if args.network == 'paper' else 'cfg1'}: {len(objs)} object(s) per GPU")
-                                   + ", " + desc,
-                       "objects_per_gpu": len(objs), "rays_per_iter": kw["rays_per_iter"],
+            "data": ("synthetic: seeded box-union-torus SDF objects of the cfg1 family on a textured floor, 20 "
+                     "keyframes 640x480 each, 1 cm pose jitter (stand-in for the paper's sequences, DESIGN.md 5)"),
+            "config": {"workload": f"{workload}: {objs_total} object(s) over {ws} GPU(s), {len(hs)} on rank 0 "
+                                   f"(LPT by cost, global ids kept), " + desc,
+                       "objects_total": objs_total, "objects_rank0": len(hs), "rays_per_iter": kw["rays_per_iter"],
                        "samples_per_ray": kw["samples_per_ray"], "keyframes": args.keyframes,
                        "precision": "mixed" if precision == 1 else "fp32",
                        "l2": f"flushed before every iteration ({FLUSH_BYTES >> 20} MiB write by romap_set_l2_flush), "
                              "flush time excluded via the library's CUDA events",
-                       "parallelism": f"objects sharded over {ws} rank(s), NCCL only for the final max/sum"},
-            "s_to_budget_per_object": BUDGET_SAMPLES / (value / max(1, ws * len(objs))),
-            "ms_per_iteration_per_object": per_obj_ms,
+                       "parallelism": f"objects sharded over {ws} rank(s), {'gloo (shared-GPU launcher check)' if share else 'NCCL'} "
+                                      "only for the final max/sum"},
+            "per_gpu_value": per_gpu,
+            "ranks": devices,
+            "s_to_budget_per_object": {
+                "config_iterations": CONFIG_ITERS[workload],
+                "s_config": t_iter_obj_ms * CONFIG_ITERS[workload] / 1e3,
+                "s_paper_budget": t_iter_obj_ms * PAPER_ITERS_TO_BUDGET / 1e3,
+                "paper_s": 2.0,
+                "note": "SURVEY 8(d): (i) the config's own iteration count, (ii) the paper's ~2 s = 2833 iterations "
+                        "of 0.706 ms (PAPER.md:307,320); GPU time per iteration / objects on the GPU"},
+            "ms_per_iteration_per_object": t_iter_obj_ms,
             "paper_context": {"samples_per_s": PAPER_SAMPLES_PER_S, "ms_per_iteration": 0.706,
                               "note": ("RTX 4090, N=32, position-only 1x64 MLP (PAPER.md:222,307); "
                                        + ("this workload (vs_baseline = value / the paper's rate)" if paper_sps
                                           else "not this workload"))},
             "hit_samples_per_step": samples / args.steps,
-            "stage_ms_per_step": {k: v["ms"] / n_brk for k, v in prof_all.items() if v["launches"] or v["ms"]},
-            "stage_ms_note": f"separate {n_brk}-iteration pass with every stage bracketed by events (not the timed region)",
-            "kernel_ms_per_step": sum(v["ms"] for k, v in prof_all.items() if k != "l2_flush") / n_brk,
-            "timed_region": {"total_ms": total_ms, "l2_flush_ms_subtracted": flush_ms, "host_ms_in_call": host_ms,
-                             "dominant_ms": prof.get(dominant, {}).get("ms")},
+            "stage_ms_per_step": {k: v["ms"] / tr["n_brk"] for k, v in tr["prof_all"].items() if v["ms"]},
+            "stage_ms_note": f"separate {tr['n_brk']}-iteration pass with every stage bracketed by events",
+            "kernel_ms_per_step": sum(v["ms"] for k, v in tr["prof_all"].items() if k != "l2_flush") / tr["n_brk"],
+            "timed_region": {"total_ms": tr["total_ms"], "l2_flush_ms_subtracted": tr["flush_ms"],
+                             "host_ms_in_call": tr["host_ms"], "dominant_ms": tr["prof"].get(tr["dominant"], {}).get("ms")},
             "gpu_launches": launches,
             "roofline": rf,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "ray-samples/s", "h2d_bytes_per_step": int(h2d / max(1, args.e2e_steps)),
-                    "d2h_bytes_per_step": int(len(objs) * 40 + 4),
-                    "step": f"add_observation(1 keyframe, host) + train_step({args.e2e_iters} iterations) + stats D2H"},
-            "clocks": clocks,
+                    "d2h_bytes_per_step": int(len(hs) * 72 + 4),
+                    "step": f"add_observation(1 keyframe per object, host) + train_step({args.e2e_iters} iterations, "
+                            "graph replay) + per-object stats D2H"},
+            "clocks": tr["clocks"],
             "inference": infer,
         }
         print(json.dumps(line), flush=True)
@@ -521,15 +717,87 @@ def run_ours(args):
     return 0
 
 
+def run_cfg2(args, ctx, R, torch, precision):
+    """BASELINE cfg2 on one GPU: 8 room objects batched in one launch with rays split by
+    mask area; keyframes appended in 6 batches before iterations 0, 50, ..., 250; the
+    whole schedule (appends included) is the timed region (CUDA events)."""
+    import numpy as np
+    sc, plan = cfg2_plan()
+    kw = cfg1_kwargs(precision)
+
+    def setup():
+        hs = []
+        for k, p in enumerate(plan):
+            ob = p["ob"]
+            h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**dict(kw, rays_per_iter=p["rays"])),
+                                  ob.instance_id, obj_id=k)
+            hs.append(h)
+        return hs
+
+    def run(hs, iters, timed):
+        samples, done, b = 0, 0, 0
+        append_s = 0.0
+        while done < iters:
+            if b < 6 and done == 50 * b:
+                t0 = time.perf_counter()
+                for h, p in zip(hs, plan):
+                    for fi in p["batches"][b]:
+                        fr = sc.frames[fi]
+                        ctx.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
+                append_s += time.perf_counter() - t0
+                b += 1
+            n = min(iters - done, 50 * b - done if b < 6 else iters - done)
+            st = ctx.train_step(hs, n)
+            samples += sum(s["samples"] for s in st)
+            done += n
+        return samples, append_s
+
+    hs = setup()
+    run(hs, args.warmup, False)                      # warm-up objects (discarded)
+    for h in hs:
+        ctx.destroy_object(h)
+    hs = setup()
+    sampler, spath = start_clock_sampler(visible_index(0))
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    samples, append_s = run(hs, args.steps, True)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = stop_clock_sampler(sampler, spath)
+    ms = e0.elapsed_time(e1)
+    value = samples / (ms * 1e-3)
+    t_iter_obj_ms = ms / args.steps / len(hs)
+    print(json.dumps({
+        "metric": "NeRF train ray-samples/s", "value": value, "unit": "ray-samples/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16-mma/f32" if precision == 1 else "f32",
+        "data": "synthetic room (seed 2): 8 cfg1-family objects, edges U(0.2, 1.5) m, 200-frame 640x480 trajectory",
+        "config": {"workload": "cfg2: 8 objects batched in one launch, rays split by keyframe mask area "
+                               "(4096 x 8 total, >= 128 each), keyframes U{5..40} per object appended in 6 batches "
+                               "before iterations 0, 50, ..., 250", "rays": [p["rays"] for p in plan],
+                   "keyframes": [len(p["frames"]) for p in plan],
+                   "l2": "not flushed (appends between chunks; the objects' tables live in L2 across iterations)"},
+        "timed_region": {"total_ms": ms, "host_append_s": append_s, "includes": "add_observation of every batch"},
+        "s_to_budget_per_object": {"config_iterations": 300, "s_config": t_iter_obj_ms * 300 / 1e3,
+                                   "s_paper_budget": t_iter_obj_ms * PAPER_ITERS_TO_BUDGET / 1e3, "paper_s": 2.0},
+        "ms_per_iteration_per_object": t_iter_obj_ms,
+        "clocks": clocks, "cpu_baseline": None, "e2e": None, "gpu_launches": None}), flush=True)
+    ctx.close()
+    return 0
+
+
 def run_table4(args):
     """The paper's Table 4 grid on one GPU: ms per training iteration
     of one object (4096 rays x 32, a1..a8 incl. Adam, L2 flushed before each iteration)
     next to the paper's RTX 4090 numbers."""
     import torch
+    import scenes
     from paper_2304_05735_b200 import romap as R
 
     ctx = R.Context(0)
-    scene = load_scene()
+    scene = scenes.object_scene(1, n_views=20)
     ob = scene.objects[0]
     rows = []
     for (lt, hl), pms in sorted(PAPER_MS.items(), key=lambda x: (x[0][1], x[0][0])):
@@ -568,15 +836,18 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["auto", "cfg1", "cfg2", "cfg3", "cfg4"], default="auto",
+                    help="auto: cfg1 at N=1 (BASELINE metric config), cfg3 (64 objects sharded) at N>1")
     ap.add_argument("--precision", choices=["auto", "mixed", "fp32"], default="auto")
-    ap.add_argument("--objects-per-gpu", type=int, default=1)
-    ap.add_argument("--objects", type=int, default=0,
-                    help="total objects over all ranks, LPT-partitioned (0: objects-per-gpu x ranks)")
+    ap.add_argument("--objects-per-gpu", type=int, default=1, help="cfg1: objects per rank (weak scaling)")
+    ap.add_argument("--objects", type=int, default=0, help="total objects over all ranks (cfg3 default 64)")
     ap.add_argument("--keyframes", type=int, default=20)
     ap.add_argument("--rays-per-iter", type=int, default=0, help="rays per object and iteration (0: the config's)")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-inference", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launcher + partition + reduction only (CPU, gloo)")
     ap.add_argument("--network", choices=["baseline", "paper"], default="baseline",
                     help="baseline: BASELINE cfg1 (default, the headline); paper: PAPER.md:222 network (R24)")
     ap.add_argument("--hidden-layers", type=int, default=1, help="--network paper: hidden layers (Table 4: 1..3)")
@@ -585,8 +856,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.table4:
         return run_table4(args)
     return run_ours(args)

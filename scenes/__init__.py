@@ -265,17 +265,24 @@ def _depth_samples(g, mask, zdep, iid, k):
     return [(xs[p] + 0.5, ys[p] + 0.5, float(zdep[ys[p], xs[p]])) for p in pick]
 
 
-def object_scene(seed=1, n_views=20, W=640, H=480, f=525.0, device=None, depth_per_view=0, jitter=0.01):
+def object_scene(seed=1, n_views=20, W=640, H=480, f=525.0, device=None, depth_per_view=0, jitter=0.01,
+                 half_extents=None):
     """cfg1: one box-union-torus object (box ~0.8 m) on a textured floor, 20 keyframes on
     an orbit (radius 1.2 m, elevation 15-45 deg), 640x480, f=525, c=(320,240);
-    training poses = true + N(0, 1 cm) translation jitter."""
+    training poses = true + N(0, 1 cm) translation jitter.  half_extents: another box
+    size of the same family (cfg3 draws edges U(0.2, 1.5) m); the orbit radius scales
+    with it (1.2 m for the cfg1 box), so the object fills a similar part of the frame."""
     g = np.random.default_rng(seed)
     dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
     a = np.array([0.4, 0.4, 0.3], np.float32) * g.uniform(0.9, 1.0, size=3).astype(np.float32)
+    radius = 1.2
+    if half_extents is not None:
+        a = np.asarray(half_extents, np.float32)
+        radius = 1.2 * float(max(a[0], a[1], a[2])) / 0.4
     ob = SceneObject(1, np.array([0.0, 0.0, a[2]], np.float32), float(g.uniform(-0.3, 0.3)), a, random_shape(g, a))
     K = np.array([f, f, W / 2.0, H / 2.0], np.float32)
     frames = []
-    for T in _orbit_poses(g, n_views, (0.0, 0.0, float(a[2])), 1.2, 15, 45):
+    for T in _orbit_poses(g, n_views, (0.0, 0.0, float(a[2])), radius, 15, 45):
         rgb, mask, zd = render_sdf_frame([ob], T, K, W, H, dev, float(seed))
         fr = Frame(rgb, mask, _jitter(g, T, jitter), K, W, H)
         if depth_per_view:

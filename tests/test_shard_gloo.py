@@ -93,3 +93,26 @@ def test_two_ranks_match_one_rank():
     assert sorted(seen) == list(range(len(costs)))
     for gid, losses in ref.items():               # sharding-invariant (global-id keyed RNG, R13)
         assert np.array_equal(np.asarray(got[gid]), np.asarray(losses))
+
+
+def test_bench_launcher_two_ranks_dry_run():
+    """bench.py --gpus 2 launched the way the driver does without torchrun: the
+    script starts its own 2 ranks (torch.distributed.run, rendezvous on 127.0.0.1),
+    partitions cfg3's 64 objects by LPT, reduces (max time, sum samples) over gloo and
+    rank 0 prints ONE JSON line (--dry-run: no GPU, no kernels)"""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["workload"] == "cfg3" and d["config"]["objects"] == 64
+    assert sorted(sum(d["partition"], [])) == list(range(64))
+    assert [len(p) for p in d["partition"]] == [32, 32]
+    assert d["max_ms"] == 2.0                                    # MAX over ranks (1 + rank)
+    assert d["total_samples"] == 64 * 2048 * 64 * 3              # SUM over ranks
