@@ -738,62 +738,4 @@ void launch_debug_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* 
     k_debug<<<(unsigned)((S + 127) / 128), 128, 0, lc.st>>>(cfg, objs, rays, ray_begin, n_rays, what, out);
 }
 
-// ---------------------------------------------------------------------------
-// a11 render_scene (R20): t_near of every pixel's segment in one object's box
-// (+inf for a miss), taken from that object's render rays
-__global__ void __launch_bounds__(256) k_seg_tnear(const RayRec* __restrict__ rays, long long n, float* __restrict__ tn) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const RayRec& r = rays[p];
-    tn[p] = (r.flags & RF_ACTIVE) ? r.tn : __int_as_float(0x7f800000);
-}
-
-void launch_seg_tnear(const LaunchCtx& lc, const RayRec* rays, long long n, float* tn) {
-    if (n > 0) k_seg_tnear<<<(unsigned)((n + 255) / 256), 256, 0, lc.st>>>(rays, n, tn);
-}
-
-// per pixel: the n_obj segments (objects in ascending id order; per object a
-// slice of 6 HW floats: C interleaved rgb (3 HW), A, D, t_near) composited front to back in
-// ascending (t_near, id) order over black: C += T C_s, D += T D_s, T *= 1 - A_s
-__global__ void __launch_bounds__(256) k_scene_composite(int n_obj, long long HW, const float* __restrict__ seg,
-                                                         float* __restrict__ out_rgb, float* __restrict__ out_depth,
-                                                         float* __restrict__ out_opa) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= HW) return;
-    const long long stride = 6 * HW;
-    float C[3] = {0.f, 0.f, 0.f}, D = 0.f, T = 1.f;
-    float last_t = -__int_as_float(0x7f800000);
-    int last_o = -1;
-    for (int step = 0; step < n_obj; ++step) {
-        // next segment after (last_t, last_o) in (t_near, id) order
-        int best = -1;
-        float bt = __int_as_float(0x7f800000);
-        for (int o = 0; o < n_obj; ++o) {
-            const float t = seg[o * stride + 5 * HW + p];
-            const bool after = t > last_t || (t == last_t && o > last_o);
-            if (after && (t < bt || (t == bt && best < 0))) { bt = t; best = o; }
-        }
-        if (best < 0 || !(bt < __int_as_float(0x7f800000))) break;
-        const float* sb = seg + best * stride;
-        C[0] += T * sb[3 * p];
-        C[1] += T * sb[3 * p + 1];
-        C[2] += T * sb[3 * p + 2];
-        D += T * sb[4 * HW + p];
-        T *= 1.0f - sb[3 * HW + p];
-        last_t = bt;
-        last_o = best;
-    }
-    if (out_rgb) {
-        out_rgb[3 * p] = C[0];
-        out_rgb[3 * p + 1] = C[1];
-        out_rgb[3 * p + 2] = C[2];
-    }
-    if (out_depth) out_depth[p] = D;
-    if (out_opa) out_opa[p] = 1.0f - T;
-}
-
-void launch_scene_composite(const LaunchCtx& lc, int n_obj, long long HW, const float* seg, float* rgb, float* depth,
-                            float* opa) {
-    if (HW > 0) k_scene_composite<<<(unsigned)((HW + 255) / 256), 256, 0, lc.st>>>(n_obj, HW, seg, rgb, depth, opa);
-}
 

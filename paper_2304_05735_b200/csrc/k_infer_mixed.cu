@@ -183,7 +183,9 @@ void launch_query_density_mixed(const LaunchCtx& lc, const CfgDev& cfg, const Ob
 // ---------------------------------------------------------------------------
 // a11 render, mixed path: the forward half of the training step on the tensor
 // cores for midpoint samples (R12), one sample per thread, tiles of 128 samples
-// (whole rays of the object).  Writes sigma, rgb, dist, delta per sample in the
+// (whole rays of one object: a ray's `slot` indexes `objs`; render_scene lays the
+// segments of every object out contiguously, padded to whole tiles, and a CTA
+// reloads the fp16 weights when its next tile belongs to another object).  Writes sigma, rgb, dist, delta per sample in the
 // layout k_composite consumes (inactive rays: sigma = 0, rgb = 0), so the
 // compositing (front to back over black, R20) is shared with the fp32 path.
 namespace {
@@ -222,27 +224,9 @@ __device__ __forceinline__ void f_sync_for_mma() {
 }
 }  // namespace
 
-template <int L>
-__global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __restrict__ obj,
-                                                  const RayRec* __restrict__ rays, int n_rays,
-                                                  float* __restrict__ sigma_o, float* __restrict__ rgb_o,
-                                                  float* __restrict__ dist_o, float* __restrict__ delta_o) {
-    constexpr int LF = 2 * L;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    FMisc* misc = reinterpret_cast<FMisc*>(smem + F_OFF_MISC);
-    const int t = threadIdx.x, warp = t >> 5;
-    const ObjDev& ob = *obj;
-    const int N = cfg.N;
-    if (warp == 0) tc::tmem_alloc(&misc->tmem, 64);
-    if (t == 32) {
-        tc::mbar_init(&misc->mbar, 1);
-        tc::fence_mbar_init();
-    }
-    if (t < L) {
-        misc->lv[t] = level_params(cfg, t);
-        misc->lvoff[t] = cfg.off[t];
-    }
-    {   // fp16 weights -> interleaved operand layout (W5: rows 3..15 zero)
+// fp16 weights of one object -> interleaved operand layout (W5: rows 3..15 zero)
+__device__ __forceinline__ void f_load_weights(uint8_t* smem, const CfgDev& cfg, const ObjDev& ob, int LF, int t) {
+    {
         const __half* mlp16 = ob.p16 + cfg.n_table;
         struct Lw { int off, rows, cols, srows, smem; };
         Lw ls[5] = {{cfg.w_off[0], 64, LF, 64, F_OFF_W1}, {cfg.w_off[1], 16, 64, 16, F_OFF_W2},
@@ -272,6 +256,27 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
             }
         }
     }
+}
+
+template <int L>
+__global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __restrict__ objs,
+                                                  const RayRec* __restrict__ rays, int n_rays,
+                                                  float* __restrict__ sigma_o, float* __restrict__ rgb_o,
+                                                  float* __restrict__ dist_o, float* __restrict__ delta_o) {
+    constexpr int LF = 2 * L;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    FMisc* misc = reinterpret_cast<FMisc*>(smem + F_OFF_MISC);
+    const int t = threadIdx.x, warp = t >> 5;
+    const int N = cfg.N;
+    if (warp == 0) tc::tmem_alloc(&misc->tmem, 64);
+    if (t == 32) {
+        tc::mbar_init(&misc->mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (t < L) {
+        misc->lv[t] = level_params(cfg, t);
+        misc->lvoff[t] = cfg.off[t];
+    }
     f_sync_for_mma();
     const uint32_t tm = misc->tmem;
     const uint32_t wk = tc::taddr(tm, warp * 32, 0);
@@ -286,8 +291,8 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
     uint8_t* CIN = smem + F_OFF_CIN;
     uint8_t* G1 = smem + F_OFF_G1;
     uint8_t* G2 = smem + F_OFF_G2;
-    const uint32_t* tab = reinterpret_cast<const uint32_t*>(ob.p16);
     const unsigned hmask = (unsigned)cfg.T - 1u;
+    int cur = -1;
     uint32_t phase = 0;
     auto mma_wait = [&]() {
         tc::mbar_wait(&misc->mbar, phase);
@@ -300,6 +305,14 @@ __global__ void __launch_bounds__(QT) k_fwd_mixed(CfgDev cfg, const ObjDev* __re
         const bool valid = s < S;
         const long long ray = valid ? s / N : 0;
         const int i = valid ? (int)(s - ray * N) : 0;
+        const int slot = rays[tile * QT / N].slot;        // uniform: a tile holds rays of one object
+        if (slot != cur) {
+            f_load_weights(smem, cfg, objs[slot], LF, t);
+            f_sync_for_mma();
+            cur = slot;
+        }
+        const ObjDev& ob = objs[slot];
+        const uint32_t* tab = reinterpret_cast<const uint32_t*>(ob.p16);
         const RayRec rr = rays[ray];
         const bool active = valid && (rr.flags & RF_ACTIVE);
         // R12 inference samples: midpoints, delta = Delta (bit-exact with k_fwd_fp32)

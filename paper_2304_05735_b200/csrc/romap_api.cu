@@ -183,8 +183,12 @@ struct romap_ctx {
     size_t rays_c_cap = 0;
     int* ray_idx = nullptr;      // render: pixel of each packed ray (+ the packed count)
     size_t ray_idx_cap = 0;
-    float* scene_d = nullptr;    // render_scene: per object C (rgb), A, D, t_near, HW floats each
+    float* scene_d = nullptr;    // render_scene: per segment t_near, id, C (rgb), A, D + pixel segment lists
     size_t scene_cap = 0;
+    int* scene_i = nullptr;      // render_scene: per pixel counts / offsets, per object counts / ranges, scan scratch
+    size_t scene_i_cap = 0;
+    ObjDev* scene_objs_d = nullptr;   // render_scene: descriptors of the scene's objects
+    size_t scene_objs_cap = 0;
     float* mesh_d = nullptr;     // extract_mesh: lattice points | sigma | counts | offsets | CUB scratch
     size_t mesh_cap = 0;
     float* tris_d = nullptr;     // extract_mesh: triangles (device staging for host outputs)
@@ -536,6 +540,8 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->samp);
     dfree(ctx, ctx->srec);
     dfree(ctx, ctx->scene_d);
+    dfree(ctx, ctx->scene_i);
+    dfree(ctx, ctx->scene_objs_d);
     dfree(ctx, ctx->rays_c);
     dfree(ctx, ctx->ray_idx);
     dfree(ctx, ctx->mesh_d);
@@ -1508,6 +1514,7 @@ romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, 
                                 float* opacity, int32_t flags) {
     CHECK_CTX();
     if (!objs || n < 1) return fail(ROMAP_E_INVALID, "empty object list");
+    if (n > 8192) return fail(ROMAP_E_INVALID, "render_scene takes at most 8192 objects");
     if (!T_wc || !K || K->width < 1 || K->height < 1 || !(K->fx > 0) || !(K->fy > 0))
         return fail(ROMAP_E_INVALID, "bad pose / intrinsics");
     const int N = samples_per_segment;
@@ -1520,24 +1527,122 @@ romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, 
             if (objs[j] == objs[i]) return fail(ROMAP_E_INVALID, "object %d listed twice", objs[i]);
         obs.push_back(ob);
     }
-    // R20 tie-break: equal t_near -> smaller object id first; slices in id order
+    // scene order: objects grouped by model configuration (one forward launch per
+    // group), ascending id within a group; the composite orders segments by
+    // (t_near, object id) whatever the scene order (R20)
     std::sort(obs.begin(), obs.end(), [](const Object* a, const Object* b) { return a->id < b->id; });
-    const long long HW = (long long)K->width * K->height;
-    if (!grow(ctx, ctx->scene_d, ctx->scene_cap, (size_t)6 * HW * obs.size()))
-        return fail(ROMAP_E_OOM, "scene segment buffer");
-    LaunchCtx lc{ctx->st, ctx->num_sms};
-    for (size_t o = 0; o < obs.size(); ++o) {
-        float* sl = ctx->scene_d + 6 * HW * o;   // C (3 HW, interleaved rgb), A, D, t_near
-        romap_status st = render_one(ctx, obs[o], T_wc, K, N, sl, sl + 4 * HW, sl + 3 * HW, ROMAP_DEVICE_PTRS);
-        if (st) return st;
-        launch_seg_tnear(lc, ctx->rays, HW, sl + 5 * HW);
+    std::vector<std::vector<Object*>> groups;
+    for (Object* ob : obs) {
+        bool placed = false;
+        for (auto& g : groups)
+            if (same_model(g[0]->cfg, ob->cfg)) { g.push_back(ob); placed = true; break; }
+        if (!placed) groups.push_back({ob});
     }
-    if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)HW * 5)) return fail(ROMAP_E_OOM, "output buffer");
+    obs.clear();
+    for (auto& g : groups) obs.insert(obs.end(), g.begin(), g.end());
+    const int W = K->width, H = K->height;
+    const long long HW = (long long)W * H;
+    LaunchCtx lc{ctx->st, ctx->num_sms};
+    // device descriptors of the scene's objects and the camera
+    std::vector<ObjDev> od(n);
+    for (int i = 0; i < n; ++i) od[i] = make_objdev(obs[i]);
+    if (!grow(ctx, ctx->scene_objs_d, ctx->scene_objs_cap, (size_t)n)) return fail(ROMAP_E_OOM, "scene descriptors");
+    KfDev cam;
+    memset(&cam, 0, sizeof cam);
+    for (int k = 0; k < 12; ++k) cam.T[k] = T_wc[k];
+    cam.fx = K->fx; cam.fy = K->fy; cam.cx = K->cx; cam.cy = K->cy;
+    cam.w = W; cam.h = H;
+    CK(cudaMemcpyAsync(ctx->scene_objs_d, od.data(), n * sizeof(ObjDev), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->cam_d, &cam, sizeof cam, cudaMemcpyHostToDevice, ctx->st));
+    // integers: pix_cnt, pix_off (HW each), obj_cnt, obj_fill, obj_off, obj_len (n each), scan scratch
+    const size_t scan_bytes = scene_scan_bytes(HW);
+    const size_t ints = 2 * (size_t)HW + 4 * (size_t)n + scan_bytes / 4 + 64;
+    if (!grow(ctx, ctx->scene_i, ctx->scene_i_cap, ints)) return fail(ROMAP_E_OOM, "scene index buffers");
+    int* pix_cnt = ctx->scene_i;
+    int* pix_off = pix_cnt + HW;
+    int* obj_cnt = pix_off + HW;
+    int* obj_fill = obj_cnt + n;
+    int* obj_off = obj_fill + n;
+    int* obj_len = obj_off + n;
+    void* scan_tmp = reinterpret_cast<void*>(((uintptr_t)(obj_len + n) + 255) & ~(uintptr_t)255);
+    CK(cudaMemsetAsync(obj_cnt, 0, 2 * n * sizeof(int), ctx->st));          // obj_cnt, obj_fill
+    launch_scene_count(lc, ctx->cam_d, ctx->scene_objs_d, n, W, H, pix_cnt, obj_cnt);
+    launch_scene_scan(lc, pix_cnt, pix_off, HW, scan_tmp, scan_bytes);
+    std::vector<int> cnt(n);
+    CK(cudaMemcpyAsync(cnt.data(), obj_cnt, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));                                       // the one host read per frame
+    // object ranges: whole 128-sample tiles (a tile never holds two objects)
+    int g = 128;
+    for (int a = N, b = 128; b;) { int r = a % b; a = b; b = r; g = a; }
+    const int spt = 128 / g;                                                  // segments per tile boundary
+    std::vector<int> off(n), len(n);
+    long long total = 0, hits = 0;
+    for (int i = 0; i < n; ++i) {
+        off[i] = (int)total;
+        len[i] = (cnt[i] + spt - 1) / spt * spt;
+        total += len[i];
+        hits += cnt[i];
+    }
+    if (total >= (1LL << 31)) return fail(ROMAP_E_INVALID, "too many scene segments");
+    CK(cudaMemcpyAsync(obj_off, off.data(), n * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(obj_len, len.data(), n * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
     const bool dev = flags & ROMAP_DEVICE_PTRS;
-    float* o_rgb = dev ? rgb : (rgb ? ctx->io_d : nullptr);
-    float* o_dep = dev ? depth : (depth ? ctx->io_d + 3 * HW : nullptr);
-    float* o_opa = dev ? opacity : (opacity ? ctx->io_d + 4 * HW : nullptr);
-    launch_scene_composite(lc, (int)obs.size(), HW, ctx->scene_d, o_rgb, o_dep, o_opa);
+    float* o_rgb = rgb;
+    float* o_dep = depth;
+    float* o_opa = opacity;
+    if (!dev) {
+        if (!grow(ctx, ctx->io_d, ctx->io_cap, (size_t)HW * 5)) return fail(ROMAP_E_OOM, "output buffer");
+        o_rgb = rgb ? ctx->io_d : nullptr;
+        o_dep = depth ? ctx->io_d + 3 * HW : nullptr;
+        o_opa = opacity ? ctx->io_d + 4 * HW : nullptr;
+    }
+    if (total > 0) {
+        // segment records + per segment t_near, id, C (3), A, D + the pixels' segment lists
+        if (!grow(ctx, ctx->rays_c, ctx->rays_c_cap, (size_t)total)) return fail(ROMAP_E_OOM, "segment records");
+        if (!grow(ctx, ctx->scene_d, ctx->scene_cap, (size_t)total * 7 + (size_t)hits + 64))
+            return fail(ROMAP_E_OOM, "segment buffers");
+        float* seg_tn = ctx->scene_d;
+        int* seg_id = reinterpret_cast<int*>(seg_tn + total);
+        float* segC = seg_tn + 2 * total;
+        float* segA = segC + 3 * total;
+        float* segD = segA + total;
+        int* pix_list = reinterpret_cast<int*>(segD + total);
+        launch_scene_emit(lc, ctx->cam_d, ctx->scene_objs_d, n, W, H, pix_off, obj_off, obj_fill, ctx->rays_c, seg_tn,
+                          seg_id, pix_list);
+        launch_scene_pad(lc, n, obj_cnt, obj_off, obj_len, ctx->rays_c);
+        // per model group: the forward over its objects' ranges in chunks of segments
+        // (chunk starts are multiples of spt, so every tile stays within one object)
+        const long long chunk = ((1 << 18) / spt) * spt;
+        const long long S = chunk * N;
+        if (!grow(ctx, ctx->samp, ctx->samp_cap, (size_t)S * 6)) return fail(ROMAP_E_OOM, "sample buffer");
+        float* sg = ctx->samp;
+        float* cl = sg + S;
+        float* ds = cl + 3 * S;
+        float* dl = ds + S;
+        int first = 0;
+        for (auto& grp : groups) {
+            const int last = first + (int)grp.size();
+            CfgDev cfg = grp[0]->cdev;
+            cfg.N = N;
+            const long long g0 = off[first], g1 = off[last - 1] + len[last - 1];
+            for (long long r0 = g0; r0 < g1; r0 += chunk) {
+                const int nr = (int)std::min<long long>(chunk, g1 - r0);
+                if (grp[0]->cfg.precision == 1)
+                    launch_fwd_mixed(lc, cfg, ctx->scene_objs_d, ctx->rays_c + r0, nr, sg, cl, ds, dl);
+                else
+                    launch_fwd_fp32(lc, cfg, ctx->scene_objs_d, ctx->rays_c + r0, nr, false, true, sg, cl, ds, dl,
+                                    nullptr, 0);
+                launch_composite(lc, N, ctx->rays_c + r0, nr, sg, cl, ds, dl, segC + 3 * r0, segD + r0, segA + r0,
+                                 nullptr);
+            }
+            first = last;
+        }
+        launch_scene_final(lc, HW, pix_cnt, pix_off, pix_list, seg_tn, seg_id, segC, segA, segD, o_rgb, o_dep, o_opa);
+    } else {
+        if (o_rgb) CK(cudaMemsetAsync(o_rgb, 0, HW * 3 * 4, ctx->st));
+        if (o_dep) CK(cudaMemsetAsync(o_dep, 0, HW * 4, ctx->st));
+        if (o_opa) CK(cudaMemsetAsync(o_opa, 0, HW * 4, ctx->st));
+    }
     CK(cudaGetLastError());
     if (!dev) {
         if (rgb) CK(cudaMemcpyAsync(rgb, o_rgb, HW * 3 * 4, cudaMemcpyDeviceToHost, ctx->st));

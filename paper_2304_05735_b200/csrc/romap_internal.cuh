@@ -370,9 +370,20 @@ void launch_composite(const LaunchCtx& lc, int N, const RayRec* rays, int n_rays
                       const float* rgb, const float* dist, const float* delta, float* out_rgb, float* out_depth,
                       float* out_opacity, const int* out_idx = nullptr);
 void launch_compact_rays(const LaunchCtx& lc, const RayRec* rays, int n, RayRec* out, int* idx, int* count);
-void launch_seg_tnear(const LaunchCtx& lc, const RayRec* rays, long long n, float* tn);
-void launch_scene_composite(const LaunchCtx& lc, int n_obj, long long HW, const float* seg, float* rgb, float* depth,
-                            float* opa);
+// k_scene.cu: render_scene batched over objects (R20)
+void launch_scene_count(const LaunchCtx& lc, const KfDev* cam, const ObjDev* objs, int n_obj, int W, int H,
+                        int* pix_cnt, int* obj_cnt);
+size_t scene_scan_bytes(long long HW);
+void launch_scene_scan(const LaunchCtx& lc, const int* pix_cnt, int* pix_off, long long HW, void* temp,
+                       size_t temp_bytes);
+void launch_scene_emit(const LaunchCtx& lc, const KfDev* cam, const ObjDev* objs, int n_obj, int W, int H,
+                       const int* pix_off, const int* obj_off, int* obj_fill, RayRec* segs, float* seg_tn, int* seg_id,
+                       int* pix_list);
+void launch_scene_pad(const LaunchCtx& lc, int n_obj, const int* obj_cnt, const int* obj_off, const int* obj_len,
+                      RayRec* segs);
+void launch_scene_final(const LaunchCtx& lc, long long HW, const int* pix_cnt, const int* pix_off, const int* pix_list,
+                        const float* seg_tn, const int* seg_id, const float* segC, const float* segA, const float* segD,
+                        float* rgb, float* depth, float* opa);
 void launch_query_density(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* obj, const float* xyz, long long n,
                           float* sigma);
 void launch_debug_samples(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
