@@ -52,7 +52,12 @@ def test_trained_sphere_reconstruction():
     c.close()
 
 
-def test_carved_mesh_matches_oracle_and_improves_accuracy():
+def test_carved_mesh_matches_oracle_and_keeps_the_observed_surface():
+    """ROMAP_MESH_CARVE equals the oracle's carve on the same lattice; on a trained
+    sphere it removes no observed surface (completion, completion ratio) and adds no
+    triangles.  No accuracy gain is claimed: on these 8 views nearly every lattice
+    vertex is seen by some keyframe, so the floaters that remain are in observed
+    space."""
     c = R.Context(0)
     sc = scenes.sphere_scene(0, n_views=8)
     h, st = make_pair(R, c, sc, CFG0M, avoid_kinks=False)
@@ -66,8 +71,9 @@ def test_carved_mesh_matches_oracle_and_improves_accuracy():
     To = O.to_world(O.marching_tetrahedra(np.where(seen, sig, 0.0), P, iso), st.box_t, st.box_yaw)
     assert T.shape == To.shape and np.abs(T - To).max() < 1e-5
     c.close()
-    # trained sphere: carving removes the untrained box regions -> accuracy
+    # trained sphere (deterministic reductions: the same mesh every run)
     c = R.Context(0)
+    c.set_deterministic(True)
     ob = sc.objects[0]
     h = c.create_object(ob.t, ob.yaw, ob.a, R.model_config(**dict(CFG0M, rays_per_iter=1024)), ob.instance_id)
     for fr in sc.frames:
@@ -78,12 +84,12 @@ def test_carved_mesh_matches_oracle_and_improves_accuracy():
     T0, T1 = c.extract_mesh(h, 64, 20.0), c.extract_mesh(h, 64, 20.0, carve=True)
     m0 = O.mesh_metrics(O.sample_mesh_points(T0, 8000), gt, tau=0.08)
     m1 = O.mesh_metrics(O.sample_mesh_points(T1, 8000), gt, tau=0.08)
-    # carving only zeroes sigma in space no keyframe sees (R26): it never adds
-    # surface there and keeps the observed surface (completeness).  Whether the
-    # unseen box regions grew floaters (which carving removes) depends on the
-    # training run (fp32 atomics sum in a different order every run), so accuracy
-    # is only required not to degrade beyond point-sampling noise (8000 points)
+    # carving only zeroes sigma in space no keyframe sees (R26): it adds no surface
+    # (cells straddling the seen / unseen boundary may re-triangulate, at most a few)
+    # and keeps the observed surface; accuracy may move by boundary cells and the
+    # 8000-point sampling of the two meshes, nothing more
     assert len(T1) <= len(T0) + len(T0) // 50
-    assert m1["acc"] <= m0["acc"] + 1e-2 and m1["comp"] < 0.04 and m1["cr"] > 0.9, (m0, m1)
+    assert m1["comp"] < 0.04 and m1["cr"] > 0.9, (m0, m1)
+    assert m1["acc"] <= m0["acc"] + 1e-2, (m0, m1)
     print("uncarved", m0, "carved", m1)
     c.close()
