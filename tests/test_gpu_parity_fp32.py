@@ -264,3 +264,34 @@ def test_error_paths(ctx, scene0):
     assert ctx.object_info(h1)["step"] == 2
     ctx.destroy_object(h1)
     ctx.destroy_object(h2)
+
+
+def test_fp32_deterministic_batch_equals_alone_and_oracle():
+    """fp32 path in the deterministic-reduction mode (romap_set_deterministic): the
+    gradients of two room objects computed in one batch equal each object's alone
+    bit for bit, a rerun is bitwise identical, and the result keeps
+    the fp32 tolerance against the oracle (1e-4 norm-relative per block)"""
+    c = R.Context(0)
+    c.set_deterministic(True)
+    sc = scenes.room_scene(4, n_objects=3, n_frames=6, W=160, H=120, f=131.25, room_half=1.5)
+    kw = dict(CFG0, rays_per_iter=128, seed=4)
+    hs, sts = [], []
+    for k, ob in enumerate(sc.objects[:2]):
+        h, st = make_pair(R, c, sc, kw, param_seed=10 + k, inst=ob.instance_id, obj_id=100 + k)
+        hs.append(h)
+        sts.append(st)
+    grads = lambda h: (c.get_params(h, R.BLOCK_GRAD_TABLE), c.get_params(h, R.BLOCK_GRAD_MLP))
+    sb = c.forward_backward(hs)
+    gb = [grads(h) for h in hs]
+    for k in range(2):
+        L, g, _ = O.loss_and_grads(sts[k], 1)
+        assert abs(sb[k]["l_total"] - L["l_total"]) <= 1e-5 * L["l_total"]
+        assert norm_rel(gb[k][0].reshape(-1, 2), g["table"]) < 1e-4
+        assert norm_rel(gb[k][1], flat_W(g["W"])) < 1e-4
+    for k in range(2):
+        sa = c.forward_backward([hs[k]])[0]
+        ga = grads(hs[k])
+        assert sa["l_total"] == sb[k]["l_total"] and sa["l_rgb"] == sb[k]["l_rgb"]
+        assert np.array_equal(ga[0].view(np.uint32), gb[k][0].view(np.uint32))
+        assert np.array_equal(ga[1].view(np.uint32), gb[k][1].view(np.uint32))
+    c.close()
