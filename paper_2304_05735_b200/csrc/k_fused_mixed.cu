@@ -616,6 +616,11 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                         const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
                         issue = as_ && ((lane - run0) & wmask) == 0;
                     }
+#if defined(ROMAP_EXP_NORED_COARSE)                 // experiment: no REDs on the merged (coarse) levels
+                    if (P[q].x < MERGE_RES) { asm volatile("" :: "f"(v[0]), "f"(v[15])); issue = false; }
+#elif defined(ROMAP_EXP_NORED_FINE)                 // experiment: no REDs on the other levels
+                    if (P[q].x >= MERGE_RES) { asm volatile("" :: "f"(v[0]), "f"(v[15])); issue = false; }
+#endif
                     if (issue) {
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
