@@ -248,7 +248,11 @@ def algorithmic_per_sample(kw, precision):
     mlp_bwd = 2 * mlp_fwd
     gather = L * 8 * F * (2 if precision == 1 else 4)          # table reads
     scatter = L * 8 * F * 4                                      # fp32 gradient atomics
-    return {"mlp_fwd_flop": mlp_fwd, "mlp_bwd_flop": mlp_bwd, "gather_bytes": gather, "scatter_bytes": scatter}
+    # the fused kernel's own inputs: the sample record (u, d_i) + delta written by
+    # k_samples (20 B) and the ray record (84 B) shared by the ray's N samples
+    inputs = 20 + 84.0 / kw["samples_per_ray"]
+    return {"mlp_fwd_flop": mlp_fwd, "mlp_bwd_flop": mlp_bwd, "gather_bytes": gather, "scatter_bytes": scatter,
+            "input_bytes": inputs}
 
 
 def load_measured_peaks():
@@ -303,8 +307,9 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
     ms = st["ms"] / st["launches"]
     sm_clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
     if dom in ("fused_mixed",):
-        # algorithmic bytes of the hash gathers + gradient atomics
-        bytes_ = samples_per_launch * (work["gather_bytes"] + work["scatter_bytes"])
+        # algorithmic bytes of the hash gathers + gradient atomics + the per-sample
+        # inputs the kernel reads
+        bytes_ = samples_per_launch * (work["gather_bytes"] + work["scatter_bytes"] + work["input_bytes"])
         achieved = bytes_ / (ms * 1e-3) / 1e9
         out = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
         rq = request_roofline(kw, samples_per_launch, ms, sm_clk, 148)
@@ -326,7 +331,8 @@ def roofline(prof, kw, precision, samples_per_launch, n_objs):
     out["frac"] = out["achieved"] / out["peak"]
     out["kernel"] = dom
     out["ms_per_launch"] = ms
-    out["algorithmic_bytes_per_hit_sample"] = work["gather_bytes"] + work["scatter_bytes"]
+    out["algorithmic_bytes_per_hit_sample"] = work["gather_bytes"] + work["scatter_bytes"] + (
+        work["input_bytes"] if dom == "fused_mixed" else 0)
     out["hit_samples_per_launch"] = samples_per_launch
     out["peak_source"] = src
     out["traffic"] = ncu_traffic(dom)
