@@ -399,7 +399,18 @@ def measure_inference(ctx, hs, obs, poses, torch):
     for T, K in poses:
         rgb, dep, opa = ctx.render_scene(hs, T, K, 640, 480, 128)
     rs_s = (time.perf_counter() - t0) / len(poses)
-    return {"query_density": {"objects": len(hs), "points": int(npts), "points_per_s": npts / (q_ms * 1e-3),
+    # f2 mesh extraction at the paper's 64^3 (2.84 ms per object incl.
+    # marching cubes): lattice + density + marching tetrahedra + triangles to the host
+    nm = min(len(hs), 8)
+    ctx.extract_mesh(hs[0], 64, 20.0)
+    t0 = time.perf_counter()
+    tris = [ctx.extract_mesh(h, 64, 20.0) for h in hs[:nm]]
+    mesh_s = (time.perf_counter() - t0) / nm
+    return {"mesh": {"objects": nm, "lattice": "65^3 vertices (64^3 cells)", "ms_per_object": mesh_s * 1e3,
+                     "triangles_per_object": float(sum(len(t) for t in tris)) / nm, "paper_ms_per_object": 2.84,
+                     "what": "romap_extract_mesh (k_lattice, density query, marching tetrahedra count / scan / emit), "
+                             "world-frame triangles copied to the host, wall clock"},
+            "query_density": {"objects": len(hs), "points": int(npts), "points_per_s": npts / (q_ms * 1e-3),
                               "ms_per_object_lattice": q_ms / len(hs),
                               "what": "128^3 vertex lattice per object box, device buffers, CUDA events (mixed path: "
                                       "fp16 tables + tcgen05 first layer)",
@@ -588,6 +599,8 @@ def run_ours(args):
     workload = resolve_workload(args, ws)
     if workload == "cfg2":
         return run_cfg2(args, ctx, R, torch, precision)
+    if workload == "online":
+        return run_online(args, ctx, R, torch, precision)
     if workload == "paper":
         precision = 1
     items, kw, _ = objects_for_rank(workload, args, ws, rank, precision)
@@ -798,6 +811,60 @@ def run_cfg2(args, ctx, R, torch, precision):
     return 0
 
 
+def run_online(args, ctx, R, torch, precision):
+    """SURVEY f3 measured: the paper's online schedule on the cfg2 room.  The frames of
+    the 200-frame trajectory arrive at --online-hz (the paper's SLAM rate, 25 Hz,
+    PAPER.md:7,305); every object visible in a frame is offered to the asynchronous
+    trainer (romap_async_offer: Eq. 5 gate at 25 deg, +300 iterations per accepted
+    keyframe); after the last frame the worker finishes every
+    pending budget.  Reports the producer's offer latency (it must never block), the
+    keyframes accepted, and the iterations and drawn ray-samples per second of the
+    trainer over the whole run."""
+    import numpy as np
+    sc, plan = cfg2_plan()
+    kw = cfg1_kwargs(precision)
+    hs = {}
+    for k, p in enumerate(plan):
+        ob = p["ob"]
+        hs[ob.instance_id] = (ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**dict(kw, rays_per_iter=p["rays"])),
+                                                ob.instance_id, obj_id=k), p["rays"])
+    period = 1.0 / args.online_hz if args.online_hz > 0 else 0.0
+    ctx.async_start(chunk=50, alpha_deg=25.0, iters_per_update=300, queue_cap=256)
+    lat = []
+    t_start = time.perf_counter()
+    for i, fr in enumerate(sc.frames):
+        ids = [iid for iid in np.unique(fr.mask) if iid in hs]
+        for iid in ids:
+            t0 = time.perf_counter()
+            ctx.async_offer(hs[iid][0], fr.rgb, fr.mask, fr.T_wc, fr.K)
+            lat.append(time.perf_counter() - t0)
+        if period:
+            time.sleep(max(0.0, t_start + (i + 1) * period - time.perf_counter()))
+    t_frames = time.perf_counter() - t_start
+    st = ctx.async_stop(finish_pending=True)
+    torch.cuda.synchronize()
+    t_all = time.perf_counter() - t_start
+    steps = {iid: int(ctx.get_params(h, R.BLOCK_STEP)[0]) for iid, (h, _) in hs.items()}
+    drawn = sum(steps[iid] * rays * kw["samples_per_ray"] for iid, (_, rays) in hs.items())
+    lat_ms = sorted(x * 1e3 for x in lat)
+    print(json.dumps({
+        "metric": "NeRF train ray-samples/s (online schedule)", "value": drawn / t_all, "unit": "drawn ray-samples/s",
+        "n_gpus": 1, "higher_is_better": True, "dtype": "f16-mma/f32" if precision == 1 else "f32",
+        "data": "synthetic room (seed 2): 8 cfg1-family objects, 200-frame 640x480 trajectory",
+        "config": {"workload": f"online (SURVEY f3): frames at {args.online_hz} Hz, Eq. 5 gate 25 deg, 300 iterations "
+                               "per accepted keyframe, async trainer (chunks of 50), rays split by mask area",
+                   "rays": [r for _, r in hs.values()]},
+        "producer": {"offers": len(lat), "offer_ms_median": lat_ms[len(lat_ms) // 2], "offer_ms_max": lat_ms[-1],
+                     "frames_s": t_frames, "note": "a queue push; the producer never waits on the GPU"},
+        "trainer": {"accepted_keyframes": st["accepted"], "rejected": st["rejected"], "dropped": st["dropped"],
+                    "iterations_per_object": steps, "wall_s": t_all,
+                    "s_after_last_frame": t_all - t_frames,
+                    "note": "value = drawn ray-samples (steps x rays x N, misses included) / wall time of the run"}}),
+          flush=True)
+    ctx.close()
+    return 0
+
+
 def run_table4(args):
     """The paper's Table 4 grid on one GPU: ms per training iteration
     of one object (4096 rays x 32, a1..a8 incl. Adam, L2 flushed before each iteration)
@@ -846,7 +913,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["auto", "cfg1", "cfg2", "cfg3", "cfg4"], default="auto",
+    ap.add_argument("--online-hz", type=float, default=25.0, help="--workload online: frame rate of the producer")
+    ap.add_argument("--workload", choices=["auto", "cfg1", "cfg2", "cfg3", "cfg4", "online"], default="auto",
                     help="auto: cfg1 at N=1 (BASELINE metric config), cfg3 (64 objects sharded) at N>1")
     ap.add_argument("--precision", choices=["auto", "mixed", "fp32"], default="auto")
     ap.add_argument("--objects-per-gpu", type=int, default=1, help="cfg1: objects per rank (weak scaling)")
