@@ -239,6 +239,9 @@ class Context:
             self._h = C.c_void_p()
 
     def __del__(self):
+        import sys
+        if sys.is_finalizing():       # torch's allocator (the free callbacks) may be gone already
+            return
         try:
             self.close()
         except Exception:
