@@ -101,9 +101,6 @@ def spawn_ranks(args):
     """--gpus N without a launcher: run this script under torch.distributed.run with
     N ranks on this node (rendezvous on 127.0.0.1), pass rank 0's JSON line through"""
     env = dict(os.environ)
-    if not args.dry_run:
-        env.setdefault("NCCL_DEBUG", "INFO")            # the rank / device map of the communicator
-        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd, env=env)
@@ -589,6 +586,10 @@ def run_ours(args):
         if share:
             dist.init_process_group("gloo")
         else:
+            # the communicator's rank / device map in the log (stderr: stdout carries the JSON line)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
     from paper_2304_05735_b200 import romap as R
