@@ -443,7 +443,7 @@ def oracle_run(ob, frames, kw, rays, iters, obj_id=0):
     return samples, dt
 
 
-def cpu_baseline(ob, frames, kw, rays=1024, iters=3):
+def cpu_baseline(ob, frames, kw, rays=1024, iters=8):
     samples, dt = oracle_run(ob, frames, kw, rays, iters)
     return dict({"value": samples / dt, "unit": "ray-samples/s", "cores": 1, "kind": "oracle",
                  "sample": f"{iters} oracle iterations of one object of this workload at {rays} rays x "
