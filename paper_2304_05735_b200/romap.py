@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 import numpy as np
 
@@ -239,8 +240,10 @@ class Context:
             self._h = C.c_void_p()
 
     def __del__(self):
-        import sys
-        if sys.is_finalizing():       # torch's allocator (the free callbacks) may be gone already
+        try:
+            if sys.is_finalizing():   # torch's allocator (the free callbacks) may be gone already
+                return
+        except Exception:
             return
         try:
             self.close()

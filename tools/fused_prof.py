@@ -16,7 +16,8 @@ fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 ctx = R.Context(0)
 paper = "--paper" in sys.argv                  # the paper's workload (network 1, 4096 x 32)
 kw = bench.paper_kwargs() if paper else bench.cfg1_kwargs(1)
-sc = bench.load_scene()
+import scenes  # noqa: E402
+sc = scenes.object_scene(1, n_views=20)
 ob = sc.objects[0]
 h = ctx.create_object(ob.t, ob.yaw, ob.a, R.model_config(**kw), ob.instance_id)
 for fr in sc.frames:
