@@ -195,6 +195,12 @@ struct romap_ctx {
     size_t tris_cap = 0;
     float* io_d = nullptr;       // render / query staging
     size_t io_cap = 0;
+    // add_observation: pinned host staging of the in-box crop (+ depth) so its H2D
+    // copy is a true async DMA; reused once the previous copy from it completed
+    void* pin = nullptr;
+    size_t pin_cap = 0;
+    cudaEvent_t pin_ev = nullptr;
+    bool pin_pending = false;
     // last batch
     std::vector<ObjDev> last_objdev;
     CfgDev last_cfg{};
@@ -556,6 +562,8 @@ romap_status romap_ctx_destroy(romap_ctx* ctx) {
     dfree(ctx, ctx->io_d);
     dfree(ctx, ctx->flush_buf);
     dfree(ctx, ctx->det_mem);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
+    if (ctx->pin_ev) cudaEventDestroy(ctx->pin_ev);
     if (ctx->tg.exec) cudaGraphExecDestroy(ctx->tg.exec);
     prof_collect(ctx);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
@@ -693,6 +701,32 @@ romap_status romap_get_object_info(romap_ctx* ctx, int32_t obj, romap_object_inf
     return ROMAP_OK;
 }
 
+// pinned staging of at least `bytes` (waits for the previous copy out of it); null
+// if pinned memory is unavailable (the caller then stages in pageable memory)
+static void* pinned_staging(romap_ctx* ctx, size_t bytes) {
+    if (ctx->pin_pending) {
+        cudaEventSynchronize(ctx->pin_ev);
+        ctx->pin_pending = false;
+    }
+    if (bytes > ctx->pin_cap) {
+        if (ctx->pin) cudaFreeHost(ctx->pin);
+        ctx->pin = nullptr;
+        ctx->pin_cap = 0;
+        const size_t cap = bytes + bytes / 4 + 4096;
+        if (cudaMallocHost(&ctx->pin, cap) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->pin = nullptr;
+            return nullptr;
+        }
+        ctx->pin_cap = cap;
+    }
+    if (!ctx->pin_ev && cudaEventCreateWithFlags(&ctx->pin_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return ctx->pin;
+}
+
 static void* kf_alloc(romap_ctx* ctx, Object* ob, size_t bytes) {
     bytes = (bytes + 255) & ~(size_t)255;
     if (ob->kf_chunks.empty() || ob->kf_used + bytes > ob->kf_cap) {
@@ -751,11 +785,20 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     const auto t1 = std::chrono::steady_clock::now();
     const int w = x1 - x0 + 1, h = y1 - y0 + 1;
     if (ob->total_area + (long long)w * h >= (1LL << 31)) return fail(ROMAP_E_INVALID, "too many keyframe pixels");
-    std::vector<uchar4> crop((size_t)w * h);
+    // crop (+ depth crop) written straight into pinned staging memory
+    const size_t npx = (size_t)w * h, crop_bytes = npx * sizeof(uchar4);
+    const size_t dep_off = (crop_bytes + 255) & ~(size_t)255;
+    std::vector<uint8_t> fallback;
+    uint8_t* stage = static_cast<uint8_t*>(pinned_staging(ctx, dep_off + (n_depth > 0 ? npx * 4 : 0)));
+    if (!stage) {
+        fallback.resize(dep_off + (n_depth > 0 ? npx * 4 : 0));
+        stage = fallback.data();
+    }
+    uchar4* crop = reinterpret_cast<uchar4*>(stage);
     for (int y = 0; y < h; ++y) {
         const uint16_t* mrow = mask + (size_t)(y0 + y) * W + x0;
         const uint8_t* crow = rgb + 3 * ((size_t)(y0 + y) * W + x0);
-        uchar4* out = crop.data() + (size_t)y * w;
+        uchar4* out = crop + (size_t)y * w;
         for (int x = 0; x < w; ++x) {
             const uint16_t mv = mrow[x];
             const unsigned char cls = mv == id ? CLS_OBJ : (mv == 0 ? CLS_BG : CLS_OCC);
@@ -763,10 +806,10 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
         }
     }
     const auto t2 = std::chrono::steady_clock::now();
-    std::vector<float> dep;
+    float* dep = n_depth > 0 ? reinterpret_cast<float*>(stage + dep_off) : nullptr;
     bool any_depth = false;
     if (n_depth > 0) {
-        dep.assign((size_t)w * h, 0.f);
+        memset(dep, 0, npx * 4);
         for (int i = 0; i < n_depth; ++i) {
             int px = (int)floorf(depth[i].u), py = (int)floorf(depth[i].v);
             if (px < x0 || px > x1 || py < y0 || py > y1 || !(depth[i].z > 0)) continue;
@@ -787,10 +830,10 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
     kf.dev.w = w;
     kf.dev.h = h;
     kf.area = (long long)w * h;
-    kf.crop_d = (uchar4*)kf_alloc(ctx, ob, crop.size() * sizeof(uchar4));
+    kf.crop_d = (uchar4*)kf_alloc(ctx, ob, crop_bytes);
     if (!kf.crop_d) return fail(ROMAP_E_OOM, "crop allocation failed");
     if (any_depth) {
-        kf.depth_d = (float*)kf_alloc(ctx, ob, dep.size() * 4);
+        kf.depth_d = (float*)kf_alloc(ctx, ob, npx * 4);
         if (!kf.depth_d) return fail(ROMAP_E_OOM, "depth allocation failed");
     }
     kf.dev.crop = kf.crop_d;
@@ -812,8 +855,14 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
         ob->kfs_cap = nc;
     }
     const auto t3 = std::chrono::steady_clock::now();
-    CK(cudaMemcpyAsync(kf.crop_d, crop.data(), crop.size() * sizeof(uchar4), cudaMemcpyHostToDevice, ctx->st));
-    if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep.data(), dep.size() * 4, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(kf.crop_d, crop, crop_bytes, cudaMemcpyHostToDevice, ctx->st));
+    if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep, npx * 4, cudaMemcpyHostToDevice, ctx->st));
+    if (stage == ctx->pin) {                       // the staging buffer is busy until these copies ran
+        CK(cudaEventRecord(ctx->pin_ev, ctx->st));
+        ctx->pin_pending = true;
+    } else {
+        CK(cudaStreamSynchronize(ctx->st));        // pageable fallback: the vector dies with this call
+    }
     ob->kfs.push_back(kf);
     ob->total_area += kf.area;
     // descriptor table and exclusive area prefix, uploaded whole (the arrays may have been reallocated)
