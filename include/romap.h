@@ -356,6 +356,20 @@ romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes);
 romap_status romap_selftest_mma(const float* X, const float* W, const float* Dl, float* out1, float* out2,
                                 float* out3);
 
+/* Checkpoint / resume of one object (SPEC.md "Model checkpoint
+ * file: header (config), then raw little-endian parameter arrays"): save_object
+ * writes the model configuration, box, instance and object id, Adam step,
+ * online-policy state (gate reference, pending budget), the fp32 parameters, Adam
+ * moments and gradients, and every keyframe (descriptor, in-box crop, optional
+ * depth crop) to `path` (host byte order; one file per object).  load_object
+ * recreates the object from such a file under obj_id (or the saved id when
+ * obj_id < 0), *out_obj = its id: continuing to train it is identical to
+ * continuing the saved one (bitwise in the deterministic mode).  E_INVALID: the
+ * file cannot be written / read, or is not a checkpoint of this version (nothing
+ * created); E_INVALID also if the id exists. */
+romap_status romap_save_object(romap_ctx* ctx, int32_t obj, const char* path);
+romap_status romap_load_object(romap_ctx* ctx, const char* path, int32_t obj_id, int32_t* out_obj);
+
 /* Deterministic-reduction mode (tests; SURVEY.md 8(c) "bitwise in a
  * deterministic-reduction debug mode").  on = 1: every
  * later train_step / forward_backward writes each table-gradient, weight-gradient

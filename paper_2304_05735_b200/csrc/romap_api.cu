@@ -742,6 +742,72 @@ static void* kf_alloc(romap_ctx* ctx, Object* ob, size_t bytes) {
     return p;
 }
 
+// append one keyframe to the object from its host-side in-box crop (rgb + class)
+// and optional depth crop: device arena copies, descriptor table, area prefix
+static romap_status append_keyframe(romap_ctx* ctx, Object* ob, const float T_wc[12], const romap_intrinsics* K,
+                                    int x0, int y0, int w, int h, const uchar4* crop, const float* dep,
+                                    bool staged_pinned) {
+    Keyframe kf;
+    for (int k = 0; k < 12; ++k) kf.dev.T[k] = T_wc[k];
+    kf.dev.fx = K->fx;
+    kf.dev.fy = K->fy;
+    kf.dev.cx = K->cx;
+    kf.dev.cy = K->cy;
+    kf.dev.x0 = x0;
+    kf.dev.y0 = y0;
+    kf.dev.w = w;
+    kf.dev.h = h;
+    kf.area = (long long)w * h;
+    const size_t npx = (size_t)w * h, crop_bytes = npx * sizeof(uchar4);
+    const bool any_depth = dep != nullptr;
+    kf.crop_d = (uchar4*)kf_alloc(ctx, ob, crop_bytes);
+    if (!kf.crop_d) return fail(ROMAP_E_OOM, "crop allocation failed");
+    if (any_depth) {
+        kf.depth_d = (float*)kf_alloc(ctx, ob, npx * 4);
+        if (!kf.depth_d) return fail(ROMAP_E_OOM, "depth allocation failed");
+    }
+    kf.dev.crop = kf.crop_d;
+    kf.dev.depth = kf.depth_d;
+    // descriptor / prefix arrays (re-uploaded whole; grown geometrically)
+    if (ob->kfs.size() + 1 > ob->kfs_cap) {
+        size_t nc = ob->kfs_cap ? ob->kfs_cap * 2 : 16;
+        KfDev* nk = (KfDev*)dalloc(ctx, nc * sizeof(KfDev));
+        long long* np = (long long*)dalloc(ctx, nc * sizeof(long long));
+        if (!nk || !np) {
+            dfree(ctx, nk); dfree(ctx, np);          // (arena space of the crop stays with the object)
+            return fail(ROMAP_E_OOM, "keyframe table allocation failed");
+        }
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(ctx, ob->kfs_d);
+        dfree(ctx, ob->prefix_d);
+        ob->kfs_d = nk;
+        ob->prefix_d = np;
+        ob->kfs_cap = nc;
+    }
+    CK(cudaMemcpyAsync(kf.crop_d, crop, crop_bytes, cudaMemcpyHostToDevice, ctx->st));
+    if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep, npx * 4, cudaMemcpyHostToDevice, ctx->st));
+    if (staged_pinned) {                           // the staging buffer is busy until these copies ran
+        CK(cudaEventRecord(ctx->pin_ev, ctx->st));
+        ctx->pin_pending = true;
+    } else {
+        CK(cudaStreamSynchronize(ctx->st));        // pageable source: it may die with the caller's call
+    }
+    ob->kfs.push_back(kf);
+    ob->total_area += kf.area;
+    // descriptor table and exclusive area prefix, uploaded whole (the arrays may have been reallocated)
+    std::vector<KfDev> descs(ob->kfs.size());
+    std::vector<long long> prefix(ob->kfs.size());
+    long long acc = 0;
+    for (size_t i = 0; i < ob->kfs.size(); ++i) {
+        descs[i] = ob->kfs[i].dev;
+        prefix[i] = acc;
+        acc += ob->kfs[i].area;
+    }
+    CK(cudaMemcpyAsync(ob->kfs_d, descs.data(), descs.size() * sizeof(KfDev), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ob->prefix_d, prefix.data(), prefix.size() * sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
+    return ROMAP_OK;
+}
+
 romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
                                    const float T_wc[12], const romap_intrinsics* K,
                                    const romap_depth_sample* depth, int32_t n_depth) {
@@ -819,63 +885,10 @@ romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* r
             any_depth = true;
         }
     }
-    Keyframe kf;
-    for (int k = 0; k < 12; ++k) kf.dev.T[k] = T_wc[k];
-    kf.dev.fx = K->fx;
-    kf.dev.fy = K->fy;
-    kf.dev.cx = K->cx;
-    kf.dev.cy = K->cy;
-    kf.dev.x0 = x0;
-    kf.dev.y0 = y0;
-    kf.dev.w = w;
-    kf.dev.h = h;
-    kf.area = (long long)w * h;
-    kf.crop_d = (uchar4*)kf_alloc(ctx, ob, crop_bytes);
-    if (!kf.crop_d) return fail(ROMAP_E_OOM, "crop allocation failed");
-    if (any_depth) {
-        kf.depth_d = (float*)kf_alloc(ctx, ob, npx * 4);
-        if (!kf.depth_d) return fail(ROMAP_E_OOM, "depth allocation failed");
-    }
-    kf.dev.crop = kf.crop_d;
-    kf.dev.depth = kf.depth_d;
-    // descriptor / prefix arrays (re-uploaded whole; grown geometrically)
-    if (ob->kfs.size() + 1 > ob->kfs_cap) {
-        size_t nc = ob->kfs_cap ? ob->kfs_cap * 2 : 16;
-        KfDev* nk = (KfDev*)dalloc(ctx, nc * sizeof(KfDev));
-        long long* np = (long long*)dalloc(ctx, nc * sizeof(long long));
-        if (!nk || !np) {
-            dfree(ctx, nk); dfree(ctx, np);          // (arena space of the crop stays with the object)
-            return fail(ROMAP_E_OOM, "keyframe table allocation failed");
-        }
-        CK(cudaStreamSynchronize(ctx->st));
-        dfree(ctx, ob->kfs_d);
-        dfree(ctx, ob->prefix_d);
-        ob->kfs_d = nk;
-        ob->prefix_d = np;
-        ob->kfs_cap = nc;
-    }
     const auto t3 = std::chrono::steady_clock::now();
-    CK(cudaMemcpyAsync(kf.crop_d, crop, crop_bytes, cudaMemcpyHostToDevice, ctx->st));
-    if (any_depth) CK(cudaMemcpyAsync(kf.depth_d, dep, npx * 4, cudaMemcpyHostToDevice, ctx->st));
-    if (stage == ctx->pin) {                       // the staging buffer is busy until these copies ran
-        CK(cudaEventRecord(ctx->pin_ev, ctx->st));
-        ctx->pin_pending = true;
-    } else {
-        CK(cudaStreamSynchronize(ctx->st));        // pageable fallback: the vector dies with this call
-    }
-    ob->kfs.push_back(kf);
-    ob->total_area += kf.area;
-    // descriptor table and exclusive area prefix, uploaded whole (the arrays may have been reallocated)
-    std::vector<KfDev> descs(ob->kfs.size());
-    std::vector<long long> prefix(ob->kfs.size());
-    long long acc = 0;
-    for (size_t i = 0; i < ob->kfs.size(); ++i) {
-        descs[i] = ob->kfs[i].dev;
-        prefix[i] = acc;
-        acc += ob->kfs[i].area;
-    }
-    CK(cudaMemcpyAsync(ob->kfs_d, descs.data(), descs.size() * sizeof(KfDev), cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ob->prefix_d, prefix.data(), prefix.size() * sizeof(long long), cudaMemcpyHostToDevice, ctx->st));
+    romap_status ak = append_keyframe(ctx, ob, T_wc, K, x0, y0, w, h, crop, any_depth ? dep : nullptr,
+                                      stage == ctx->pin);
+    if (ak) return ak;
     // (copies from pageable memory return once the source is staged: the host
     // vectors may go; the device sees the data in stream order)
     if (host_prof) {
@@ -2019,6 +2032,154 @@ romap_status romap_set_l2_flush(romap_ctx* ctx, int64_t bytes) {
         if (!ctx->flush_buf) return fail(ROMAP_E_OOM, "flush buffer");
         ctx->flush_bytes = (size_t)bytes;
     }
+    return ROMAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// checkpoint / resume of one object (SPEC.md External Interfaces: "header (config),
+// then raw little-endian parameter arrays"): the model configuration, box,
+// instance / object ids, Adam step, online-policy state, the fp32 parameters,
+// Adam moments and gradients, and every keyframe (descriptor + in-box crop +
+// optional depth crop), so that training resumes exactly where it stopped.
+namespace {
+const char kCkMagic[8] = {'R', 'O', 'M', 'A', 'P', 'C', 'K', '1'};
+struct CkHeader {
+    char magic[8];
+    uint32_t version, header_bytes;
+    romap_model_config cfg;
+    romap_box box;
+    int32_t instance_id, obj_id, rays_per_iter, has_gate_ref;
+    int64_t step, pending_iters, n_params;
+    double gate_ref[3];
+    int32_t n_kf, pad;
+};
+struct CkKeyframe {
+    float T[12];
+    float fx, fy, cx, cy;
+    int32_t x0, y0, w, h, has_depth, pad;
+};
+struct FileCloser {
+    FILE* f;
+    ~FileCloser() { if (f) fclose(f); }
+};
+}  // namespace
+
+romap_status romap_save_object(romap_ctx* ctx, int32_t obj, const char* path) {
+    CHECK_CTX();
+    Object* ob = find(ctx, obj);
+    if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
+    if (!path) return fail(ROMAP_E_INVALID, "null path");
+    const size_t n = (size_t)ob->cdev.n_table + ob->cdev.n_mlp;
+    std::vector<float> blk(4 * n);
+    CK(cudaMemcpyAsync(blk.data(), ob->p32, n * 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(blk.data() + n, ob->m, n * 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(blk.data() + 2 * n, ob->v, n * 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(blk.data() + 3 * n, ob->g32, n * 4, cudaMemcpyDeviceToHost, ctx->st));
+    std::vector<std::vector<uchar4>> crops(ob->kfs.size());
+    std::vector<std::vector<float>> deps(ob->kfs.size());
+    for (size_t i = 0; i < ob->kfs.size(); ++i) {
+        const Keyframe& kf = ob->kfs[i];
+        crops[i].resize((size_t)kf.area);
+        CK(cudaMemcpyAsync(crops[i].data(), kf.crop_d, (size_t)kf.area * 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (kf.depth_d) {
+            deps[i].resize((size_t)kf.area);
+            CK(cudaMemcpyAsync(deps[i].data(), kf.depth_d, (size_t)kf.area * 4, cudaMemcpyDeviceToHost, ctx->st));
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    CkHeader hd;
+    memset(&hd, 0, sizeof hd);
+    memcpy(hd.magic, kCkMagic, 8);
+    hd.version = 1;
+    hd.header_bytes = sizeof(CkHeader);
+    hd.cfg = ob->cfg;
+    hd.box = ob->box;
+    hd.instance_id = ob->instance_id;
+    hd.obj_id = ob->id;
+    hd.rays_per_iter = ob->rays_per_iter;
+    hd.has_gate_ref = ob->has_gate_ref ? 1 : 0;
+    hd.step = ob->step;
+    hd.pending_iters = ob->pending_iters;
+    hd.n_params = (int64_t)n;
+    for (int k = 0; k < 3; ++k) hd.gate_ref[k] = ob->gate_ref[k];
+    hd.n_kf = (int32_t)ob->kfs.size();
+    FileCloser fc{fopen(path, "wb")};
+    if (!fc.f) return fail(ROMAP_E_INVALID, "cannot open %s for writing", path);
+    bool ok = fwrite(&hd, sizeof hd, 1, fc.f) == 1 && fwrite(blk.data(), 4, blk.size(), fc.f) == blk.size();
+    for (size_t i = 0; ok && i < ob->kfs.size(); ++i) {
+        const Keyframe& kf = ob->kfs[i];
+        CkKeyframe ck;
+        memset(&ck, 0, sizeof ck);
+        for (int k = 0; k < 12; ++k) ck.T[k] = kf.dev.T[k];
+        ck.fx = kf.dev.fx; ck.fy = kf.dev.fy; ck.cx = kf.dev.cx; ck.cy = kf.dev.cy;
+        ck.x0 = kf.dev.x0; ck.y0 = kf.dev.y0; ck.w = kf.dev.w; ck.h = kf.dev.h;
+        ck.has_depth = kf.depth_d ? 1 : 0;
+        ok = fwrite(&ck, sizeof ck, 1, fc.f) == 1 && fwrite(crops[i].data(), 4, crops[i].size(), fc.f) == crops[i].size();
+        if (ok && kf.depth_d) ok = fwrite(deps[i].data(), 4, deps[i].size(), fc.f) == deps[i].size();
+    }
+    if (!ok) return fail(ROMAP_E_INVALID, "write error on %s", path);
+    return ROMAP_OK;
+}
+
+romap_status romap_load_object(romap_ctx* ctx, const char* path, int32_t obj_id, int32_t* out_obj) {
+    CHECK_CTX();
+    if (!path || !out_obj) return fail(ROMAP_E_INVALID, "null path / output");
+    FileCloser fc{fopen(path, "rb")};
+    if (!fc.f) return fail(ROMAP_E_INVALID, "cannot open %s", path);
+    CkHeader hd;
+    if (fread(&hd, sizeof hd, 1, fc.f) != 1 || memcmp(hd.magic, kCkMagic, 8) != 0 || hd.version != 1 ||
+        hd.header_bytes != sizeof(CkHeader))
+        return fail(ROMAP_E_INVALID, "%s is not a romap checkpoint of this version", path);
+    CfgDev cd;
+    romap_status st = build_cfg(&hd.cfg, cd);
+    if (st) return st;
+    if (hd.n_params != (int64_t)cd.n_table + cd.n_mlp || hd.n_kf < 0)
+        return fail(ROMAP_E_INVALID, "%s: parameter count does not match its configuration", path);
+    const size_t n = (size_t)hd.n_params;
+    std::vector<float> blk(4 * n);
+    if (fread(blk.data(), 4, blk.size(), fc.f) != blk.size()) return fail(ROMAP_E_INVALID, "%s: truncated", path);
+    struct Kf { CkKeyframe ck; std::vector<uchar4> crop; std::vector<float> dep; };
+    std::vector<Kf> kfs(hd.n_kf);
+    for (auto& k : kfs) {
+        if (fread(&k.ck, sizeof k.ck, 1, fc.f) != 1 || k.ck.w < 1 || k.ck.h < 1 || (long long)k.ck.w * k.ck.h > (1LL << 30))
+            return fail(ROMAP_E_INVALID, "%s: bad keyframe record", path);
+        k.crop.resize((size_t)k.ck.w * k.ck.h);
+        if (fread(k.crop.data(), 4, k.crop.size(), fc.f) != k.crop.size()) return fail(ROMAP_E_INVALID, "%s: truncated", path);
+        if (k.ck.has_depth) {
+            k.dep.resize(k.crop.size());
+            if (fread(k.dep.data(), 4, k.dep.size(), fc.f) != k.dep.size()) return fail(ROMAP_E_INVALID, "%s: truncated", path);
+        }
+    }
+    const int32_t id = obj_id >= 0 ? obj_id : hd.obj_id;
+    st = create_impl(ctx, &hd.box, &hd.cfg, hd.instance_id, id);
+    if (st) return st;
+    Object* ob = find(ctx, id);
+    CK(cudaMemcpyAsync(ob->p32, blk.data(), n * 4, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ob->m, blk.data() + n, n * 4, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ob->v, blk.data() + 2 * n, n * 4, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ob->g32, blk.data() + 3 * n, n * 4, cudaMemcpyHostToDevice, ctx->st));
+    k_to_half<<<(unsigned)((n + 255) / 256), 256, 0, ctx->st>>>(ob->p32, ob->p16, (long long)n);
+    CK(cudaGetLastError());
+    ob->step = hd.step;
+    CK(cudaMemcpyAsync(ob->step_d, &ob->step, 8, cudaMemcpyHostToDevice, ctx->st));
+    CK(upload_bias_corrections(ctx, ob));
+    ob->rays_per_iter = hd.rays_per_iter;
+    ob->has_gate_ref = hd.has_gate_ref != 0;
+    for (int k = 0; k < 3; ++k) ob->gate_ref[k] = hd.gate_ref[k];
+    ob->pending_iters = hd.pending_iters;
+    ob->grads_dirty = false;
+    for (auto& k : kfs) {
+        romap_intrinsics K{k.ck.fx, k.ck.fy, k.ck.cx, k.ck.cy, 0, 0};
+        st = append_keyframe(ctx, ob, k.ck.T, &K, k.ck.x0, k.ck.y0, k.ck.w, k.ck.h, k.crop.data(),
+                             k.ck.has_depth ? k.dep.data() : nullptr, false);
+        if (st) {
+            ctx->objs.erase(id);
+            free_object(ctx, ob);
+            return st;
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    *out_obj = id;
     return ROMAP_OK;
 }
 

@@ -116,6 +116,8 @@ _SIGS = {
     "romap_train_pending": [_P, _I, _I, _P, _P, _I, C.POINTER(_I)],
     "romap_set_l2_flush": [_P, C.c_int64],
     "romap_set_deterministic": [_P, _I],
+    "romap_save_object": [_P, _I, C.c_char_p],
+    "romap_load_object": [_P, C.c_char_p, _I, C.POINTER(_I)],
 }
 
 # device allocator callbacks of romap_ctx_create (romap.h): void* alloc(size_t, void*), void free(void*, void*)
@@ -438,6 +440,16 @@ class Context:
 
     def set_l2_flush(self, nbytes: int):
         _check(_lib.romap_set_l2_flush(self._h, int(nbytes)))
+
+    def save_object(self, obj: int, path: str):
+        """Checkpoint one object (romap.h romap_save_object)."""
+        _check(_lib.romap_save_object(self._h, obj, os.fsencode(path)))
+
+    def load_object(self, path: str, obj_id: int | None = None) -> int:
+        """Recreate an object from a checkpoint; returns its id."""
+        out = C.c_int32()
+        _check(_lib.romap_load_object(self._h, os.fsencode(path), -1 if obj_id is None else int(obj_id), C.byref(out)))
+        return out.value
 
     def set_deterministic(self, on: bool = True):
         """Deterministic-reduction mode (romap.h): fixed-order gradient / loss sums."""
