@@ -115,3 +115,19 @@ def test_paper_net_rejects_fp32_and_bad_layers(ctx):
         ctx.create_object([0, 0, 0], 0.0, [1, 1, 1], R.model_config(network=1, precision=0), 1)
     with pytest.raises(R.RomapError):
         ctx.create_object([0, 0, 0], 0.0, [1, 1, 1], R.model_config(network=1, precision=1, hidden_layers=4), 1)
+
+
+def test_paper_net_largest_table_grads(ctx):
+    """Table 4's largest table (T = 2^20: 16 levels of up to 1 M
+    entries, 64 MB fp16 / 128 MB fp32) on a ragged batch (777 rays x 32): geometry
+    bit-exact (the fused kernel's corner entries), every block within the fp64
+    tolerance and every level within the fp16 model's"""
+    sc = scenes.sphere_scene(0, depth_per_view=2)
+    kw = dict(PAPER, log2_T=20, rays_per_iter=777)
+    h, st = make_pair(R, ctx, sc, kw, avoid_kinks=False)
+    _grads(ctx, h, st)
+    rs = O.forward_rays(st, 1)
+    _, idx, _ = O.hash_encode(rs["u"][rs["hit"]].reshape(-1, 3), st.params["table"], st.cfg)
+    gi = ctx.debug_dump(h, R.DUMP_HASH_IDX).reshape(777, 32, 16, 8)[rs["hit"]].reshape(-1, 16, 8)
+    assert np.array_equal(gi.astype(np.int64), idx)
+    ctx.destroy_object(h)
