@@ -107,3 +107,42 @@ def test_atomic_build_matches_deterministic_build_per_level():
         assert max(e) < 1e-4, (j, np.round(e, 7))
         assert norm_rel(wa, wd) < 1e-4, j
         assert np.count_nonzero(td) > 0
+
+
+def test_many_tiny_objects_batch_equals_alone():
+    """40 objects of 1-5 rays (N = 32: 4 rays per tile, so most objects are one
+    padded tile and every CTA switches objects at almost every tile, reloading the
+    weights) trained 3 iterations in ONE graph-replayed train_step equal each object
+    trained alone, bit for bit, in the deterministic mode."""
+    sc = scenes.sphere_scene(0, n_views=8)
+    ob = sc.objects[0]
+    kw = dict(levels=8, log2_T=12, base_res=16, finest_res=2048.0, res_cap=128, samples_per_ray=32, precision=1,
+              seed=9)
+    rays = [1 + (7 * k) % 5 for k in range(40)]
+
+    def make(c, k):
+        h = c.create_object(ob.t, ob.yaw, ob.a, R.model_config(**dict(kw, rays_per_iter=rays[k])), ob.instance_id,
+                            obj_id=100 + k)
+        for fr in sc.frames:
+            c.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K)
+        return h
+
+    def read(c, h, st):
+        return (c.get_params(h, R.BLOCK_TABLE).copy(), c.get_params(h, R.BLOCK_MLP).copy(),
+                {k: st[k] for k in ("l_rgb", "l_rr", "l_depth", "l_density", "hit_rays", "step")})
+
+    c = R.Context(0)
+    c.set_deterministic(True)
+    hs = [make(c, k) for k in range(len(rays))]
+    st = c.train_step(hs, 3)
+    batch = [read(c, h, s) for h, s in zip(hs, st)]
+    for h in hs:
+        c.destroy_object(h)
+    alone = []
+    for k in range(len(rays)):
+        h = make(c, k)
+        alone.append(read(c, h, c.train_step([h], 3)[0]))
+        c.destroy_object(h)
+    c.close()
+    assert sum(b[2]["hit_rays"] for b in batch) > 0
+    _assert_same(batch, alone, "tiny objects")
