@@ -30,7 +30,8 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   hash_encode       vertex / cell-centre cases, sum of
                     trilinear weights = 1, dense-level bijection, continuity
                     (SPEC.md:278), brute-force XOR-hash on python ints
-  sh4               quadrature orthonormality + addition theorem
+  sh4               quadrature orthonormality + addition theorem; signs against
+                    scipy's complex harmonics with the Condon-Shortley phase
   mlp_forward       zero model (SPEC.md:253 adapted to R4), selection weights;
                     network 1 (R24): shapes for 1..3 hidden layers, zero model,
                     selection weights, whole-step central differences
@@ -41,7 +42,8 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   backward          central differences in fp64 through the whole step
   adam_update       closed form for constant gradient, zero-gradient no-op
                     (SPEC.md:271-273), sparse locality
-  render / query    constant-density closed form, outside-box zero (R21)
+  render / query    constant-density closed form, outside-box zero (R21);
+                    midpoints by hand, opaque-field depth = first stratum centre
   marching_tetrahedra  single-vertex case counts (6 on the Kuhn diagonal, 2
                     elsewhere), exact vertices for a linear field, sphere radius /
                     area within the lattice step; mesh_metrics shifted-grid closed form

@@ -2,7 +2,11 @@
 mutation below (a wrong operand, index, sign, RNG stream or dropped clamp in
 oracle/romap_oracle.py) is applied to a COPY of the oracle in a temporary tree,
 tests/test_oracle_pins.py runs against that copy, and at least one pin must fail.
-The working tree is never modified."""
+The working tree is never modified; the copies run several at a time.  Round 2
+added one mutation per remaining step of the path (levels, pixel draw, rays,
+slab, samples, encode / backward, SH, MLP backward, render forward / backward,
+losses, Adam, f2 / f3 host policy)."""
+import concurrent.futures
 import os
 import shutil
 import subprocess
@@ -32,27 +36,84 @@ MUTATIONS = {
                                      "w = w * (1.0 - fr[:, k] if bits[k] else fr[:, k])"),
     "render transmittance inclusive": ("Tr[:, 1:] = np.cumprod(alpha, axis=1)[:, :-1]", "Tr[:, :] = np.cumprod(alpha, axis=1)"),
     "Adam bias correction dropped": ("    mh = m[upd] / (1 - b1 ** t)", "    mh = m[upd]"),
+    # round 2: one mutation per remaining step of the path
+    "level resolution rounded": ("n = int(math.floor(cfg.base_res * b ** l + 1e-6))",
+                                 "n = int(math.floor(cfg.base_res * b ** l + 0.5))"),
+    "level blocks not padded": ("        off += (size + 15) // 16 * 16\n    return out", "        off += size\n    return out"),
+    "pixel draw modulo": ("idx = ((u * U64(total)) >> U64(32)).astype(np.int64)", "idx = (u % U64(total)).astype(np.int64)"),
+    "pixel_of_index left search": ('k = np.searchsorted(P, idx, side="right") - 1', 'k = np.searchsorted(P, idx, side="left") - 1'),
+    "unit float 23 bits": ("(np.asarray(u, dtype=np.uint32) >> np.uint32(8))", "(np.asarray(u, dtype=np.uint32) >> np.uint32(9))"),
+    "make_rays pixel centre dropped": ("    px = np.asarray(px).astype(f32) + f32(0.5)\n    py = np.asarray(py).astype(f32) + f32(0.5)\n    fx, fy, cx, cy = (f32(v)",
+                                       "    px = np.asarray(px).astype(f32)\n    py = np.asarray(py).astype(f32)\n    fx, fy, cx, cy = (f32(v)"),
+    "ray_box t_near not clamped at 0": ("    tn = np.zeros(R, f32)\n    tf = np.full(R, np.inf, f32)",
+                                        "    tn = np.full(R, -np.inf, f32)\n    tf = np.full(R, np.inf, f32)"),
+    "ray_box parallel miss ignored": ("        miss |= zero & (np.abs(ok) > ak)\n", ""),
+    "stratified last delta 0": ("    delta[:, -1] = Dl[:, 0]", "    delta[:, -1] = 0"),
+    "midpoints at 0": ("    s = np.arange(N, dtype=f32)[None, :] + f32(0.5)\n    dist = tn + s * Dl\n    return dist.astype(f32), np.broadcast_to",
+                       "    s = np.arange(N, dtype=f32)[None, :] + f32(0.0)\n    dist = tn + s * Dl\n    return dist.astype(f32), np.broadcast_to"),
+    "cell clamp at res": ("c = np.clip(np.floor(pos), 0, lev.res - 1).astype(np.int64)", "c = np.clip(np.floor(pos), 0, lev.res).astype(np.int64)"),
+    "dense index axes swapped": ("        return cx + n1 * (cy + n1 * cz)", "        return cz + n1 * (cy + n1 * cx)"),
+    "hash backward weights dropped": ("np.add.at(g, idx_all[:, l, b], w_all[:, l, b][:, None] * dfeat[:, l * F:(l + 1) * F])",
+                                      "np.add.at(g, idx_all[:, l, b], dfeat[:, l * F:(l + 1) * F])"),
+    "SH band 1 sign": ("    out[:, 1] = -0.48860251190291987 * y", "    out[:, 1] = 0.48860251190291987 * y"),
+    "SH band 2 constant sign": ("    out[:, 6] = 0.94617469575755997 * zz - 0.31539156525251999",
+                                "    out[:, 6] = 0.94617469575755997 * zz + 0.31539156525251999"),
+    "density clamp dropped": ("        return np.exp(np.minimum(r0, SIGMA_RAW_CLAMP))", "        return np.exp(r0)"),
+    "ReLU mask dropped in backward": ('    dh1 = (dr @ W[1]) * (fw["h1"] > 0)', '    dh1 = (dr @ W[1])'),
+    "density path dropped in backward": ('    dr[:, 0] += dsigma * density_activation_grad(fw["r"][:, 0], fw["sigma"], cfg.density_act)\n',
+                                         ""),
+    "colour sigmoid derivative": ("    dcraw = drgb * c * (1.0 - c)", "    dcraw = drgb * c"),
+    "background not composited": ("    C = (w[..., None] * rgb).sum(axis=1) + TN[:, None] * bg", "    C = (w[..., None] * rgb).sum(axis=1)"),
+    "render backward bg sign": ("- (TN * (gC * bg).sum(axis=1))[:, None])", "+ (TN * (gC * bg).sum(axis=1))[:, None])"),
+    "render backward suffix inclusive": ("        return s - x\n", "        return s\n"),
+    "density loss on object rays": ("    L_density = sigma_bg_sum[bgr].sum() / B", "    L_density = sigma_bg_sum[obj].sum() / B"),
+    "depth gradient sign": ("gD = np.where(dep, cfg.lambda_depth * np.sign(ed) / B, 0.0)", "gD = np.where(dep, -cfg.lambda_depth * np.sign(ed) / B, 0.0)"),
+    "occluders supervised": ("    sup = obj | bgr\n", "    sup = obj | bgr | hit\n"),
+    "Adam dense on tables": ("    upd = (g != 0) if sparse else np.ones(g.shape, bool)", "    upd = np.ones(g.shape, bool)"),
+    "Adam v without square": ("v[upd] = b2 * v[upd] + (1 - b2) * g[upd] * g[upd]", "v[upd] = b2 * v[upd] + (1 - b2) * np.abs(g[upd])"),
+    "occluder rays kept": ("    hit = hit & (cls != CLS_OCCLUDER)                       # R10: occluders dropped\n", ""),
+    "keyframe gate comparison inverted": ("    return alpha > alpha_deg, alpha", "    return alpha < alpha_deg, alpha"),
+    "scheduler ignores max_iters": ("        n = min(chunk, min(pending[k] for k in live), max_iters - done)",
+                                    "        n = min(chunk, min(pending[k] for k in live))"),
+    "marching tetrahedra edge point": ("        return pa + (iso - sa) / (sb - sa) * (pb - pa)", "        return pa + 0.5 * (pb - pa)"),
+    "to_world yaw sign": ("    out[..., 0] = c * X[..., 0] - s * X[..., 1] + box_t[0]", "    out[..., 0] = c * X[..., 0] + s * X[..., 1] + box_t[0]"),
 }
 
 
-@pytest.fixture(scope="module")
-def tree(tmp_path_factory):
-    d = tmp_path_factory.mktemp("mut")
+def _run_one(root, name):
+    """apply mutation `name` to a private copy of the oracle and run the pins on it"""
+    d = os.path.join(root, "m%02d" % list(MUTATIONS).index(name))
     for sub in ("oracle", "tests", "scenes"):
         shutil.copytree(os.path.join(ROOT, sub), os.path.join(d, sub),
                         ignore=shutil.ignore_patterns("__pycache__", "test_oracle_mutations.py"))
-    return str(d)
+    orig = open(os.path.join(ROOT, "oracle", "romap_oracle.py")).read()
+    a, b = MUTATIONS[name]
+    with open(os.path.join(d, "oracle", "romap_oracle.py"), "w") as f:
+        f.write(orig.replace(a, b))
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_oracle_pins.py", "-x", "-q", "-p", "no:cacheprovider"],
+                       cwd=d, capture_output=True, text=True, timeout=900, env=env)
+    return r.returncode, r.stdout[-2000:]
+
+
+@pytest.fixture(scope="module")
+def results(tmp_path_factory):
+    """every mutation's pin run, several at a time (each in its own tree)"""
+    root = str(tmp_path_factory.mktemp("mut"))
+    workers = max(1, min(8, os.cpu_count() or 1))
+    with concurrent.futures.ThreadPoolExecutor(workers) as ex:
+        futs = {name: ex.submit(_run_one, root, name) for name in MUTATIONS}
+        return {name: f.result() for name, f in futs.items()}
+
+
+def test_mutations_apply_once():
+    orig = open(os.path.join(ROOT, "oracle", "romap_oracle.py")).read()
+    for name, (a, _) in MUTATIONS.items():
+        assert orig.count(a) == 1, name
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name", list(MUTATIONS))
-def test_mutation_fails_a_pin(tree, name):
-    src = os.path.join(ROOT, "oracle", "romap_oracle.py")
-    orig = open(src).read()
-    a, b = MUTATIONS[name]
-    assert orig.count(a) == 1, name
-    with open(os.path.join(tree, "oracle", "romap_oracle.py"), "w") as f:
-        f.write(orig.replace(a, b))
-    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_oracle_pins.py", "-x", "-q", "-p", "no:cacheprovider"],
-                       cwd=tree, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 1 and " failed" in r.stdout, (name, r.stdout[-2000:])
+def test_mutation_fails_a_pin(results, name):
+    rc, out = results[name]
+    assert rc == 1 and " failed" in out, (name, out)

@@ -887,3 +887,98 @@ def test_depth_target_is_ray_distance():
     on = rs["px"] == 3
     assert np.all(rs["depth_t"][on] == f32(2.0))
     assert np.allclose(rs["depth_t"][~on].astype(np.float64), 3.0 * math.sqrt(1.0 + 1.0 / 16.0), rtol=1e-6, atol=0)
+
+
+# ---------------------------------------------------------------- round 2: pins found by the mutation test
+def test_midpoint_samples_hand_computed_and_opaque_depth():
+    # R12 inference sampling (xi = 1/2, delta = Delta): [1, 3] in 4 strata -> centres
+    dist, delta = O.midpoints(np.array([1.0], f32), np.array([3.0], f32), 4)
+    assert np.array_equal(dist[0], np.array([1.25, 1.75, 2.25, 2.75], f32))
+    assert np.array_equal(delta[0], np.full(4, 0.5, f32))
+    # an opaque constant field puts all weight on the first sample: the rendered depth
+    # is the centre of the first stratum, t_near + Delta / 2 (Eq. 6)
+    cfg = O.ModelConfig(levels=2, log2_T=8, base_res=4, finest_res=8.0, res_cap=0)
+    P = _constant_density_params(cfg, 14.0)
+    a = np.array([0.4, 0.3, 0.2], f32)
+    T = np.concatenate([np.eye(3), [[0.0], [0.0], [-2.0]]], 1).astype(f32)
+    K = np.array([40, 40, 8, 8], f32)
+    N = 16
+    _, dep, opa = O.render(cfg, np.zeros(3, f32), 0.0, a, P, T, K, 16, 16, N)
+    o, d, _ = O.make_rays(np.tile(np.arange(16), 16), np.repeat(np.arange(16), 16), K, T, np.zeros(3), 0.0)
+    tn, tf, hit = O.ray_box(o, d, a)
+    assert hit.any()
+    first = tn[hit].astype(np.float64) + 0.5 * (tf[hit] - tn[hit]).astype(np.float64) / N
+    assert np.allclose(dep.reshape(-1)[hit], first, rtol=0, atol=1e-5)
+    assert np.allclose(opa.reshape(-1)[hit], 1.0, atol=1e-9)
+
+
+def test_upper_face_belongs_to_the_last_cell():
+    # R5 / R6: u = 1 (the +a face, where the clamp of R6 lands points outside the box)
+    # is in cell N_l - 1 with fraction 1, so all 8 corners are those of the last cell
+    # and every index stays inside the level's own block
+    cfg = O.ModelConfig(levels=3, log2_T=10, base_res=4, finest_res=40.0, res_cap=0)
+    lt = O.level_table(cfg)
+    assert lt[0].dense and not lt[-1].dense
+    T = 1 << cfg.log2_T
+    u = np.array([[1.0, 1.0, 1.0], [1.0, 0.3, 0.0]], f32)
+    _, idx, w = O.hash_encode(u, np.zeros((O.table_entries(cfg), 2)), cfg)
+    for l, lev in enumerate(lt):
+        N = lev.res
+        for s, (cx, cy, cz) in enumerate([(N - 1, N - 1, N - 1), (N - 1, int(np.floor(f32(0.3) * f32(N))), 0)]):
+            exp = {lev.offset + int(O.corner_index(lev, cx + (b & 1), cy + ((b >> 1) & 1), cz + ((b >> 2) & 1), T))
+                   for b in range(8)}
+            assert set(idx[s, l].tolist()) == exp, (l, s)
+            assert np.all((idx[s, l] >= lev.offset) & (idx[s, l] < lev.offset + lev.size))
+        assert abs(w[0, l, 7] - 1.0) < 1e-12                      # the (N, N, N) vertex carries it all
+
+
+def test_sh_matches_complex_harmonics_with_condon_shortley_phase():
+    # R2: the 16 real SH of degree <= 3 are sqrt(2) Im Y_l^|m| (m < 0), Y_l^0, sqrt(2) Re Y_l^m
+    # (m > 0) of the complex orthonormal harmonics WITH the Condon-Shortley phase
+    # (scipy.special.sph_harm_y), ordered l = 0..3, m = -l..l -- this fixes the signs
+    # that orthonormality and the addition theorem leave free
+    from scipy.special import sph_harm_y
+    g = np.random.default_rng(8)
+    d = g.normal(size=(64, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    theta = np.arccos(np.clip(d[:, 2], -1, 1))
+    phi = np.arctan2(d[:, 1], d[:, 0])
+    cols = []
+    for l in range(4):
+        for m in range(-l, l + 1):
+            y = sph_harm_y(l, abs(m), theta, phi)
+            cols.append(math.sqrt(2) * y.imag if m < 0 else (y.real if m == 0 else math.sqrt(2) * y.real))
+    assert np.allclose(O.sh4(d), np.stack(cols, 1), atol=1e-12)
+
+
+def test_density_activation_saturates_at_the_clamp():
+    # R3: sigma = exp(min(raw0, 15)) saturates at e^15 (continuous at the clamp), with
+    # the straight-through derivative sigma; softplus is log(1 + e^r)
+    r = np.array([-3.0, 14.0, 15.0, 15.5, 40.0, 1e4])
+    s = O.density_activation(r, 0)
+    assert np.allclose(s[:3], np.exp(r[:3])) and np.all(s[2:] == s[2]) and s[2] == math.exp(15.0)
+    assert np.array_equal(O.density_activation_grad(r, s, 0), s)
+    assert np.allclose(O.density_activation(np.array([0.0, 30.0]), 1), [math.log(2.0), 30.0])
+
+
+def test_occluder_rays_are_dropped_before_sampling():
+    # R10: a ray of an occluder pixel gets no samples and no loss, even
+    # when it crosses the box; losses_and_render_grads also gives an occluder ray
+    # (if one reached it) neither loss nor gradient
+    cfg = O.ModelConfig(rays_per_iter=256, samples_per_ray=8)
+    st = _small_state(cfg, occluders=True)
+    rs = O.forward_rays(st, 1)
+    occ = rs["cls"] == O.CLS_OCCLUDER
+    _, _, box_hit = O.ray_box(rs["o"], rs["d"], st.box_a)
+    assert (occ & box_hit).any()
+    assert not (rs["hit"] & occ).any()
+    assert np.array_equal(rs["hit"], box_hit & ~occ)
+    L, _, _ = O.loss_and_grads(st, 1)
+    assert L["hit_rays"] == int((box_hit & ~occ).sum())
+    C = np.array([[0.9, 0.1, 0.3], [0.5, 0.5, 0.5]])
+    cls = np.array([O.CLS_OCCLUDER, O.CLS_OBJECT])
+    Ls, gC, gD = O.losses_and_render_grads(cls, np.array([True, True]), np.array([True, True]), C, np.array([3.0, 1.0]),
+                                           np.zeros((2, 3)), np.zeros((2, 3)), np.array([1.0, 1.0]),
+                                           np.array([5.0, 0.0]), 2.0, cfg)
+    assert np.all(gC[0] == 0) and gD[0] == 0 and np.any(gC[1] != 0)
+    assert abs(Ls["l_rgb"] - np.linalg.norm(C[1]) / 2) < 1e-12 and Ls["l_rr"] == 0 and Ls["l_density"] == 0
