@@ -77,6 +77,27 @@ MUTATIONS = {
                                     "        n = min(chunk, min(pending[k] for k in live))"),
     "marching tetrahedra edge point": ("        return pa + (iso - sa) / (sb - sa) * (pb - pa)", "        return pa + 0.5 * (pb - pa)"),
     "to_world yaw sign": ("    out[..., 0] = c * X[..., 0] - s * X[..., 1] + box_t[0]", "    out[..., 0] = c * X[..., 0] + s * X[..., 1] + box_t[0]"),
+    "scene segments by object id": ("    segs.sort(key=lambda s: (s[2], s[0], s[1]))", "    segs.sort(key=lambda s: (s[2], s[1], s[0]))"),
+    "query outside the box not zero": ("    inside = np.all(np.abs(xyz) <= a, axis=1)\n    u = (xyz + a)",
+                                       "    inside = np.ones(xyz.shape[0], bool)\n    u = (xyz + a)"),
+    "colour input order [sh || r]": ("    cin = np.concatenate([r, sh], axis=1)", "    cin = np.concatenate([sh, r], axis=1)"),
+    "paper net colour from raw 0..2": ("    c = 1.0 / (1.0 + np.exp(-raw[:, 1:4]))", "    c = 1.0 / (1.0 + np.exp(-raw[:, 0:3]))"),
+    "depth rendered from delta": ('"D": (w * dist).sum(axis=1)}', '"D": (w * delta).sum(axis=1)}'),
+    "rgb loss not divided by B": ("    L_rgb = ne[obj].sum() / B", "    L_rgb = ne[obj].sum()"),
+    "density-loss gradient not divided by B": ("cfg.lambda_density / B, 0.0)[:, None]", "cfg.lambda_density, 0.0)[:, None]"),
+    "hash mask modulo T - 1": ("    return (h & 0xFFFFFFFF) & (T - 1)", "    return (h & 0xFFFFFFFF) % (T - 1)"),
+    "crop one pixel short": ("    x0, x1 = int(xs.min()), int(xs.max()) + 1", "    x0, x1 = int(xs.min()), int(xs.max())"),
+    "depth kept on any class": ("z > 0 and cls[py - y0, px - x0] == CLS_OBJECT:", "z > 0:"),
+    "pixel stream 4": ("    u = rng_u32(seed, obj, t, np.arange(R), 0).astype(U64)", "    u = rng_u32(seed, obj, t, np.arange(R), 4).astype(U64)"),
+    "Adam eps inside the root": ("    p[upd] = p[upd] - cfg.lr * mh / (np.sqrt(vh) + cfg.eps)", "    p[upd] = p[upd] - cfg.lr * mh / np.sqrt(vh + cfg.eps)"),
+    "gate angle in radians": ("    return math.degrees(math.acos(min(1.0, max(-1.0, c))))", "    return math.acos(min(1.0, max(-1.0, c)))"),
+    "lattice axis swapped": ("    P = np.stack(np.meshgrid(*axes, indexing=\"ij\"), -1)", "    P = np.stack(np.meshgrid(*axes, indexing=\"xy\"), -1)"),
+    "metrics acc / comp swapped": ('    return {"acc": float(acc), "comp": float(dc.mean())', '    return {"acc": float(dc.mean()), "comp": float(acc)'),
+    "carve ignores points behind the camera": ("        seen |= (xc[2] > 0) & (u >= kf.x0)", "        seen |= (u >= kf.x0)"),
+    "object rays composited over black": ("    if cfg.obj_bg == 1:", "    if cfg.obj_bg == 0:"),
+    "initial tables not small": ("    table = g.uniform(-1e-4, 1e-4, size=(table_entries(cfg), cfg.feats))",
+                                 "    table = g.uniform(-1e-2, 1e-2, size=(table_entries(cfg), cfg.feats))"),
+    "paper net hidden ReLU dropped": ("        hs.append(relu(hs[-1] @ W[k].T))", "        hs.append(hs[-1] @ W[k].T)"),
 }
 
 

@@ -982,3 +982,100 @@ def test_occluder_rays_are_dropped_before_sampling():
                                            np.array([5.0, 0.0]), 2.0, cfg)
     assert np.all(gC[0] == 0) and gD[0] == 0 and np.any(gC[1] != 0)
     assert abs(Ls["l_rgb"] - np.linalg.norm(C[1]) / 2) < 1e-12 and Ls["l_rr"] == 0 and Ls["l_density"] == 0
+
+
+def _constant_field_params(cfg, raw0, rgb):
+    # network 0: sigma = exp(raw0) and colour = rgb everywhere: feat = ones, raw = (raw0,
+    # 0, ...); the SH band-0 constant 1/(2 sqrt(pi)) feeds g1[0] = g2[0] = Y00 and the
+    # last layer turns it into logit(rgb)
+    P = _constant_density_params(cfg, abs(raw0))
+    P["W"][1][0, 0] = math.copysign(1.0, raw0)          # raw0 < 0 through the positive h1[0]
+    y00 = 0.28209479177387814
+    P["W"][2][0, cfg.density_out] = 1.0
+    P["W"][3][0, 0] = 1.0
+    P["W"][4][:, 0] = [math.log(c / (1 - c)) / y00 for c in rgb]
+    return P
+
+
+def test_render_scene_composites_by_t_near_not_id():
+    # R20: the nearer box is composited first whatever its id: C = C_1 + (1 - A_1) C_0
+    # with C_s = rgb_s A_s, A_s = 1 - exp(-sigma_s L_s) (box 1 in front of box 0)
+    cfg = O.ModelConfig(levels=2, log2_T=8, base_res=4, finest_res=8.0, res_cap=0)
+    a = np.array([0.3, 0.3, 0.3], f32)
+    spec = {0: (0.4, (0.9, 0.1, 0.2), np.array([0.0, 0.0, 1.0], f32)),
+            1: (0.1, (0.2, 0.7, 0.3), np.array([0.0, 0.0, 0.0], f32))}
+    objs = [(cfg, spec[i][2], 0.0, a, _constant_field_params(cfg, spec[i][0], spec[i][1]), i) for i in (0, 1)]
+    T = np.concatenate([np.eye(3), [[0.0], [0.0], [-2.0]]], 1).astype(f32)
+    K = np.array([60, 60, 6, 6], f32)
+    rgb, _, opa = O.render_scene(objs, T, K, 12, 12, 32)
+    px, py = np.tile(np.arange(12), 12), np.repeat(np.arange(12), 12)
+    A, C = {}, {}
+    for i in (0, 1):
+        o, d, _ = O.make_rays(px, py, K, T, spec[i][2], 0.0)
+        tn, tf, hit = O.ray_box(o, d, a)
+        A[i] = np.where(hit, 1 - np.exp(-math.exp(spec[i][0]) * (tf - tn).astype(np.float64)), 0.0)
+        C[i] = A[i][:, None] * np.asarray(spec[i][1])[None, :]
+    both = (A[0] > 0) & (A[1] > 0)
+    assert both.any()
+    assert np.allclose(rgb.reshape(-1, 3), C[1] + (1 - A[1])[:, None] * C[0], atol=1e-6)
+    assert np.allclose(opa.reshape(-1), 1 - (1 - A[0]) * (1 - A[1]), atol=1e-6)
+
+
+def test_supervised_rays_composite_over_their_background_colour():
+    # R14: obj_bg = 0 composites every supervised ray over its random colour b, so an
+    # (almost) empty field renders C = b and L_rgb = sum_{R_o} |b - C_gt| / B (Eq. 7);
+    # obj_bg = 1 composites object rays over black: L_rgb = sum_{R_o} |C_gt| / B
+    for obj_bg in (0, 1):
+        cfg = O.ModelConfig(rays_per_iter=128, samples_per_ray=8, obj_bg=obj_bg)
+        st = _small_state(cfg)
+        st.params = _constant_field_params(cfg, -60.0, (0.5, 0.5, 0.5))
+        L, _, dbg = O.loss_and_grads(st, 1)
+        rs = dbg["rays"]
+        obj = rs["hit"] & (rs["cls"] == O.CLS_OBJECT)
+        assert obj.any()
+        ref = rs["tgt"][obj].astype(np.float64) - (rs["bg"][obj] if obj_bg == 0 else 0.0)
+        assert abs(L["l_rgb"] - np.linalg.norm(ref, axis=1).sum() / 128) < 1e-9, obj_bg
+
+
+def test_ingest_keeps_depth_on_object_pixels_only():
+    # SPEC.md:304 (has_depth => object pixel): samples on occluder / background pixels
+    # of the box or outside it are dropped; a sample lands on (floor u, floor v)
+    mask = np.zeros((6, 8), np.uint16)
+    mask[2:5, 3:6] = 7
+    mask[2, 3] = 9
+    mask[4, 5] = 0
+    rgb = np.zeros((6, 8, 3), np.uint8)
+    samples = [(4.7, 3.2, 1.5), (3.5, 2.5, 2.0), (5.2, 4.9, 2.5), (0.5, 0.5, 3.0), (4.1, 2.0, -1.0)]
+    kf = O.ingest_observation(rgb, mask, np.eye(3, 4), [1, 1, 0, 0], 7, samples)
+    exp = np.zeros((3, 3), f32)
+    exp[1, 1] = 1.5
+    assert np.array_equal(kf.depth, exp)
+
+
+def test_adam_epsilon_outside_the_root():
+    # Adam (Kingma & Ba, Alg. 1): p -= lr m_hat / (sqrt(v_hat) + eps);
+    # for a constant g from zero moments the step is lr g / (|g| + eps): g = eps -> lr / 2
+    cfg = O.ModelConfig(eps=1e-2)
+    p = np.array([0.0])
+    O.adam_update(p, np.array([1e-2]), np.zeros(1), np.zeros(1), 1, cfg, sparse=False)
+    assert abs(p[0] + cfg.lr / 2) < 1e-15
+
+
+def test_lattice_points_axes_and_metric_directions():
+    # R21 lattice: P[ix, iy, iz] = (-a_x + 2 a_x ix / R, ...) for unequal half extents
+    a = (0.1, 0.2, 0.3)
+    P = O.lattice_points(a, 2)
+    assert P.shape == (3, 3, 3, 3)
+    assert np.allclose(P[2, 0, 1], [0.1, -0.2, 0.0]) and np.allclose(P[0, 1, 2], [-0.1, 0.0, 0.3])
+    # PAPER.md:255 metrics: a reconstruction that is half of the ground truth is exact
+    # (accuracy 0) but incomplete (completion > 0, ratio < 1)
+    xs = np.linspace(0, 1, 11)
+    G = np.stack(np.meshgrid(xs, xs, [0.0], indexing="ij"), -1).reshape(-1, 3)
+    m = O.mesh_metrics(G[G[:, 0] <= 0.5], G, tau=0.05)
+    assert m["acc"] == 0.0 and m["comp"] > 0.1 and m["cr"] < 0.6
+
+
+def test_initial_tables_are_small():
+    # R19 / SPEC.md:285: tables start U(-1e-4, 1e-4)
+    t = O.init_params(O.ModelConfig(), 0)["table"]
+    assert np.abs(t).max() <= 1e-4 and np.abs(t).max() > 0.99e-4 and abs(t.std() - 1e-4 / math.sqrt(3)) < 2e-6
