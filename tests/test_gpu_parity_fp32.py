@@ -137,6 +137,9 @@ def test_adam_on_identical_gradients(ctx, scene0):
         pick = g.choice(ne, size=ne // 3, replace=False)
         gt[pick] = g.normal(0, 1e-3, (pick.size, 2)).astype(np.float32)
         gw = [g.normal(0, 1e-2, w.shape).astype(np.float32) for w in st.params["W"]]
+        if t > 1:                                # the MLP is dense (R18): exact zeros still move p, m, v
+            for w in gw:
+                w[g.random(w.shape) < 0.2] = 0.0
         ctx.set_params(h, R.BLOCK_GRAD_TABLE, gt)
         ctx.set_params(h, R.BLOCK_GRAD_MLP, flat_W(gw))
         ctx.optimizer_step([h])
@@ -158,6 +161,9 @@ def test_adam_on_identical_gradients(ctx, scene0):
     assert np.all(m[untouched] == 0) and np.all(v[untouched] == 0)
     pm = ctx.get_params(h, R.BLOCK_MLP)
     assert np.allclose(pm, flat_W(st.params["W"]), rtol=1e-6, atol=3e-8)
+    # MLP moments (g ~ 1e-2: m ~ 1e-3, v ~ 1e-7), absolute floors ~1e-6 of those for cancellations
+    assert np.allclose(ctx.get_params(h, R.BLOCK_M_MLP), flat_W(st.m["W"]), rtol=1e-5, atol=1e-9)
+    assert np.allclose(ctx.get_params(h, R.BLOCK_V_MLP), flat_W(st.v["W"]), rtol=1e-5, atol=1e-13)
     assert ctx.get_params(h, R.BLOCK_STEP)[0] == 3
     assert np.all(ctx.get_params(h, R.BLOCK_GRAD_TABLE) == 0)
     ctx.destroy_object(h)
