@@ -326,7 +326,12 @@ romap_status romap_block_bytes(romap_ctx* ctx, int32_t obj, int32_t block, int64
 romap_status romap_dump_bytes(romap_ctx* ctx, int32_t obj, int32_t what, int64_t* bytes);
 romap_status romap_debug_dump(romap_ctx* ctx, int32_t obj, int32_t what, void* buf, int64_t bytes);
 
-/* Per-stage device timing of train_step / forward_backward / optimizer_step:
+/* Tracing: every training / inference entry point (and each graph-replay batch
+ * inside train_step) is an NVTX range named after the call ("romap_train_step",
+ * "graph_replay", "romap_render_scene", ...), so a profiler can select its kernels,
+ * e.g. `ncu --nvtx --nvtx-include "romap_train_step/"`.  No cost without a tool.
+ *
+ * Per-stage device timing of train_step / forward_backward / optimizer_step:
  * when enabled, the library brackets every kernel it launches with CUDA events
  * on the context's stream and accumulates the elapsed time per stage.  Launch
  * counters are always kept.  enable(ctx, 1) also resets the counters. */

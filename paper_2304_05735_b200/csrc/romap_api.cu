@@ -24,8 +24,21 @@
 #include <cstdlib>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/romap.h"
 #include "romap_internal.cuh"
+
+// NVTX ranges around the public entry points and the stages of a train_step, so
+// `ncu --nvtx --nvtx-include "romap_train_step/"` (or an nsys timeline) can select
+// and attribute kernels; header-only NVTX3, a no-op unless a tool is attached
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define NVTX_RANGE(name) NvtxRange nvtx_range_(name)
 
 void launch_fused_mixed(const LaunchCtx& lc, const CfgDev& cfg, const ObjDev* objs, const RayRec* rays,
                         const float4* srec, const float* sdelta, int n_rays, double* loss_acc, int* nonfinite,
@@ -643,6 +656,7 @@ static romap_status create_impl(romap_ctx* ctx, const romap_box* box, const roma
 
 romap_status romap_create_object(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
                                  int32_t instance_id, int32_t* out_obj) {
+    NVTX_RANGE("romap_create_object");
     CHECK_CTX();
     if (!out_obj) return fail(ROMAP_E_INVALID, "null out_obj");
     int id = ctx->next_id;
@@ -653,6 +667,7 @@ romap_status romap_create_object(romap_ctx* ctx, const romap_box* box, const rom
 
 romap_status romap_create_object_with_id(romap_ctx* ctx, const romap_box* box, const romap_model_config* cfg,
                                          int32_t instance_id, int32_t obj_id) {
+    NVTX_RANGE("romap_create_object_with_id");
     CHECK_CTX();
     return create_impl(ctx, box, cfg, instance_id, obj_id);
 }
@@ -811,6 +826,7 @@ static romap_status append_keyframe(romap_ctx* ctx, Object* ob, const float T_wc
 romap_status romap_add_observation(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, const uint16_t* mask,
                                    const float T_wc[12], const romap_intrinsics* K,
                                    const romap_depth_sample* depth, int32_t n_depth) {
+    NVTX_RANGE("romap_add_observation");
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
@@ -1160,6 +1176,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
             memcpy(g.ptrs, ptrs, sizeof ptrs);
         }
         if (g.exec) {
+            NVTX_RANGE("graph_replay");
             for (int c = 0; c < n_chunks; ++c) CK(cudaGraphLaunch(g.exec, ctx->st));
             ctx->prof.launches[ST_GRAPH] += n_chunks;
             it0 = n_chunks * K;
@@ -1219,6 +1236,7 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
 
 romap_status romap_train_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs, int32_t n_iters,
                               romap_train_stats* out) {
+    NVTX_RANGE("romap_train_step");
     CHECK_CTX();
     if (n_iters < 1) return fail(ROMAP_E_INVALID, "n_iters must be >= 1");
     Batch b;
@@ -1230,6 +1248,7 @@ romap_status romap_train_step(romap_ctx* ctx, const int32_t* objs, int32_t n_obj
 }
 
 romap_status romap_forward_backward(romap_ctx* ctx, const int32_t* objs, int32_t n_objs, romap_train_stats* out) {
+    NVTX_RANGE("romap_forward_backward");
     CHECK_CTX();
     Batch b;
     romap_status s = make_batch(ctx, objs, n_objs, true, b);
@@ -1247,6 +1266,7 @@ romap_status romap_offer_observation(romap_ctx* ctx, int32_t obj, const uint8_t*
                                      const float T_wc[12], const romap_intrinsics* K,
                                      const romap_depth_sample* depth, int32_t n_depth, float alpha_deg,
                                      int32_t iters_per_update, int32_t* accepted, float* alpha_out) {
+    NVTX_RANGE("romap_offer_observation");
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
@@ -1292,6 +1312,7 @@ romap_status romap_pending_iters(romap_ctx* ctx, int32_t obj, int64_t* pending) 
 
 romap_status romap_train_pending(romap_ctx* ctx, int32_t chunk, int32_t max_iters, int32_t* objs_out,
                                  int32_t* iters_out, int32_t cap, int32_t* n_out) {
+    NVTX_RANGE("romap_train_pending");
     CHECK_CTX();
     if (chunk < 1 || max_iters < 0 || cap < 0 || !n_out || (cap > 0 && (!objs_out || !iters_out)))
         return fail(ROMAP_E_INVALID, "bad scheduler arguments");
@@ -1473,6 +1494,7 @@ romap_status romap_async_stop(romap_ctx* ctx, int32_t finish_pending, romap_asyn
 }
 
 romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs) {
+    NVTX_RANGE("romap_optimizer_step");
     CHECK_CTX();
     Batch b;
     romap_status s = make_batch(ctx, objs, n_objs, false, b);
@@ -1561,6 +1583,7 @@ static romap_status render_one(romap_ctx* ctx, Object* ob, const float T_wc[12],
 
 romap_status romap_render(romap_ctx* ctx, int32_t obj, const float T_wc[12], const romap_intrinsics* K,
                           int32_t samples_per_ray, float* rgb, float* depth, float* opacity, int32_t flags) {
+    NVTX_RANGE("romap_render");
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
@@ -1574,6 +1597,7 @@ romap_status romap_render(romap_ctx* ctx, int32_t obj, const float T_wc[12], con
 romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, const float T_wc[12],
                                 const romap_intrinsics* K, int32_t samples_per_segment, float* rgb, float* depth,
                                 float* opacity, int32_t flags) {
+    NVTX_RANGE("romap_render_scene");
     CHECK_CTX();
     if (!objs || n < 1) return fail(ROMAP_E_INVALID, "empty object list");
     if (n > 8192) return fail(ROMAP_E_INVALID, "render_scene takes at most 8192 objects");
@@ -1720,6 +1744,7 @@ romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, 
 // marching tetrahedra count / scan / emit (k_mesh.cu)
 romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float sigma_iso, float* tris,
                                 int64_t cap_tris, int64_t* n_tris, int32_t flags) {
+    NVTX_RANGE("romap_extract_mesh");
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
@@ -1769,6 +1794,7 @@ romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float 
 
 romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, int64_t n, float* sigma,
                                  int32_t flags) {
+    NVTX_RANGE("romap_query_density");
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
@@ -2065,6 +2091,7 @@ struct FileCloser {
 }  // namespace
 
 romap_status romap_save_object(romap_ctx* ctx, int32_t obj, const char* path) {
+    NVTX_RANGE("romap_save_object");
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
@@ -2122,6 +2149,7 @@ romap_status romap_save_object(romap_ctx* ctx, int32_t obj, const char* path) {
 }
 
 romap_status romap_load_object(romap_ctx* ctx, const char* path, int32_t obj_id, int32_t* out_obj) {
+    NVTX_RANGE("romap_load_object");
     CHECK_CTX();
     if (!path || !out_obj) return fail(ROMAP_E_INVALID, "null path / output");
     FileCloser fc{fopen(path, "rb")};
