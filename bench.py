@@ -684,7 +684,8 @@ def run_ours(args):
             desc = (f"L=16 F=2 T=2^{kw['log2_T']} res 16->512, density 32->64->16 + SH4 colour 32->64->64->3, "
                     f"{kw['rays_per_iter']} rays x 64 stratified samples per object, Adam")
         objs_total = args.objects or (64 if workload in ("cfg3", "cfg4") else ws * args.objects_per_gpu)
-        cpu = None if args.no_cpu_baseline else cpu_baseline(obs[0][0], obs[0][1], kw)
+        # the oracle's CPU baseline: rank 0 at N = 1 only (the contract; a multi-GPU run stays short)
+        cpu = None if (args.no_cpu_baseline or ws > 1) else cpu_baseline(obs[0][0], obs[0][1], kw)
         t_iter_obj_ms = (t_max_ms / args.steps) / len(hs)
         strong = workload in ("cfg3", "cfg4") or bool(args.objects)
         line = {
