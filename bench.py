@@ -636,6 +636,11 @@ def run_ours(args):
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
+    # device-timed (CUDA events on torch's stream; the library's blocking stream is
+    # ordered with it), so the host work between the records (ingest, enqueue, the
+    # statistics read) is inside the interval
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         for h, (rgb, mask, fr, ob) in zip(hs, pinned):
@@ -645,8 +650,10 @@ def run_ours(args):
             h2d += (xs.max() - xs.min() + 1) * (ys.max() - ys.min() + 1) * 4 + 96 + 8
         st = ctx.train_step(hs, args.e2e_iters)
         e2e_samples += sum(s["samples"] for s in st)
+    e1.record()
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    e2e_wall_s = time.perf_counter() - t0
+    e2e_s = e0.elapsed_time(e1) * 1e-3
     if pg:
         pg.barrier()
 
@@ -731,7 +738,8 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "ray-samples/s", "h2d_bytes_per_step": int(h2d / max(1, args.e2e_steps)),
                     "d2h_bytes_per_step": int(len(hs) * 72 + 4),
                     "step": f"add_observation(1 keyframe per object, host) + train_step({args.e2e_iters} iterations, "
-                            "graph replay) + per-object stats D2H"},
+                            "graph replay) + per-object stats D2H",
+                    "timing": "CUDA events around the e2e steps (max over ranks)", "wall_s_rank0": e2e_wall_s},
             "clocks": tr["clocks"],
             "inference": infer,
         }
