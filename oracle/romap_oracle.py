@@ -15,6 +15,7 @@ contraction; everything else in fp64.
 
 Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   level_table       hand-listed resolutions / entry totals (BASELINE cfg0, cfg1)
+  init_params       table range U(-1e-4, 1e-4) (R19)
   mix64 / rng_u32   published SplitMix64 output vectors (golden file)
   draw_pixels       bijection over all in-box pixels (brute force), chi^2
   rng_u32 key       golden u32 of the composed key from an independent python-int
@@ -23,13 +24,16 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   make_rays         principal-point ray, projection round trip
   make_rays_per_ray equals make_rays ray by ray (bitwise), round trip with per-ray K
   sample_points     hand-computed u for unequal half extents, clamp at the faces (R6)
-  forward_rays      R17 depth target: z on the optical axis, z*|dc| off axis
+  forward_rays      R17 depth target: z on the optical axis, z*|dc| off axis;
+                    occluder rays dropped even when they cross the box (R10)
+  ingest_observation  AABB / classes by hand; depth kept on object pixels only
   ray_box           (4,6) example, parallel miss,
                     dense-stepping membership oracle
   stratified        one sample per stratum, ascending, mean≈midpoint
   hash_encode       vertex / cell-centre cases, sum of
                     trilinear weights = 1, dense-level bijection, continuity
-                    (SPEC.md:278), brute-force XOR-hash on python ints
+                    (SPEC.md:278), brute-force XOR-hash on python ints; the
+                    upper face u = 1 in the last cell (R5 / R6)
   sh4               quadrature orthonormality + addition theorem; signs against
                     scipy's complex harmonics with the Condon-Shortley phase
   mlp_forward       zero model (SPEC.md:253 adapted to R4), selection weights;
@@ -38,17 +42,24 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   volume_render     sigma=0, opaque first sample, ln2 case,
                     constant-density closed form 1-exp(-sigma L) (north_star)
   losses            (0.3,0,0.4)->0.5, decomposition identity,
-                    occluder exclusion, background-only batch
+                    occluder exclusion, background-only batch (SPEC.md:427,449,450);
+                    an empty field renders every supervised ray as its
+                    background colour (R14, both obj_bg settings)
+  density_activation  saturation at the clamp, straight-through derivative (R3)
   backward          central differences in fp64 through the whole step
   adam_update       closed form for constant gradient, zero-gradient no-op
-                    (SPEC.md:271-273), sparse locality
+                    (SPEC.md:271-273), sparse locality, g = eps
+                    gives a step of lr/2 (eps outside the root)
   render / query    constant-density closed form, outside-box zero (R21);
                     midpoints by hand, opaque-field depth = first stratum centre
+  render_scene      two boxes closed form; the nearer box first whatever its id (R20)
   marching_tetrahedra  single-vertex case counts (6 on the Kuhn diagonal, 2
                     elsewhere), exact vertices for a linear field, sphere radius /
                     area within the lattice step; mesh_metrics shifted-grid closed form
-tests/test_oracle_mutations.py applies plausible mistakes (wrong index / sign / stream /
-operand) to this file one at a time and checks that each fails a pin.
+                    and a half reconstruction (acc 0, comp > 0); lattice axes
+tests/test_oracle_mutations.py applies 64 plausible mistakes (wrong index / sign /
+stream / operand / dropped term) to copies of this file, one at a time, and checks
+that each fails a pin.
 """
 from __future__ import annotations
 
