@@ -427,8 +427,9 @@ __device__ __forceinline__ void epi_mask64(uint32_t wk, uint8_t* out, const uint
 }
 
 // ---------------------------------------------------------------------------
-// G: gathers of tile `it` interleaved with the scatter of tile `it - 2`
-// (warpgroup WG owns levels [WG L/2, (WG + 1) L/2); one code path for both
+// G: gathers of tile `it` interleaved with the scatter of tile `it - NB`
+// (warpgroup WG owns the level pairs (p, L-1-p) with p = WG, WG + 2, ...: a coarse
+// and a fine level per trip; one code path for both
 // warpgroups, level loop not unrolled: the body stays in the instruction cache)
 template <int L>
 __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restrict__ objs,
@@ -542,7 +543,7 @@ __device__ __forceinline__ void g_loop(const CfgDev& cfg, const ObjDev* __restri
                     xv[q][p] = (ag_ && !same) ? xldg1(tl + e[q][2 * p + 1]) : 0u;
                 }
             }
-            // (2) scatter of the same levels of tile it-2 (fire-and-forget REDs).
+            // (2) scatter of the same levels of tile it-NB (fire-and-forget REDs).
             // Coarse levels (res < MERGE_RES): consecutive samples of a ray often
             // share a cell, i.e. all 8 corners; a 2-step warp segmented sum over
             // runs of equal cells lets one lane per 4 run members issue the REDs
