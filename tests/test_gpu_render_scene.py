@@ -81,8 +81,9 @@ def test_render_scene_camera_inside_and_miss():
 
 
 def test_render_scene_batched_mixed_and_fp32_groups():
-    """the batched path with two model groups in one scene (5 mixed-precision objects
-    and one fp32 object: one forward launch per group, segments of all objects in one
+    """the batched path with three model groups in one scene (4 mixed-precision
+    objects of the BASELINE network, one of the paper's network with 2 hidden layers,
+    R24, and one fp32 object: one forward launch per group, segments of all objects in one
     composite), a sample count that is not a power of two (object ranges padded to
     128-sample tile boundaries), against the oracle: hit pixels identical (bit-exact
     geometry), colour / opacity within the mixed path's 2e-2 (fp32-only pixels 1e-4)"""
@@ -91,10 +92,16 @@ def test_render_scene_batched_mixed_and_fp32_groups():
     hs, objs = [], []
     for k, ob in enumerate(sc.objects[:6]):
         kw = dict(CFG0, precision=0 if k == 2 else 1)
+        if k == 4:
+            kw.update(network=1, hidden_layers=2)
         h, st = make_pair(R, c, sc, kw, param_seed=30 + k, inst=ob.instance_id, obj_id=600 + k, avoid_kinks=False)
         hs.append(h)
         objs.append((st.cfg, st.box_t, st.box_yaw, st.box_a, st.params, h))
     W, H, N = 120, 90, 24
+    # every group is on screen in some frame (the paper-network object included)
+    for k in (2, 4):
+        cf, bt, yaw, ba, params, _ = objs[k]
+        assert any(O.render(cf, bt, yaw, ba, params, fr.T_wc, fr.K, W, H, N)[2].max() > 0 for fr in sc.frames[:3]), k
     for fr in sc.frames[:3]:
         rgb, dep, opa = c.render_scene(hs, fr.T_wc, fr.K, W, H, N)
         orgb, odep, oopa = O.render_scene(objs, fr.T_wc, fr.K, W, H, N)
