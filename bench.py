@@ -473,7 +473,8 @@ def run_reference(args):
     v = samples / dt
     line = {"impl": "reference", "metric": "NeRF train ray-samples/s", "value": v, "unit": "ray-samples/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if workload in ("cfg3", "cfg4") else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded box-union-torus SDF object, 20 keyframes 640x480)",
             "config": {"workload": f"{workload} (reference = the CPU oracle on one object, bounded sample)",
                        "rays_per_iter": rays, "samples_per_ray": kw["samples_per_ray"], "levels": kw["levels"],
