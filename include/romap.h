@@ -133,9 +133,11 @@ typedef struct {
 
 /* Parameter blocks for get/set_params (little-endian, row-major):
  *   TABLE*: fp32 [table_entries][feats], levels back to back (level l starts at the
- *           sum of E_k for k < l; dense index x+(N+1)(y+(N+1)z), R5)
- *   MLP*:   fp32 W1[64][L*F], W2[16][64], W3[64][32], W4[64][64], W5[3][64]
- *           (out x in, bias-free, R1/R4), concatenated in that order
+ *           sum over k < l of E_k rounded up to a multiple of 16 entries; dense
+ *           index x+(N+1)(y+(N+1)z), hashed as R5; R5)
+ *   MLP*:   fp32, out x in, bias-free (R1/R4), concatenated in this order:
+ *           network 0: W1[64][L*F], W2[16][64], W3[64][32], W4[64][64], W5[3][64];
+ *           network 1 (R24): W1[64][L*F], (hidden_layers - 1) x W[64][64], W_out[4][64]
  *   STEP:   int64 Adam step t */
 #define ROMAP_BLOCK_TABLE 0
 #define ROMAP_BLOCK_MLP 1
@@ -159,7 +161,7 @@ typedef struct {
  *   HASH_IDX: int32[n_rays][N][L][8] absolute table entry per corner
  *   FEATURES: float[n_rays][N][L*F]
  *   FIELD:    float[n_rays][N][4] = sigma, r, g, b
- *   RAY_GRADS:float[n_rays][N][4] = dL/dsigma, dL/dc (r,g,b) (fp32 path only) */
+ *   RAY_GRADS:float[n_rays][N][4] = dL/dsigma, dL/dc (r,g,b) (after forward_backward) */
 #define ROMAP_DUMP_RAYS 0
 #define ROMAP_DUMP_SAMPLES 1
 #define ROMAP_DUMP_HASH_IDX 2
