@@ -245,8 +245,10 @@ romap_status romap_forward_backward(romap_ctx* ctx, const int32_t* objs, int32_t
 romap_status romap_optimizer_step(romap_ctx* ctx, const int32_t* objs, int32_t n_objs);
 
 /* Render one object from pose T_wc (R12 midpoint samples, composited over black):
- * rgb float [H][W][3], depth float [H][W] (ray distance), opacity float [H][W];
- * any output may be NULL. */
+ * rgb float [H][W][3], depth float [H][W] (ray distance), opacity float [H][W]
+ * (H = K->height, W = K->width); any output may be NULL.  E_INVALID: null pose /
+ * intrinsics, non-positive size or focal length, samples_per_ray outside [1, 128];
+ * E_NOT_FOUND: no such object. */
 romap_status romap_render(romap_ctx* ctx, int32_t obj, const float T_wc[12], const romap_intrinsics* K,
                           int32_t samples_per_ray, float* rgb, float* depth, float* opacity, int32_t flags);
 
@@ -296,13 +298,19 @@ romap_status romap_async_offer(romap_ctx* ctx, int32_t obj, const uint8_t* rgb, 
 romap_status romap_async_stop(romap_ctx* ctx, int32_t finish_pending, romap_async_stats* out);
 
 /* Render several objects (R20): per ray, intersect every box, sort the hit segments
- * by t_near, composite each segment's (C, A, D) front to back. */
+ * by t_near (tie: smaller object id), composite each segment's (C, A, D) front to
+ * back over black.  Outputs as romap_render.  The objects may differ in model
+ * configuration (one forward launch per configuration).  E_INVALID: empty or
+ * duplicate object list, more than 8192 objects, bad pose / intrinsics,
+ * samples_per_segment outside [1, 128]; E_NOT_FOUND: an unknown object. */
 romap_status romap_render_scene(romap_ctx* ctx, const int32_t* objs, int32_t n, const float T_wc[12],
                                 const romap_intrinsics* K, int32_t samples_per_segment, float* rgb, float* depth,
                                 float* opacity, int32_t flags);
 
 /* Density at object-frame points (m) for marching cubes:
- * xyz float [n][3] -> sigma float [n]; 0 outside the box (R21). */
+ * xyz float [n][3] -> sigma float [n] (1/m); 0 outside the box (R21); n = 0 is a
+ * no-op.  Host buffers, or device buffers with ROMAP_DEVICE_PTRS.  E_INVALID: n < 0
+ * or a null buffer with n > 0; E_NOT_FOUND: no such object. */
 romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, int64_t n, float* sigma,
                                  int32_t flags);
 
