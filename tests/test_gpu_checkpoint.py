@@ -19,18 +19,26 @@ CFG = dict(levels=8, log2_T=12, base_res=16, finest_res=2048.0, res_cap=128, sam
 BLOCKS = (R.BLOCK_TABLE, R.BLOCK_MLP, R.BLOCK_M_TABLE, R.BLOCK_M_MLP, R.BLOCK_V_TABLE, R.BLOCK_V_MLP, R.BLOCK_STEP)
 
 
-def test_save_load_resume_bitwise(tmp_path):
+VARIANTS = {"mixed": {}, "fp32": dict(precision=0), "paper net, 2 layers": dict(network=1, hidden_layers=2),
+            "softplus, obj_bg=1": dict(density_act=1, obj_bg=1, lambda_density=0.03)}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_save_load_resume_bitwise(tmp_path, variant):
     sc = scenes.sphere_scene(0, n_views=8, depth_per_view=2)
     ob = sc.objects[0]
     a = R.Context(0)
     a.set_deterministic(True)
-    h = a.create_object(ob.t, ob.yaw, ob.a, R.model_config(**CFG), ob.instance_id, obj_id=41)
+    h = a.create_object(ob.t, ob.yaw, ob.a, R.model_config(**dict(CFG, **VARIANTS[variant])), ob.instance_id,
+                        obj_id=41)
     for fr in sc.frames[:6]:
         a.add_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K, fr.depth.get(ob.instance_id))
     fr = sc.frames[6]
     acc, _ = a.offer_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K, alpha_deg=1.0, iters_per_update=77)
     assert acc
     a.train_step([h], 20)
+    a.set_box(h, [ob.t[0] + 0.01, ob.t[1], ob.t[2]], ob.yaw + 0.02, [x * 1.05 for x in ob.a])   # R27: the box round-trips
+    a.train_step([h], 3)
     path = str(tmp_path / "obj41.romap")
     a.save_object(h, path)
     b = R.Context(0)
