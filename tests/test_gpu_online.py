@@ -140,3 +140,46 @@ def test_all_rays_miss_after_box_moves_away():
     Wo = np.concatenate([w.reshape(-1) for w in st.params["W"]])
     assert norm_rel(W, Wo) < 5e-2                                      # momentum steps as the oracle
     c.close()
+
+
+def test_scheduler_with_two_model_configurations():
+    """R25 scheduler over objects of different model configurations (one batched
+    train_step per configuration per round, the round length n = min(chunk,
+    smallest pending) over ALL objects with budget): per-object iteration counts and
+    Adam steps follow the oracle's schedule, and each object trained in its group
+    equals the same object trained alone (deterministic mode, bitwise)."""
+    sc = scenes.room_scene(7, n_objects=3, n_frames=24, W=160, H=120, f=131.25, room_half=1.5)
+    cfgs = [dict(CFG), dict(CFG), dict(CFG, seed=9, precision=0)]     # groups {0, 1} and {2}
+    budgets = [130, 70, 100]
+
+    def setup(c, ks):
+        hs = {}
+        for k in ks:
+            ob = sc.objects[k]
+            h = c.create_object(ob.t, ob.yaw, ob.a, R.model_config(**cfgs[k]), ob.instance_id, obj_id=700 + k)
+            fr = [f for f in sc.frames if (f.mask == ob.instance_id).any()][0]
+            acc, _ = c.offer_observation(h, fr.rgb, fr.mask, fr.T_wc, fr.K, iters_per_update=budgets[k])
+            assert acc
+            hs[k] = h
+        return hs
+
+    c = R.Context(0)
+    c.set_deterministic(True)
+    hs = setup(c, range(3))
+    batches, rest = O.schedule_budgets({hs[k]: budgets[k] for k in range(3)}, chunk=40, max_iters=1000)
+    ran = c.train_pending(chunk=40)
+    assert ran == {hs[k]: budgets[k] for k in range(3)} and all(v == 0 for v in rest.values())
+    assert len(batches) > 2
+    got = {k: (c.get_params(hs[k], R.BLOCK_TABLE).copy(), int(c.get_params(hs[k], R.BLOCK_STEP)[0])) for k in range(3)}
+    c.close()
+    for k in range(3):
+        assert got[k][1] == budgets[k]
+        # alone: the same iterations in the same chunk lengths as the schedule gave it
+        a = R.Context(0)
+        a.set_deterministic(True)
+        h = setup(a, [k])[k]
+        for objs, n in batches:
+            if hs[k] in objs:
+                a.train_step([h], n)
+        assert np.array_equal(a.get_params(h, R.BLOCK_TABLE).view(np.uint32), got[k][0].view(np.uint32)), k
+        a.close()
