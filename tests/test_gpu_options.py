@@ -68,3 +68,35 @@ def test_mixed_options(scene0, name):
     assert norm_rel(gt, g["table"]) < 2e-2, name
     for a, b in _blocks(gm, g["W"]):
         assert norm_rel(a, b) < 2e-2, name
+
+
+DEGENERATE = {
+    "N=1": dict(samples_per_ray=1),
+    "N=2": dict(samples_per_ray=2),
+    "one level": dict(levels=1, finest_res=16.0),
+    "T=2^4 (every level hashed into 16 entries)": dict(log2_T=4),
+    "b=1 (all levels at res 16)": dict(levels=4, finest_res=16.0),
+}
+
+
+@pytest.mark.parametrize("name", list(DEGENERATE))
+def test_fp32_degenerate_configurations(scene0, name):
+    """the method's degenerate cases (one sample per ray: delta = the whole segment;
+    one level; a table smaller than every level; a growth factor of 1) keep the fp32
+    parity bar, including bit-exact hash indices"""
+    kw = dict(CFG0, precision=0, **DEGENERATE[name])
+    c = R.Context(0)
+    h, st = make_pair(R, c, scene0, kw)
+    stats = c.forward_backward([h])[0]
+    L, g, dbg = O.loss_and_grads(st, 1)
+    for k in ("l_rgb", "l_rr", "l_depth", "l_density", "l_total"):
+        assert abs(stats[k] - L[k]) <= 1e-5 * max(abs(L[k]), 1e-6), (name, k, stats[k], L[k])
+    rs = dbg["rays"]
+    N = kw["samples_per_ray"]
+    hi = c.debug_dump(h, R.DUMP_HASH_IDX).reshape(rs["R"], N, kw["levels"], 8)
+    assert np.array_equal(hi[rs["hit"]].reshape(-1, kw["levels"], 8), dbg["idx"])
+    gt = c.get_params(h, R.BLOCK_GRAD_TABLE).reshape(-1, 2)
+    assert norm_rel(gt, g["table"]) < 1e-4, name
+    for a, b in _blocks(c.get_params(h, R.BLOCK_GRAD_MLP), g["W"]):
+        assert norm_rel(a, b) < 1e-4, name
+    c.close()
