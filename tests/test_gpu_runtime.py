@@ -69,3 +69,20 @@ def test_profiler_and_l2_flush_change_no_result():
     assert p0["l2_flush"]["launches"] == 0 and p0["fused_mixed"]["launches"] == 5
     # without per-stage events the 5 iterations replay a graph chunk
     assert p0["graph_replay"]["launches"] >= 1 and p1["graph_replay"]["launches"] == 0
+
+
+def test_query_density_device_pointers_equal_host():
+    """ROMAP_DEVICE_PTRS: a CUDA tensor in, a CUDA tensor out, in stream order on
+    the context's stream -- bitwise the host-buffer result (both paths)"""
+    import torch
+    sc = scenes.sphere_scene(0)
+    g = np.random.default_rng(4)
+    pts = g.uniform(-0.6, 0.6, (70001, 3)).astype(np.float32)      # ragged last tile, points outside the box
+    for precision in (0, 1):
+        c = R.Context(0)
+        h, _ = make_pair(R, c, sc, dict(CFG0M, precision=precision))
+        host = c.query_density(h, pts)
+        dev = c.query_density(h, torch.from_numpy(pts).cuda()).cpu().numpy()
+        assert np.array_equal(host.view(np.uint32), dev.view(np.uint32)), precision
+        assert (host == 0).any() and (host > 0).any()
+        c.close()
