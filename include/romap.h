@@ -320,7 +320,8 @@ romap_status romap_query_density(romap_ctx* ctx, int32_t obj, const float* xyz, 
  * sigma_iso (1/m).  Writes the triangles (9 floats each: 3 vertices x (x, y, z),
  * WORLD frame, m) in the deterministic cell / tetrahedron order to tris (host, or
  * device with ROMAP_DEVICE_PTRS) when they fit in cap_tris; *n_tris = triangle
- * count either way (call with cap_tris = 0 to size the buffer).  1 <= res <= 1024.
+ * count either way (call with cap_tris = 0 to size the buffer).  1 <= res <= 512
+ * (E_INVALID otherwise: 12 triangles per cell at most keep the int32 offsets exact).
  * flags & ROMAP_MESH_CARVE: before extraction, sigma := 0 at vertices that lie in
  * front of no keyframe camera inside its detection box (R26; E_STATE without
  * keyframes). */

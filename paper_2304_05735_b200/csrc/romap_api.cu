@@ -1748,7 +1748,9 @@ romap_status romap_extract_mesh(romap_ctx* ctx, int32_t obj, int32_t res, float 
     CHECK_CTX();
     Object* ob = find(ctx, obj);
     if (!ob) return fail(ROMAP_E_NOT_FOUND, "no object %d", obj);
-    if (res < 1 || res > 1024 || !n_tris || cap_tris < 0 || (cap_tris > 0 && !tris))
+    // res <= 512: at most 12 triangles per cell, so every count and offset of the
+    // int32 scan stays below 2^31 (12 x 512^3 = 1.6e9)
+    if (res < 1 || res > 512 || !n_tris || cap_tris < 0 || (cap_tris > 0 && !tris))
         return fail(ROMAP_E_INVALID, "bad mesh arguments");
     const long long n1 = res + 1, nv = n1 * n1 * n1, nc = (long long)res * res * res;
     const size_t scan_bytes = mt_scan_bytes(nc);

@@ -32,6 +32,9 @@ def test_mesh_matches_oracle_on_same_lattice(precision):
     assert T.shape == To.shape and T.shape[0] > 100
     assert np.abs(T - To).max() < 1e-5
     assert c.extract_mesh(h, res, float(sig.max()) + 1.0).shape[0] == 0          # nothing above the maximum
+    for bad in (0, 513):                                                         # the lattice limits
+        with pytest.raises(R.RomapError):
+            c.extract_mesh(h, bad, iso)
     c.close()
 
 
