@@ -793,21 +793,26 @@ def run_cfg2(args, ctx, R, torch, precision):
     for h in hs:
         ctx.destroy_object(h)
     hs = setup()
+    # the workload is the whole 300-iteration schedule (6 append batches), whatever --steps says
+    steps = max(args.steps, CONFIG_ITERS["cfg2"])
     sampler, spath = start_clock_sampler(visible_index(0))
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0 = ctx.profile_read()                           # launch counters are always kept
     torch.cuda.synchronize()
     e0.record()
-    samples, append_s = run(hs, args.steps, True)
+    samples, append_s = run(hs, steps, True)
     e1.record()
     torch.cuda.synchronize()
     clocks = stop_clock_sampler(sampler, spath)
+    p1 = ctx.profile_read()
+    launches = sum(p1[k]["launches"] - p0[k]["launches"] for k in p1 if k not in ("l2_flush", "graph_replay"))
     ms = e0.elapsed_time(e1)
     value = samples / (ms * 1e-3)
-    t_iter_obj_ms = ms / args.steps / len(hs)
+    t_iter_obj_ms = ms / steps / len(hs)
     print(json.dumps({
         "metric": "NeRF train ray-samples/s", "value": value, "unit": "ray-samples/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f16-mma/f32" if precision == 1 else "f32",
         "data": "synthetic room (seed 2): 8 cfg1-family objects, edges U(0.2, 1.5) m, 200-frame 640x480 trajectory",
         "config": {"workload": "cfg2: 8 objects batched in one launch, rays split by keyframe mask area "
@@ -819,7 +824,10 @@ def run_cfg2(args, ctx, R, torch, precision):
         "s_to_budget_per_object": {"config_iterations": 300, "s_config": t_iter_obj_ms * 300 / 1e3,
                                    "s_paper_budget": t_iter_obj_ms * PAPER_ITERS_TO_BUDGET / 1e3, "paper_s": 2.0},
         "ms_per_iteration_per_object": t_iter_obj_ms,
-        "clocks": clocks, "cpu_baseline": None, "e2e": None, "gpu_launches": None}), flush=True)
+        "clocks": clocks, "cpu_baseline": None,
+        "e2e": None, "e2e_note": "the timed region is itself end to end: host keyframe appends (add_observation from "
+                                 "host buffers) and per-call statistics read-backs are inside it",
+        "gpu_launches": launches}), flush=True)
     ctx.close()
     return 0
 

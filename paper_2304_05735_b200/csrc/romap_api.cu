@@ -1041,11 +1041,13 @@ static romap_status run_iterations(romap_ctx* ctx, Batch& b, int n_iters, bool a
     if (dirty) STAGE(ST_ZERO_GRADS, launch_zero_grads(lc, b.cfg, ctx->objdev_d, n));
     const size_t S = (size_t)b.total_slots * b.cfg.N;
     // mixed path: rays and sample records of up to K iterations are generated by
-    // one k_raygen + k_samples pair (slices k = it % K), ~64 MB of records at most
+    // one k_raygen + k_samples pair (slices k = it % K), ~768 MB of records at most
+    // (so multi-object batches -- 45 MB per iteration for cfg2, 180 MB for cfg3 --
+    // also replay graph chunks of several iterations)
     int K = 1;
     if (b.mixed) {
         const size_t per_iter = (size_t)b.total_slots * sizeof(RayRec) + S * 5 * sizeof(float);
-        const int Kmax = (int)std::max<size_t>(1, std::min<size_t>(16, (64u << 20) / per_iter));
+        const int Kmax = (int)std::max<size_t>(1, std::min<size_t>(16, ((size_t)768 << 20) / per_iter));
         // capacity for Kmax slices on first use, whatever n_iters is: a later call
         // with more iterations never reallocates (cudaFree synchronises the device)
         if (!grow(ctx, ctx->rays, ctx->rays_cap, (size_t)Kmax * b.total_slots))
