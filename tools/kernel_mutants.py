@@ -8,8 +8,8 @@ paper_2304_05735_b200/mutants/libromap_<k>.so; `run` (on the GPU box) runs the
 whole GPU suite against each library via ROMAP_LIB and lists the tests that
 failed (a mutant is killed when at least one does).  Results: profiles/r2_kernel_mutants.txt, DESIGN.md section 4.
 
-    python tools/kernel_mutants.py build        # here (CPU), after `make` in csrc/
-    python tools/kernel_mutants.py run          # on the GPU box
+    python tools/kernel_mutants.py build [k0]   # here (CPU), after `make` in csrc/ (mutants k0..)
+    python tools/kernel_mutants.py run [k0]     # on the GPU box
 """
 import concurrent.futures
 import os
@@ -69,6 +69,24 @@ MUTANTS = [
      "rr.bg[k] = u32_unit(rng_u32(pre, r, 2 + k));", ["k_sample.o"]),
     ("raygen pixel centre dropped", "romap_internal.cuh", "float pxf = __fadd_rn((float)px, 0.5f);",
      "float pxf = (float)px;", ALL),
+    # the other rows: slab, fp32 path, inference, scene compositing, mesh, deterministic reductions
+    ("slab t_near not clamped at 0", "romap_internal.cuh", "    tn = 0.0f;\n", "    tn = -3.0e38f;\n", ALL),
+    ("fp32 backward: ReLU mask of g1 dropped", "k_fp32.cu", "dg1[k] = v64[k] > 0.f ? acc : 0.f;", "dg1[k] = acc;",
+     ["k_fp32.o"]),
+    ("density query: outside-box zero dropped", "k_infer_mixed.cu",
+     "if (valid) out[p] = inside ? density_act(raw0, cfg.density_act) : 0.f;",
+     "if (valid) out[p] = density_act(raw0, cfg.density_act);", ["k_infer_mixed.o"]),
+    ("mixed render: midpoints at 1/4 of the stratum", "k_infer_mixed.cu", "dist = sample_dist(rr.tn, Dl, i, 0.5f);",
+     "dist = sample_dist(rr.tn, Dl, i, 0.25f);", ["k_infer_mixed.o"]),
+    ("render_scene: transmittance not carried", "k_scene.cu", "T *= 1.0f - segA[best];", "T *= 1.0f;",
+     ["k_scene.o"]),
+    ("marching tetrahedra: edge weight reversed", "k_mesh.cu", "const float w = (iso - sa) / (sb - sa);",
+     "const float w = (sb - iso) / (sb - sa);", ["k_mesh.o"]),
+    ("deterministic mode: first record of a run skipped", "k_det.cu",
+     "for (long long j = i; j < n && key[j] == k; ++j) {", "for (long long j = i + 1; j < n && key[j] == k; ++j) {",
+     ["k_det.o"]),
+    ("deterministic mode: first tile's dW skipped", "k_det.cu", "for (long long t = t0; t < t1; ++t) s +=",
+     "for (long long t = t0 + 1; t < t1; ++t) s +=", ["k_det.o"]),
 ]
 
 
@@ -101,18 +119,20 @@ def _build_one(k):
         shutil.rmtree(tmp, ignore_errors=True)
 
 
-def build():
+def build(start=0):
     missing = [o for o in OBJS if not os.path.exists(os.path.join(CSRC, o))]
     if missing:
         sys.exit(f"build the tree first (make in {CSRC}); missing {missing}")
     with concurrent.futures.ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1))) as ex:
-        for k, status in ex.map(_build_one, range(len(MUTANTS))):
+        for k, status in ex.map(_build_one, range(start, len(MUTANTS))):
             print(f"{k:02d} {MUTANTS[k][0]}: {status}", flush=True)
 
 
-def run():
+def run(start=0):
     print("mutant | GPU tests failed (of the whole suite) | rc, pytest summary", flush=True)
     for k, m in enumerate(MUTANTS):
+        if k < start:
+            continue
         lib = os.path.join(OUT, f"libromap_{k:02d}.so")
         env = dict(os.environ, ROMAP_LIB=lib)
         r = subprocess.run(["timeout", "900", sys.executable, "-m", "pytest", "tests", "-m", "gpu", "-q", "-rfE",
@@ -126,4 +146,4 @@ def run():
 
 
 if __name__ == "__main__":
-    {"build": build, "run": run}[sys.argv[1]]()
+    {"build": build, "run": run}[sys.argv[1]](int(sys.argv[2]) if len(sys.argv) > 2 else 0)
